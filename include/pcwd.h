@@ -1,0 +1,146 @@
+/* pcwd.h — C ABI of the B200 product-convolution wavelet decomposition library (libpcwd.so).
+ *
+ * What it computes (PAPER.md arxiv 2005.09870):
+ *   H f = Σ_{k=1..m} u_k ⋆ (v_k ⊙ f)                        Eq. (2)
+ *   Θ = Ψ* H Ψ,  Θ[μ][λ] := θ[λ,μ] = <H ψ_λ, ψ_μ>             P:43, P:176 (R1)
+ * in the periodic orthogonal wavelet basis of P:93-127 (depth J, filter h, g from P:100),
+ * restricted to a retained index set (R14-R16).  This is the exact form of
+ * Algorithm 1: A_k's circulant sub-band generators in spatial form
+ * (Lemma 1) times B_k by the sparse cascade (Lemma 6), the
+ * k-sum taken before the cascade; no truncation of A_k.
+ *
+ * Work unit: one test wavelet μ; the library produces row μ of Θ (all retained λ) as CSR.
+ * Units are Λ indices (layout: coarse block, then levels J..1, orientations (0,1),(1,0),
+ * (1,1), positions row-major — DESIGN.md R2/R3).  A handle owns the contiguous shard
+ * [row0, row1) of units chosen by (rank, world) with a cost-balanced split.
+ *
+ * Conventions
+ *   - All functions return a pcwd_status; pcwd_error_string() names it.  No global state:
+ *     handles are independent; one handle must not be used from two threads at once.
+ *   - "host or device" pointers are classified with cudaPointerGetAttributes.
+ *   - Streams are passed as void* (a cudaStream_t; NULL = legacy default stream).
+ *   - Nothing here blocks on the GPU unless stated ("synchronous").
+ */
+#ifndef PCWD_H
+#define PCWD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PCWD_OK = 0,
+  PCWD_E_SHAPE = 1,   /* d ∉ {1,2}, n not a power of two, n < 2  */
+  PCWD_E_CONFIG = 2,  /* levels ∉ [1, log2 n], filter length odd / < 2 / > 20  */
+  PCWD_E_PARAM = 3,   /* NULL pointer, m < 1, τ ≤ 0, L < 1 or L > N, rank ∉ [0, world) */
+  PCWD_E_CUDA = 4,    /* a CUDA runtime call failed (message: pcwd_last_error)        */
+  PCWD_E_OOM = 5,     /* device allocation failed                                     */
+  PCWD_E_STATE = 6,   /* call order violated (e.g. CSR requested before decompose)    */
+  PCWD_E_UNSUPPORTED = 7
+} pcwd_status;
+
+typedef enum { PCWD_F32 = 0, PCWD_F64 = 1 } pcwd_dtype;
+
+typedef enum {
+  PCWD_RETAIN_FULL = 0,       /* every (μ, λ): dense rows of length N, exact zeros kept (R14) */
+  PCWD_RETAIN_THRESHOLD = 1,  /* |Θ[μ][λ]| ≥ tau_rel · max|Θ|, decided in fp64 (R15)           */
+  PCWD_RETAIN_BAND = 2        /* exactly band_L partners per unit, scale/position key (R16)    */
+} pcwd_retain;
+
+typedef struct {
+  int32_t d;            /* dimension, 1 or 2  */
+  int32_t n;            /* side of the torus, power of two; N = n^d  */
+  int32_t levels;       /* J = number of analysis steps, 1 ≤ J ≤ log2 n              (R3)    */
+  int32_t filter_len;   /* 2δ, even, 2..20  */
+  const double* h;      /* HOST, filter_len taps of the low-pass filter; g from P:100        */
+  int32_t m;            /* number of product-convolution terms, ≥ 1  */
+  const double* u;      /* host or device, m × N row-major fp64: u_k(z) at index z mod n     */
+  const double* v;      /* host or device, m × N row-major fp64: v_k(y)                      */
+  int32_t dtype;        /* pcwd_dtype: arithmetic and output precision (threshold rule always
+                           decides and computes in fp64, values stored in dtype; R15)         */
+  int32_t retain;       /* pcwd_retain                                                        */
+  double tau_rel;       /* THRESHOLD: relative threshold τ_rel > 0                            */
+  int32_t band_L;       /* BAND: partners per unit, 1 ≤ L ≤ N                                 */
+  int32_t rank, world;  /* shard of units owned by this handle; world ≥ 1                    */
+  int32_t device;       /* CUDA device ordinal used by create                                */
+} pcwd_desc;
+
+typedef struct {
+  int64_t n_rows;       /* units in this shard (= row1 - row0)                                */
+  int64_t row0;         /* first global unit (Λ index) of the shard                           */
+  int64_t nnz;          /* retained entries in this shard                                      */
+  const int64_t* row_ptr;  /* DEVICE, n_rows + 1, row_ptr[0] = 0                              */
+  const int32_t* col;      /* DEVICE, nnz global λ indices, strictly increasing within a row */
+  const void* val;         /* DEVICE, nnz values of type dtype                                */
+  int32_t dtype;
+} pcwd_csr;
+
+typedef struct {
+  int64_t N, row0, row1, nnz;
+  double global_max;        /* THRESHOLD: M = max|Θ| used for τ (fp64); else 0               */
+  double fma_algorithmic;   /* algorithmic FMAs of one decompose over this shard */
+  double bytes_algorithmic; /* algorithmic HBM bytes (inputs + templates + CSR output)       */
+  int32_t kernel_launches;  /* kernels launched by the last pcwd_decompose                   */
+  int32_t compute_dtype;    /* precision the path computed in                                */
+} pcwd_info_t;
+
+/* Validate desc and build the handle: plan (sub-band table, windows, band stencil, shard),
+ * device buffers, copy of u and v cast to the compute precision.  Caller keeps ownership of
+ * every pointer in desc and may free them when this returns.  Synchronous. */
+int pcwd_create(const pcwd_desc* desc, void** out_handle);
+
+/* Compute the retained rows of this shard into handle-owned CSR (templates, k-sum, cascade,
+ * retention, compaction — all on the GPU).  Enqueued on `stream`.  THRESHOLD with world > 1
+ * needs the global max first: call pcwd_local_max, reduce over ranks, pcwd_set_global_max.
+ * The CSR stays valid until the next decompose or destroy.  Returns when the work is
+ * enqueued (THRESHOLD mode synchronises the stream once, to size the CSR). */
+int pcwd_decompose(void* handle, void* stream);
+
+/* THRESHOLD only: max|Θ[μ][·]| over this shard's units (fp64, synchronous). */
+int pcwd_local_max(void* handle, void* stream, double* out_max);
+/* THRESHOLD only: set M (e.g. the MAX all-reduce of pcwd_local_max over ranks). */
+int pcwd_set_global_max(void* handle, double M);
+
+/* Describe the CSR of the last decompose (device pointers owned by the handle). */
+int pcwd_get_csr(void* handle, pcwd_csr* out);
+/* Copy the CSR into caller buffers (host or device; sizes from pcwd_get_csr).  Any pointer
+ * may be NULL to skip that array.  Enqueued on stream. */
+int pcwd_copy_csr(void* handle, int64_t* row_ptr, int32_t* col, void* val, void* stream);
+
+/* y = Θ_ret x (transpose = 0: x has N entries, y has n_rows) or y = Θ_retᵀ x (transpose = 1:
+ * x has n_rows entries, y has N, overwritten).  x, y: DEVICE arrays of type dtype.
+ * This is the Θ_L z product of Eq. (7).  Enqueued on stream. */
+int pcwd_apply(void* handle, const void* x, void* y, int transpose, void* stream);
+
+int pcwd_info(void* handle, pcwd_info_t* out);
+
+/* Phase timing with CUDA events recorded on the decompose stream around each phase
+ * (enable = 1 before pcwd_decompose; read after the stream is synchronised).
+ * Phases: 0 = templates (a1), 1 = unit kernels (a2+a3+a4), 2 = everything else (fills, scans,
+ * threshold max/count passes).  out_ms[3] receives milliseconds of the last decompose;
+ * out_fma[3] the algorithmic FMAs of phases 0 and 1 (phase 2: 0). */
+int pcwd_profile(void* handle, int enable);
+int pcwd_phase_times(void* handle, double* out_ms, double* out_fma);
+int pcwd_destroy(void* handle);
+
+const char* pcwd_error_string(int code);
+/* Last error message of this thread (CUDA detail, failing argument). */
+const char* pcwd_last_error(void);
+
+/* ---- host-only plan queries (no GPU needed; used by the CPU tests) ---------------------- */
+int pcwd_validate(const pcwd_desc* desc);
+/* Shard [row0, row1) that (desc->rank, desc->world) would own. */
+int pcwd_plan_shard(const pcwd_desc* desc, int64_t* row0, int64_t* row1);
+/* BAND: the stencil of unit sub-band `sb` (Λ order index): band_L entries of
+ * (partner sub-band, offset o0, offset o1) in key order.  u and v may be NULL. */
+int pcwd_plan_stencil(const pcwd_desc* desc, int32_t sb, int32_t* out_sb, int32_t* out_o0,
+                      int32_t* out_o1);
+/* Number of sub-bands of the Λ layout. */
+int pcwd_plan_num_subbands(const pcwd_desc* desc, int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCWD_H */

@@ -1,0 +1,534 @@
+// api.cu — the C ABI of include/pcwd.h: handle lifetime, device buffers, launch sequencing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pcwd.h"
+#include "kernels.cuh"
+#include "plan.h"
+
+using namespace pcwd;
+
+static thread_local std::string g_err;
+
+namespace {
+
+constexpr size_t kSmemBudget = 200 * 1024;  // dynamic smem per CTA for in-smem units
+
+struct Launch {
+  int64_t u0, u1;
+  int grid;
+  size_t smem;      // 0 ⇒ global scratch
+};
+
+struct Handle {
+  pcwd_desc desc{};
+  HostPlan hp;
+  double* u_d = nullptr;
+  void* v_d = nullptr;
+  void* T_d = nullptr;
+  double* phi[2] = {nullptr, nullptr};
+  double* Ytmp = nullptr;
+  int4* stencil_d = nullptr;
+  void* gscratch = nullptr;
+  int64_t gstride = 0;
+  int ggrid = 0;
+  std::vector<Launch> launches;
+  int64_t* row_ptr = nullptr;
+  int32_t* col = nullptr;
+  void* val = nullptr;
+  int64_t nnz = 0, cap = 0;
+  double* unitmax = nullptr;
+  int32_t* cnt = nullptr;
+  int64_t* rowcnt = nullptr;
+  void* cubtmp = nullptr;
+  size_t cubbytes = 0;
+  double* dmax = nullptr;
+  double M = 0.0;
+  bool M_set = false, tmpl_fresh = false, decomposed = false;
+  int nlaunch = 0;
+  bool profile = false;
+  cudaEvent_t ev[8] = {};
+  int64_t rows() const { return hp.row1 - hp.row0; }
+};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) {                                                                      \
+      return fail(e_ == cudaErrorMemoryAllocation ? PCWD_E_OOM : PCWD_E_CUDA,                     \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                            \
+    }                                                                                             \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void free_all(Handle* h) {
+  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->gscratch,
+                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t bytes) {
+  return cudaMalloc(reinterpret_cast<void**>(p), bytes < 16 ? 16 : bytes);
+}
+
+// Templates T_{k,s} for every sub-band (a1).
+int build_templates(Handle* h, cudaStream_t st) {
+  const Plan& P = h->hp.P;
+  const HostPlan& hp = h->hp;
+  CK(launch_phi0(P, h->u_d, h->phi[0], hp.phiS[0][0], hp.phiW[0][0], hp.phiS[1][0], hp.phiW[1][0], st));
+  h->nlaunch++;
+  int cur = 0;
+  for (int lev = 1; lev <= P.J; ++lev) {
+    TmplArgs A{};
+    A.phi_in = h->phi[cur];
+    A.phi_out = h->phi[cur ^ 1];
+    A.Y = h->Ytmp;
+    A.T = h->T_d;
+    A.dil = 1 << (lev - 1);
+    for (int a = 0; a < 2; ++a) {
+      A.Sin[a] = hp.phiS[a][lev - 1];
+      A.Win[a] = hp.phiW[a][lev - 1];
+      A.Wout[a] = hp.phiW[a][lev];
+      A.Sout[a][0] = hp.phiS[a][lev];
+      A.Sout[a][1] = hp.psiS[a][lev];
+    }
+    for (int ec = 0; ec < 4; ++ec) A.toff[ec] = -1;
+    if (lev == P.J) A.toff[0] = P.sb[0].toff;
+    if (P.d == 2) {
+      for (int ec = 1; ec < 4; ++ec) A.toff[ec] = P.sb[sb_index(2, P.J, lev, ec)].toff;
+    } else {
+      A.toff[1] = P.sb[sb_index(1, P.J, lev, 1)].toff;
+    }
+    A.tstride = int64_t(A.Wout[0]) * A.Wout[1];
+    CK(launch_tmpl_level(P, A, hp.real_bytes, lev, st));
+    h->nlaunch += P.d == 2 ? 2 : 1;
+    cur ^= 1;
+  }
+  return PCWD_OK;
+}
+
+int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
+  const Plan& P = h->hp.P;
+  for (const Launch& L : h->launches) {
+    UnitArgs A{};
+    A.v = h->v_d;
+    A.T = h->T_d;
+    A.stencil = h->stencil_d;
+    A.gscratch = h->gscratch;
+    A.gscratch_stride = h->gstride;
+    A.u0 = L.u0;
+    A.u1 = L.u1;
+    A.row0 = h->hp.row0;
+    A.row_ptr = h->row_ptr;
+    A.col = h->col;
+    A.val = h->val;
+    A.unitmax = h->unitmax;
+    A.cnt = h->cnt;
+    A.tau = tau;
+    A.use_smem = L.smem > 0;
+    CK(launch_units(P, A, mode, h->hp.real_bytes, h->hp.out_bytes, L.grid, L.smem, st));
+    h->nlaunch++;
+  }
+  return PCWD_OK;
+}
+
+int local_max_impl(Handle* h, cudaStream_t st, double* out) {
+  int rc = build_templates(h, st);
+  if (rc) return rc;
+  rc = run_units(h, MODE_TMAX, st, 0.0);
+  if (rc) return rc;
+  CK(launch_max_reduce(h->unitmax, h->rows(), h->dmax, st));
+  h->nlaunch++;
+  CK(cudaMemcpyAsync(out, h->dmax, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->tmpl_fresh = true;
+  return PCWD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pcwd_error_string(int code) {
+  switch (code) {
+    case PCWD_OK: return "ok";
+    case PCWD_E_SHAPE: return "shape error (d, n)";
+    case PCWD_E_CONFIG: return "configuration error (levels, filter length)";
+    case PCWD_E_PARAM: return "parameter error";
+    case PCWD_E_CUDA: return "CUDA error";
+    case PCWD_E_OOM: return "out of device memory";
+    case PCWD_E_STATE: return "invalid call order";
+    case PCWD_E_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+const char* pcwd_last_error(void) { return g_err.c_str(); }
+
+int pcwd_validate(const pcwd_desc* desc) {
+  std::string msg;
+  int rc = validate_desc(desc, &msg);
+  if (rc) g_err = msg;
+  return rc;
+}
+
+int pcwd_plan_shard(const pcwd_desc* desc, int64_t* row0, int64_t* row1) {
+  HostPlan hp;
+  std::string msg;
+  int rc = build_plan(desc, desc ? desc->u : nullptr, &hp, &msg);
+  if (rc) return fail(rc, msg);
+  *row0 = hp.row0;
+  *row1 = hp.row1;
+  return PCWD_OK;
+}
+
+int pcwd_plan_num_subbands(const pcwd_desc* desc, int32_t* out) {
+  std::string msg;
+  int rc = validate_desc(desc, &msg);
+  if (rc) return fail(rc, msg);
+  *out = 1 + desc->levels * (desc->d == 2 ? 3 : 1);
+  return PCWD_OK;
+}
+
+int pcwd_plan_stencil(const pcwd_desc* desc, int32_t sb, int32_t* out_sb, int32_t* out_o0, int32_t* out_o1) {
+  if (!desc || desc->retain != PCWD_RETAIN_BAND) return fail(PCWD_E_PARAM, "stencil needs BAND retention");
+  HostPlan hp;
+  std::string msg;
+  int rc = build_plan(desc, nullptr, &hp, &msg);
+  if (rc) return fail(rc, msg);
+  if (sb < 0 || sb >= hp.P.nsb) return fail(PCWD_E_PARAM, "sub-band index out of range");
+  const int L = hp.P.band_L;
+  for (int j = 0; j < L; ++j) {
+    const Stencil& s = hp.stencil[hp.P.sb[sb].stencil_off + j];
+    out_sb[j] = s.sb;
+    out_o0[j] = s.o0;
+    out_o1[j] = s.o1;
+  }
+  return PCWD_OK;
+}
+
+int pcwd_create(const pcwd_desc* desc, void** out_handle) {
+  if (!out_handle) return fail(PCWD_E_PARAM, "out_handle is NULL");
+  *out_handle = nullptr;
+  std::string msg;
+  int rc = validate_desc(desc, &msg);
+  if (rc) return fail(rc, msg);
+  if (!desc->u || !desc->v) return fail(PCWD_E_PARAM, "u or v is NULL");
+  CK(cudaSetDevice(desc->device));
+  const int64_t N = desc->d == 2 ? int64_t(desc->n) * desc->n : desc->n;
+  const int64_t mN = int64_t(desc->m) * N;
+  const bool u_dev = is_device_ptr(desc->u), v_dev = is_device_ptr(desc->v);
+  std::vector<double> u_host;
+  const double* uh = desc->u;
+  if (u_dev) {
+    u_host.resize(mN);
+    CK(cudaMemcpy(u_host.data(), desc->u, mN * sizeof(double), cudaMemcpyDeviceToHost));
+    uh = u_host.data();
+  }
+  Handle* h = new Handle();
+  h->desc = *desc;
+  rc = build_plan(desc, uh, &h->hp, &msg);
+  if (rc) { delete h; return fail(rc, msg); }
+  const Plan& P = h->hp.P;
+  const int rb = h->hp.real_bytes, ob = h->hp.out_bytes;
+  auto bail = [&](int code, const std::string& m) { free_all(h); delete h; return fail(code, m); };
+#define CKB(call)                                                                                  \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return bail(e_ == cudaErrorMemoryAllocation ? PCWD_E_OOM : PCWD_E_CUDA,                      \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                             \
+  } while (0)
+
+  // inputs: u in fp64 (template build), v in the compute type (host → device boundary)
+  CKB(dalloc(&h->u_d, mN * sizeof(double)));
+  CKB(cudaMemcpy(h->u_d, desc->u, mN * sizeof(double), u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  CKB(dalloc(&h->v_d, mN * rb));
+  if (rb == 8) {
+    CKB(cudaMemcpy(h->v_d, desc->v, mN * sizeof(double), v_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+  } else {
+    double* tmp = nullptr;
+    CKB(dalloc(&tmp, mN * sizeof(double)));
+    CKB(cudaMemcpy(tmp, desc->v, mN * sizeof(double), v_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    CKB(launch_cast(tmp, h->v_d, mN, 4, 0));
+    CKB(cudaDeviceSynchronize());
+    cudaFree(tmp);
+  }
+  CKB(dalloc(&h->T_d, std::max<int64_t>(h->hp.tmpl_elems, 1) * rb));
+  CKB(dalloc(&h->phi[0], int64_t(P.m) * h->hp.phi_elems * sizeof(double)));
+  CKB(dalloc(&h->phi[1], int64_t(P.m) * h->hp.phi_elems * sizeof(double)));
+  CKB(dalloc(&h->Ytmp, int64_t(P.m) * std::max<int64_t>(h->hp.y_elems, 1) * sizeof(double)));
+  if (!h->hp.stencil.empty()) {
+    std::vector<int4> st(h->hp.stencil.size());
+    for (size_t i = 0; i < st.size(); ++i)
+      st[i] = make_int4(h->hp.stencil[i].sb, h->hp.stencil[i].o0, h->hp.stencil[i].o1, 0);
+    CKB(dalloc(&h->stencil_d, st.size() * sizeof(int4)));
+    CKB(cudaMemcpy(h->stencil_d, st.data(), st.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  }
+
+  // launch plan: one launch per level inside the shard; in-smem when the unit scratch fits
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, desc->device);
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device);
+  const size_t budget = std::min<size_t>(kSmemBudget, size_t(smem_optin > 0 ? smem_optin : 48 * 1024) - 8 * 1024);
+  int64_t gmax = 0;
+  for (int s = 0; s < P.nsb;) {
+    int lev = P.sb[s].level;
+    int e = s;
+    int64_t scr = 0;
+    while (e < P.nsb && P.sb[e].level == lev) { scr = std::max(scr, P.sb[e].scratch); ++e; }
+    int64_t u0 = std::max(h->hp.row0, P.sb[s].offset);
+    int64_t u1 = std::min(h->hp.row1, P.sb[e - 1].offset + P.sb[e - 1].count);
+    if (u1 > u0) {
+      size_t bytes = size_t(scr) * rb;
+      Launch L{u0, u1, 0, 0};
+      if (bytes <= budget) {
+        L.smem = std::max<size_t>(bytes, 16);
+        int per_sm = int(std::min<size_t>(8, (228 * 1024) / (L.smem + 2048)));
+        per_sm = std::max(per_sm, 1);
+        L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * per_sm));
+      } else {
+        L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * 2));
+        gmax = std::max(gmax, scr);
+        h->ggrid = std::max(h->ggrid, L.grid);
+      }
+      h->launches.push_back(L);
+    }
+    s = e;
+  }
+  if (gmax > 0) {
+    h->gstride = (gmax + 31) & ~int64_t(31);
+    CKB(dalloc(&h->gscratch, size_t(h->gstride) * h->ggrid * rb));
+  }
+
+  // output CSR
+  const int64_t rows = h->rows();
+  CKB(dalloc(&h->row_ptr, (rows + 1) * sizeof(int64_t)));
+  if (P.retain == PCWD_RETAIN_BAND) {
+    h->cap = h->nnz = rows * P.band_L;
+  } else if (P.retain == PCWD_RETAIN_FULL) {
+    h->cap = h->nnz = rows * P.N;
+  } else {
+    CKB(dalloc(&h->unitmax, std::max<int64_t>(rows, 1) * sizeof(double)));
+    CKB(dalloc(&h->cnt, std::max<int64_t>(rows * P.nsb, 1) * sizeof(int32_t)));
+    CKB(dalloc(&h->rowcnt, (rows + 1) * sizeof(int64_t)));
+    CKB(dalloc(&h->dmax, sizeof(double)));
+    size_t tb = 0;
+    CKB(exclusive_scan_i64(nullptr, nullptr, rows + 1, nullptr, &tb, 0));
+    h->cubbytes = tb;
+    CKB(dalloc(&h->cubtmp, tb));
+    h->cap = 0;
+  }
+  if (h->cap > 0) {
+    CKB(dalloc(&h->col, h->cap * sizeof(int32_t)));
+    CKB(dalloc(&h->val, h->cap * ob));
+  }
+  CKB(cudaDeviceSynchronize());
+#undef CKB
+  *out_handle = h;
+  return PCWD_OK;
+}
+
+int pcwd_local_max(void* handle, void* stream, double* out_max) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !out_max) return fail(PCWD_E_PARAM, "NULL argument");
+  if (h->hp.P.retain != PCWD_RETAIN_THRESHOLD) return fail(PCWD_E_STATE, "local_max needs THRESHOLD");
+  CK(cudaSetDevice(h->desc.device));
+  h->nlaunch = 0;
+  return local_max_impl(h, static_cast<cudaStream_t>(stream), out_max);
+}
+
+int pcwd_set_global_max(void* handle, double M) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(PCWD_E_PARAM, "NULL handle");
+  if (!(M >= 0.0)) return fail(PCWD_E_PARAM, "M must be >= 0");
+  h->M = M;
+  h->M_set = true;
+  return PCWD_OK;
+}
+
+int pcwd_decompose(void* handle, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(PCWD_E_PARAM, "NULL handle");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(h->desc.device));
+  const Plan& P = h->hp.P;
+  const int64_t rows = h->rows();
+  int rc;
+  if (P.retain != PCWD_RETAIN_THRESHOLD || !h->M_set) h->nlaunch = 0;
+  auto rec = [&](int i) { if (h->profile) cudaEventRecord(h->ev[i], st); };
+  if (P.retain == PCWD_RETAIN_BAND) {
+    rec(0);
+    if ((rc = build_templates(h, st))) return rc;
+    rec(1);
+    if ((rc = run_units(h, MODE_BAND, st, 0.0))) return rc;
+    rec(2);
+    CK(launch_fill_band_rowptr(h->row_ptr, rows, P.band_L, st));
+    h->nlaunch++;
+    rec(3);
+  } else if (P.retain == PCWD_RETAIN_FULL) {
+    rec(0);
+    if ((rc = build_templates(h, st))) return rc;
+    rec(1);
+    CK(cudaMemsetAsync(h->val, 0, size_t(h->cap) * h->hp.out_bytes, st));
+    CK(launch_fill_full(h->row_ptr, h->col, rows, P.N, st));
+    h->nlaunch++;
+    rec(2);
+    if ((rc = run_units(h, MODE_FULL, st, 0.0))) return rc;
+    rec(3);
+  } else {
+    if (!h->M_set) {
+      if (h->desc.world > 1) return fail(PCWD_E_STATE, "THRESHOLD with world > 1 needs pcwd_set_global_max");
+      double M = 0.0;
+      if ((rc = local_max_impl(h, st, &M))) return rc;
+      h->M = M;
+    } else if (!h->tmpl_fresh) {
+      if ((rc = build_templates(h, st))) return rc;
+    }
+    const double tau = h->desc.tau_rel * h->M;
+    CK(cudaMemsetAsync(h->cnt, 0, size_t(std::max<int64_t>(rows * P.nsb, 1)) * sizeof(int32_t), st));
+    if ((rc = run_units(h, MODE_TCOUNT, st, tau))) return rc;
+    CK(launch_row_counts(h->cnt, rows, P.nsb, h->rowcnt, st));
+    size_t tb = h->cubbytes;
+    CK(exclusive_scan_i64(h->rowcnt, h->row_ptr, rows + 1, h->cubtmp, &tb, st));
+    h->nlaunch += 2;
+    int64_t nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, h->row_ptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (nnz > h->cap) {
+      if (h->col) cudaFree(h->col);
+      if (h->val) cudaFree(h->val);
+      h->col = nullptr;
+      h->val = nullptr;
+      int64_t cap = nnz + nnz / 8 + 1024;
+      CK(dalloc(&h->col, cap * sizeof(int32_t)));
+      CK(dalloc(&h->val, cap * h->hp.out_bytes));
+      h->cap = cap;
+    }
+    h->nnz = nnz;
+    if ((rc = run_units(h, MODE_TWRITE, st, tau))) return rc;
+    h->M_set = false;
+    h->tmpl_fresh = false;
+  }
+  h->decomposed = true;
+  return PCWD_OK;
+}
+
+int pcwd_get_csr(void* handle, pcwd_csr* out) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !out) return fail(PCWD_E_PARAM, "NULL argument");
+  if (!h->decomposed) return fail(PCWD_E_STATE, "decompose first");
+  out->n_rows = h->rows();
+  out->row0 = h->hp.row0;
+  out->nnz = h->nnz;
+  out->row_ptr = h->row_ptr;
+  out->col = h->col;
+  out->val = h->val;
+  out->dtype = h->desc.dtype;
+  return PCWD_OK;
+}
+
+int pcwd_copy_csr(void* handle, int64_t* row_ptr, int32_t* col, void* val, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(PCWD_E_PARAM, "NULL handle");
+  if (!h->decomposed) return fail(PCWD_E_STATE, "decompose first");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(h->desc.device));
+  if (row_ptr) CK(cudaMemcpyAsync(row_ptr, h->row_ptr, (h->rows() + 1) * sizeof(int64_t), cudaMemcpyDefault, st));
+  if (col && h->nnz) CK(cudaMemcpyAsync(col, h->col, h->nnz * sizeof(int32_t), cudaMemcpyDefault, st));
+  if (val && h->nnz) CK(cudaMemcpyAsync(val, h->val, h->nnz * h->hp.out_bytes, cudaMemcpyDefault, st));
+  return PCWD_OK;
+}
+
+int pcwd_apply(void* handle, const void* x, void* y, int transpose, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !x || !y) return fail(PCWD_E_PARAM, "NULL argument");
+  if (!h->decomposed) return fail(PCWD_E_STATE, "decompose first");
+  CK(cudaSetDevice(h->desc.device));
+  CK(launch_spmv(h->row_ptr, h->col, h->val, x, y, h->rows(), h->hp.P.N, transpose, h->hp.out_bytes,
+                 static_cast<cudaStream_t>(stream)));
+  return PCWD_OK;
+}
+
+int pcwd_info(void* handle, pcwd_info_t* out) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !out) return fail(PCWD_E_PARAM, "NULL argument");
+  const Plan& P = h->hp.P;
+  out->N = P.N;
+  out->row0 = h->hp.row0;
+  out->row1 = h->hp.row1;
+  out->nnz = h->nnz;
+  out->global_max = h->M;
+  out->fma_algorithmic = h->hp.fma_shard;
+  const int rb = h->hp.real_bytes;
+  out->bytes_algorithmic = double(P.m) * P.N * rb + double(h->hp.tmpl_elems) * rb +
+                           double(h->nnz) * (4 + h->hp.out_bytes) + double(h->rows() + 1) * 8;
+  out->kernel_launches = h->nlaunch;
+  out->compute_dtype = rb == 8 ? PCWD_F64 : PCWD_F32;
+  return PCWD_OK;
+}
+
+int pcwd_profile(void* handle, int enable) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(PCWD_E_PARAM, "NULL handle");
+  CK(cudaSetDevice(h->desc.device));
+  if (enable && !h->ev[0])
+    for (auto& e : h->ev) CK(cudaEventCreate(&e));
+  h->profile = enable != 0;
+  return PCWD_OK;
+}
+
+int pcwd_phase_times(void* handle, double* out_ms, double* out_fma) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !out_ms || !out_fma) return fail(PCWD_E_PARAM, "NULL argument");
+  if (!h->profile || h->hp.P.retain == PCWD_RETAIN_THRESHOLD)
+    return fail(PCWD_E_STATE, "profiling not enabled (or THRESHOLD: not instrumented)");
+  float t[3] = {0, 0, 0};
+  CK(cudaEventElapsedTime(&t[0], h->ev[0], h->ev[1]));
+  if (h->hp.P.retain == PCWD_RETAIN_BAND) {
+    CK(cudaEventElapsedTime(&t[1], h->ev[1], h->ev[2]));
+    CK(cudaEventElapsedTime(&t[2], h->ev[2], h->ev[3]));
+  } else {
+    CK(cudaEventElapsedTime(&t[2], h->ev[1], h->ev[2]));
+    CK(cudaEventElapsedTime(&t[1], h->ev[2], h->ev[3]));
+  }
+  for (int i = 0; i < 3; ++i) out_ms[i] = t[i];
+  out_fma[0] = h->hp.fma_templates;
+  out_fma[1] = h->hp.fma_shard - h->hp.fma_templates;
+  out_fma[2] = 0.0;
+  return PCWD_OK;
+}
+
+int pcwd_destroy(void* handle) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return PCWD_OK;
+  cudaSetDevice(h->desc.device);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  free_all(h);
+  delete h;
+  return PCWD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,589 @@
+// kernels.cu — sm_100a kernels of the exact decomposition path.
+//
+//   a1  tmpl_*      T_{k,s} = ũ_k ⋆ ψ_{s,0} by the à-trous recursion (P:96 applied to ũ_k ⋆ φ):
+//                   T_φ^{(ℓ)}(y) = Σ_j f_0[j] T_φ^{(ℓ-1)}(y - 2^{ℓ-1} j), detail templates with f_1;
+//                   these are the spatial form of A_k's circulant sub-band generators (Lemma 1,
+//                   P:1157-1159).  fp64.
+//   a2  unit_kernel k-sum       R_μ(y) = Σ_k v_k(y) T_{k,s(μ)}(y - 2^ℓ p)   (B_k and A_kB_k of Alg. 1,
+//                   P:186-190, fused with the accumulation: Row μ of Σ_k A_k B_k is Ψ*(Σ_k v_k ⊙ τT_k))
+//   a3  unit_kernel cascade     c_μ = Ψ* R_μ on the windows R_μ can reach (sparse cascade,
+//                   P:1266-1273, Lemma 6)
+//   a4/a5 unit_kernel emit      retained gather: full rows / band stencil / threshold max-count-write
+//
+// One CTA processes one unit at a time (grid-stride over units in Λ order, coarse and costly
+// first); its windows live in shared memory when they fit, else in a per-CTA global slice.
+#include <cub/cub.cuh>
+
+#include <climits>
+
+#include "kernels.cuh"
+
+namespace pcwd {
+
+constexpr int kBlock = 256;
+
+__device__ __forceinline__ float fmaT(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmaT(double a, double b, double c) { return fma(a, b, c); }
+
+// ============================================================================= templates (a1)
+
+__global__ void phi0_kernel(const __grid_constant__ Plan P, const double* __restrict__ u,
+                            double* __restrict__ phi0, int S0, int W0, int S1, int W1) {
+  const int mask = P.n - 1;
+  const int64_t total = int64_t(P.m) * W0 * W1;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    int64_t k = idx / (int64_t(W0) * W1);
+    int64_t r = idx - k * W0 * W1;
+    int i0 = int(r / W1), i1 = int(r - int64_t(i0) * W1);
+    int z0 = P.d == 2 ? ((-(S0 + i0)) & mask) : 0;   // ũ(y) = u(-y)
+    int z1 = (-(S1 + i1)) & mask;
+    phi0[idx] = u[k * P.N + int64_t(z0) * P.n + z1];
+  }
+}
+
+__device__ __forceinline__ double win_read(const double* buf, int y, int S, int W, int mask, int64_t stride) {
+  int li = (y - S) & mask;
+  return li < W ? buf[li * stride] : 0.0;
+}
+
+template <typename Real>
+__global__ void tmpl_passA(const __grid_constant__ Plan P, const __grid_constant__ TmplArgs A, int coarse_level,
+                           int level) {
+  // along axis 1: Y[k][e1][i0][j1] = Σ_j f_{e1}[j] φ(i0, y1 - dil (o_{e1} + j))
+  const int mask = P.n - 1;
+  const int Win0 = A.Win[0], Win1 = A.Win[1], Wout1 = A.Wout[1];
+  const int64_t total = int64_t(P.m) * 2 * Win0 * Wout1;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    int j1 = int(idx % Wout1);
+    int64_t t = idx / Wout1;
+    int i0 = int(t % Win0);
+    t /= Win0;
+    int e1 = int(t & 1);
+    int64_t k = t >> 1;
+    int y1 = (A.Sout[1][e1] + j1) & mask;
+    const double* line = A.phi_in + (k * Win0 + i0) * Win1;
+    double acc = 0.0;
+    for (int j = 0; j < P.L2; ++j)
+      acc = fma(P.td[e1][j], win_read(line, y1 - A.dil * (P.to[e1] + j), A.Sin[1], Win1, mask, 1), acc);
+    if (P.d == 2) {
+      A.Y[idx] = acc;
+    } else {  // d = 1: this is the output
+      Real* T = reinterpret_cast<Real*>(A.T);
+      if (e1 == 0) {
+        A.phi_out[k * Wout1 + j1] = acc;
+        if (level == coarse_level && A.toff[0] >= 0) T[A.toff[0] + k * A.tstride + j1] = Real(acc);
+      } else if (A.toff[1] >= 0) {
+        T[A.toff[1] + k * A.tstride + j1] = Real(acc);
+      }
+    }
+  }
+}
+
+template <typename Real>
+__global__ void tmpl_passB(const __grid_constant__ Plan P, const __grid_constant__ TmplArgs A, int coarse_level,
+                           int level) {
+  // along axis 0, d = 2 only: out[k][e0 e1][j0][j1] = Σ_j f_{e0}[j] Y[k][e1](y0 - dil (o_{e0} + j), j1)
+  const int mask = P.n - 1;
+  const int Win0 = A.Win[0], Wout0 = A.Wout[0], Wout1 = A.Wout[1];
+  const int64_t per = int64_t(Wout0) * Wout1;
+  const int64_t total = int64_t(P.m) * 4 * per;
+  Real* T = reinterpret_cast<Real*>(A.T);
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    int64_t r = idx % per;
+    int64_t t = idx / per;
+    int ec = int(t & 3);
+    int64_t k = t >> 2;
+    int e0 = ec >> 1, e1 = ec & 1;
+    int j0 = int(r / Wout1), j1 = int(r - int64_t(j0) * Wout1);
+    int y0 = (A.Sout[0][e0] + j0) & mask;
+    const double* col = A.Y + ((k * 2 + e1) * Win0) * Wout1 + j1;
+    double acc = 0.0;
+    for (int j = 0; j < P.L2; ++j)
+      acc = fma(P.td[e0][j], win_read(col, y0 - A.dil * (P.to[e0] + j), A.Sin[0], Win0, mask, Wout1), acc);
+    if (ec == 0) {
+      A.phi_out[k * per + r] = acc;
+      if (level == coarse_level && A.toff[0] >= 0) T[A.toff[0] + k * A.tstride + r] = Real(acc);
+    } else if (A.toff[ec] >= 0) {
+      T[A.toff[ec] + k * A.tstride + r] = Real(acc);
+    }
+  }
+}
+
+template <typename Real>
+__global__ void cast_kernel(const double* __restrict__ src, Real* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = Real(src[i]);
+}
+
+// ============================================================================= per-unit kernel (a2-a5)
+
+template <typename Real>
+struct OutWin {
+  const Real* buf;
+  Range r0, r1;
+  int sbi;
+};
+
+__device__ __forceinline__ double block_reduce_max(double x, double* red) {
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double y = threadIdx.x < kBlock / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) y = fmax(y, __shfl_xor_sync(0xffffffffu, y, o));
+    if (threadIdx.x == 0) red[0] = y;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+__device__ __forceinline__ int block_reduce_sum(int x, int* red) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int y = threadIdx.x < kBlock / 32 ? red[threadIdx.x] : 0;
+    for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+    if (threadIdx.x == 0) red[0] = y;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+template <typename Real, typename OutT, int D, int MODE>
+__global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Plan P,
+                                                      const __grid_constant__ UnitArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red_d[kBlock / 32];
+  __shared__ int red_i[kBlock / 32];
+  using BlockScan = cub::BlockScan<int, kBlock>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+
+  Real* scratch = A.use_smem ? reinterpret_cast<Real*>(smem_raw)
+                             : reinterpret_cast<Real*>(A.gscratch) + int64_t(blockIdx.x) * A.gscratch_stride;
+  const int tid = threadIdx.x;
+  const int n = P.n, mask = P.n - 1, L2 = P.L2;
+  const Real* __restrict__ v = reinterpret_cast<const Real*>(A.v);
+
+  for (int64_t unit = A.u0 + blockIdx.x; unit < A.u1; unit += gridDim.x) {
+    const int sbi = find_subband(P, unit);
+    const SubBand& S = P.sb[sbi];
+    const int64_t row = unit - A.row0;
+    const int64_t pos = unit - S.offset;
+    const int p0 = D == 2 ? int(pos / S.nl) : 0;
+    const int p1 = D == 2 ? int(pos - int64_t(p0) * S.nl) : int(pos);
+    const Range r0 = D == 2 ? unit_window(P, S, 0, p0) : Range{0, 1, 1};
+    const Range r1 = unit_window(P, S, 1, p1);
+    Real* X0 = scratch + S.offX0;
+    Real* X1 = scratch + S.offX1;
+    Real* Y = scratch + S.offY;
+    Real* Dd = scratch + S.offD;
+    Real* stage_val = scratch + S.offStage;
+    int* stage_col = reinterpret_cast<int*>(stage_val + P.band_Lpad);
+
+    // ---- a2: R_μ(y) = Σ_k v_k(y) T_k(y - 2^ℓ p) on the unit window
+    {
+      const Real* __restrict__ T = reinterpret_cast<const Real*>(A.T) + S.toff;
+      const bool f0 = D == 2 && S.tW[0] >= n;
+      const bool f1 = S.tW[1] >= n;
+      const int tw1 = f1 ? n : S.tW[1];
+      const int total = r0.len * r1.len;
+      for (int idx = tid; idx < total; idx += kBlock) {
+        const int i0 = idx / r1.len, i1 = idx - i0 * r1.len;
+        const int y0 = D == 2 ? ((r0.lo + i0) & mask) : 0;
+        const int y1 = (r1.lo + i1) & mask;
+        const int t0 = f0 ? ((y0 - (p0 << S.level)) & mask) : i0;
+        const int t1 = f1 ? ((y1 - (p1 << S.level)) & mask) : i1;
+        const int64_t vy = int64_t(y0) * n + y1;
+        const int64_t ti = int64_t(t0) * tw1 + t1;
+        Real acc = Real(0);
+        for (int k = 0; k < P.m; ++k) acc = fmaT(v[k * P.N + vy], T[k * S.tstride + ti], acc);
+        X0[idx] = acc;
+      }
+    }
+    if (MODE == MODE_BAND) {
+      for (int j = tid; j < P.band_Lpad; j += kBlock) { stage_col[j] = INT_MAX; stage_val[j] = Real(0); }
+    }
+    __syncthreads();
+
+    // ---- a3: windowed periodic cascade, steps 1..S.steps, emitting after each step
+    Real* cur = X0;
+    Real* nxt = X1;
+    Range in0 = r0, in1 = r1;
+    double tmax = 0.0;
+    for (int s = 1; s <= S.steps; ++s) {
+      const Range a0 = D == 2 ? step_out(in0, L2, 0) : Range{0, 1, 1};
+      const Range d0 = D == 2 ? step_out(in0, L2, 1) : Range{0, 1, 1};
+      const Range a1 = step_out(in1, L2, 0);
+      const Range d1 = step_out(in1, L2, 1);
+      int s01 = 0, s10 = 0;
+      if (D == 2) {
+        const int ycols = a1.len + d1.len;
+        const int totA = in0.len * ycols;
+        for (int idx = tid; idx < totA; idx += kBlock) {       // pass A: axis 1
+          const int i0 = idx / ycols, j = idx - i0 * ycols;
+          const int e1 = j >= a1.len;
+          const int jj = e1 ? j - a1.len : j;
+          const Range& R = e1 ? d1 : a1;
+          const int q = 2 * (R.lo + jj) + P.to[e1];
+          const Real* line = cur + i0 * in1.len;
+          Real acc = Real(0);
+#pragma unroll 4
+          for (int t = 0; t < L2; ++t) {
+            const int c = local_index(in1, q + t);
+            if (c >= 0) acc = fmaT(TapsOf<Real>::get(P, e1, t), line[c], acc);
+          }
+          Y[idx] = acc;
+        }
+        __syncthreads();
+        const int s00 = a0.len * a1.len;
+        s01 = a0.len * d1.len;
+        s10 = d0.len * a1.len;
+        const int s11 = d0.len * d1.len;
+        const int totB = s00 + s01 + s10 + s11;
+        for (int idx = tid; idx < totB; idx += kBlock) {       // pass B: axis 0
+          int e0, e1, j0, j1, rem;
+          Real* dst;
+          if (idx < s00) { e0 = 0; e1 = 0; rem = idx; j0 = rem / a1.len; j1 = rem - j0 * a1.len; dst = nxt + rem; }
+          else if (idx < s00 + s01) { e0 = 0; e1 = 1; rem = idx - s00; j0 = rem / d1.len; j1 = rem - j0 * d1.len; dst = Dd + rem; }
+          else if (idx < s00 + s01 + s10) { e0 = 1; e1 = 0; rem = idx - s00 - s01; j0 = rem / a1.len; j1 = rem - j0 * a1.len; dst = Dd + s01 + rem; }
+          else { e0 = 1; e1 = 1; rem = idx - s00 - s01 - s10; j0 = rem / d1.len; j1 = rem - j0 * d1.len; dst = Dd + s01 + s10 + rem; }
+          const Range& R = e0 ? d0 : a0;
+          const int q = 2 * (R.lo + j0) + P.to[e0];
+          const int colY = (e1 ? a1.len : 0) + j1;
+          Real acc = Real(0);
+#pragma unroll 4
+          for (int t = 0; t < L2; ++t) {
+            const int r = local_index(in0, q + t);
+            if (r >= 0) acc = fmaT(TapsOf<Real>::get(P, e0, t), Y[r * ycols + colY], acc);
+          }
+          *dst = acc;
+        }
+      } else {
+        const int tot = a1.len + d1.len;
+        for (int idx = tid; idx < tot; idx += kBlock) {
+          const int e1 = idx >= a1.len;
+          const int jj = e1 ? idx - a1.len : idx;
+          const Range& R = e1 ? d1 : a1;
+          const int q = 2 * (R.lo + jj) + P.to[e1];
+          Real acc = Real(0);
+          for (int t = 0; t < L2; ++t) {
+            const int c = local_index(in1, q + t);
+            if (c >= 0) acc = fmaT(TapsOf<Real>::get(P, e1, t), cur[c], acc);
+          }
+          if (e1) Dd[jj] = acc; else nxt[jj] = acc;
+        }
+      }
+      __syncthreads();
+
+      // ---- a4/a5: emit this step's sub-bands (and the coarse block at s == J)
+      OutWin<Real> w[4];
+      int nw = 0;
+      const int base_sb = 1 + (P.J - s) * (D == 2 ? 3 : 1);
+      if (D == 2) {
+        w[nw++] = OutWin<Real>{Dd, a0, d1, base_sb + 0};
+        w[nw++] = OutWin<Real>{Dd + s01, d0, a1, base_sb + 1};
+        w[nw++] = OutWin<Real>{Dd + s01 + s10, d0, d1, base_sb + 2};
+      } else {
+        w[nw++] = OutWin<Real>{Dd, Range{0, 1, 1}, d1, base_sb};
+      }
+      if (s == P.J) w[nw++] = OutWin<Real>{nxt, a0, a1, 0};
+
+      if (MODE == MODE_FULL) {
+        OutT* out = reinterpret_cast<OutT*>(A.val) + row * P.N;
+        for (int wi = 0; wi < nw; ++wi) {
+          const OutWin<Real>& W = w[wi];
+          const SubBand& L = P.sb[W.sbi];
+          const int tot = W.r0.len * W.r1.len;
+          for (int idx = tid; idx < tot; idx += kBlock) {
+            const int i0 = idx / W.r1.len, i1 = idx - i0 * W.r1.len;
+            const int g0 = (W.r0.lo + i0) & (W.r0.nl - 1);
+            const int g1 = (W.r1.lo + i1) & (W.r1.nl - 1);
+            out[L.offset + int64_t(g0) * L.nl + g1] = OutT(W.buf[idx]);
+          }
+        }
+      } else if (MODE == MODE_BAND) {
+        const int4* st = A.stencil + S.stencil_off;
+        for (int j = tid; j < P.band_L; j += kBlock) {
+          const int4 e = st[j];
+          const SubBand& L = P.sb[e.x];
+          if (L.level != s || (e.x == 0 && s != P.J)) continue;
+          const OutWin<Real>* W = nullptr;
+          for (int wi = 0; wi < nw; ++wi) if (w[wi].sbi == e.x) W = &w[wi];
+          // partner position: base from μ's position on λ's grid, plus the stencil offset
+          int b0, b1;
+          if (L.level == S.level) { b0 = p0; b1 = p1; }
+          else if (L.level < S.level) { b0 = p0 << (S.level - L.level); b1 = p1 << (S.level - L.level); }
+          else { b0 = p0 >> (L.level - S.level); b1 = p1 >> (L.level - S.level); }
+          const int l0 = D == 2 ? ((b0 + e.y) & (L.nl - 1)) : 0;
+          const int l1 = (b1 + e.z) & (L.nl - 1);
+          Real x = Real(0);
+          if (W) {
+            const int li0 = local_index(W->r0, l0), li1 = local_index(W->r1, l1);
+            if (li0 >= 0 && li1 >= 0) x = W->buf[li0 * W->r1.len + li1];
+          }
+          stage_val[j] = x;
+          stage_col[j] = int(L.offset + int64_t(l0) * L.nl + l1);
+        }
+      } else if (MODE == MODE_TMAX) {
+        for (int wi = 0; wi < nw; ++wi) {
+          const int tot = w[wi].r0.len * w[wi].r1.len;
+          for (int idx = tid; idx < tot; idx += kBlock) tmax = fmax(tmax, fabs(double(w[wi].buf[idx])));
+        }
+      } else if (MODE == MODE_TCOUNT) {
+        for (int wi = 0; wi < nw; ++wi) {
+          int c = 0;
+          const int tot = w[wi].r0.len * w[wi].r1.len;
+          for (int idx = tid; idx < tot; idx += kBlock) c += fabs(double(w[wi].buf[idx])) >= A.tau;
+          c = block_reduce_sum(c, red_i);
+          if (tid == 0) A.cnt[row * P.nsb + w[wi].sbi] = c;
+        }
+      } else if (MODE == MODE_TWRITE) {
+        OutT* outv = reinterpret_cast<OutT*>(A.val);
+        for (int wi = 0; wi < nw; ++wi) {
+          const OutWin<Real>& W = w[wi];
+          const SubBand& L = P.sb[W.sbi];
+          int64_t base = A.row_ptr[row];
+          for (int q = 0; q < W.sbi; ++q) base += A.cnt[row * P.nsb + q];
+          const int tot = W.r0.len * W.r1.len;
+          int running = 0;
+          for (int k0 = 0; k0 < tot; k0 += kBlock) {
+            const int k = k0 + tid;
+            int keep = 0, colv = 0;
+            Real x = Real(0);
+            if (k < tot) {
+              const int ks0 = k / W.r1.len, ks1 = k - ks0 * W.r1.len;      // sorted (global) order
+              const int i0 = sorted_to_local(W.r0, ks0), i1 = sorted_to_local(W.r1, ks1);
+              x = W.buf[i0 * W.r1.len + i1];
+              keep = fabs(double(x)) >= A.tau;
+              const int g0 = (W.r0.lo + i0) & (W.r0.nl - 1);
+              const int g1 = (W.r1.lo + i1) & (W.r1.nl - 1);
+              colv = int(L.offset + int64_t(g0) * L.nl + g1);
+            }
+            int posn, agg;
+            BlockScan(scan_tmp).ExclusiveSum(keep, posn, agg);
+            if (keep) {
+              A.col[base + running + posn] = colv;
+              outv[base + running + posn] = OutT(x);
+            }
+            running += agg;
+            __syncthreads();
+          }
+        }
+      }
+      __syncthreads();
+      Real* tswap = cur; cur = nxt; nxt = tswap;
+      in0 = a0;
+      in1 = a1;
+    }
+
+    // ---- finalize the unit
+    if (MODE == MODE_BAND) {
+      const int Lp = P.band_Lpad;
+      for (int k = 2; k <= Lp; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = tid; i < Lp; i += kBlock) {
+            const int ixj = i ^ j;
+            if (ixj > i) {
+              const bool up = (i & k) == 0;
+              const int ci = stage_col[i], cj = stage_col[ixj];
+              if ((ci > cj) == up) {
+                stage_col[i] = cj; stage_col[ixj] = ci;
+                const Real vi = stage_val[i]; stage_val[i] = stage_val[ixj]; stage_val[ixj] = vi;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      OutT* outv = reinterpret_cast<OutT*>(A.val);
+      const int64_t base = row * P.band_L;
+      for (int j = tid; j < P.band_L; j += kBlock) {
+        A.col[base + j] = stage_col[j];
+        outv[base + j] = OutT(stage_val[j]);
+      }
+    } else if (MODE == MODE_TMAX) {
+      const double mx = block_reduce_max(tmax, red_d);
+      if (tid == 0) A.unitmax[row] = mx;
+    }
+    __syncthreads();
+  }
+}
+
+// ============================================================================= small kernels
+
+__global__ void fill_band_rowptr(int64_t* row_ptr, int64_t rows, int64_t L) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= rows; i += int64_t(gridDim.x) * blockDim.x)
+    row_ptr[i] = i * L;
+}
+
+__global__ void fill_full(int64_t* row_ptr, int32_t* col, int64_t rows, int64_t N) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= rows; i += int64_t(gridDim.x) * blockDim.x)
+    row_ptr[i] = i * N;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < rows * N; i += int64_t(gridDim.x) * blockDim.x)
+    col[i] = int32_t(i % N);
+}
+
+__global__ void row_counts_kernel(const int32_t* cnt, int64_t rows, int nsb, int64_t* rowcnt) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r <= rows; r += int64_t(gridDim.x) * blockDim.x) {
+    int64_t c = 0;
+    if (r < rows) for (int s = 0; s < nsb; ++s) c += cnt[r * nsb + s];
+    rowcnt[r] = c;
+  }
+}
+
+__global__ void max_reduce_kernel(const double* x, int64_t n, unsigned long long* out) {
+  __shared__ double red[kBlock / 32];
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    m = fmax(m, x[i]);
+  m = block_reduce_max(m, red);
+  if (threadIdx.x == 0) atomicMax(out, __double_as_longlong(m));   // m ≥ 0: bit order = value order
+}
+
+template <typename T>
+__global__ void spmv_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y, int64_t rows) {
+  const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  double acc = 0.0;
+  for (int64_t j = rp[warp] + lane; j < rp[warp + 1]; j += 32) acc += double(val[j]) * double(x[col[j]]);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[warp] = T(acc);
+}
+
+template <typename T>
+__global__ void spmv_t_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const T* __restrict__ val, const T* __restrict__ x, T* __restrict__ y, int64_t rows) {
+  const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const T xr = x[warp];
+  for (int64_t j = rp[warp] + lane; j < rp[warp + 1]; j += 32) atomicAdd(&y[col[j]], val[j] * xr);
+}
+
+// ============================================================================= launchers
+
+static int grid_for(int64_t n, int per = kBlock) {
+  int64_t g = (n + per - 1) / per;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return int(g);
+}
+
+cudaError_t launch_phi0(const Plan& P, const double* u, double* phi0, int S0, int W0, int S1, int W1,
+                        cudaStream_t st) {
+  phi0_kernel<<<grid_for(int64_t(P.m) * W0 * W1), kBlock, 0, st>>>(P, u, phi0, S0, W0, S1, W1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tmpl_level(const Plan& P, const TmplArgs& A, int real_bytes, int level, cudaStream_t st) {
+  const int64_t totA = int64_t(P.m) * 2 * A.Win[0] * A.Wout[1];
+  const int64_t totB = int64_t(P.m) * 4 * A.Wout[0] * A.Wout[1];
+  if (real_bytes == 4) {
+    tmpl_passA<float><<<grid_for(totA), kBlock, 0, st>>>(P, A, P.J, level);
+    if (P.d == 2) tmpl_passB<float><<<grid_for(totB), kBlock, 0, st>>>(P, A, P.J, level);
+  } else {
+    tmpl_passA<double><<<grid_for(totA), kBlock, 0, st>>>(P, A, P.J, level);
+    if (P.d == 2) tmpl_passB<double><<<grid_for(totB), kBlock, 0, st>>>(P, A, P.J, level);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cast(const double* src, void* dst, int64_t count, int real_bytes, cudaStream_t st) {
+  if (real_bytes == 4) cast_kernel<float><<<grid_for(count), kBlock, 0, st>>>(src, (float*)dst, count);
+  else cast_kernel<double><<<grid_for(count), kBlock, 0, st>>>(src, (double*)dst, count);
+  return cudaGetLastError();
+}
+
+template <typename Real, typename OutT, int D, int MODE>
+static cudaError_t launch_one(const Plan& P, const UnitArgs& A, int grid, size_t smem, cudaStream_t st) {
+  auto kern = unit_kernel<Real, OutT, D, MODE>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<grid, kBlock, smem, st>>>(P, A);
+  return cudaGetLastError();
+}
+
+template <typename Real, typename OutT, int MODE>
+static cudaError_t launch_d(const Plan& P, const UnitArgs& A, int grid, size_t smem, cudaStream_t st) {
+  return P.d == 2 ? launch_one<Real, OutT, 2, MODE>(P, A, grid, smem, st)
+                  : launch_one<Real, OutT, 1, MODE>(P, A, grid, smem, st);
+}
+
+cudaError_t launch_units(const Plan& P, const UnitArgs& A, int mode, int real_bytes, int out_bytes, int grid,
+                         size_t smem, cudaStream_t st) {
+  switch (mode) {
+    case MODE_FULL:
+      return real_bytes == 4 ? launch_d<float, float, MODE_FULL>(P, A, grid, smem, st)
+                             : launch_d<double, double, MODE_FULL>(P, A, grid, smem, st);
+    case MODE_BAND:
+      return real_bytes == 4 ? launch_d<float, float, MODE_BAND>(P, A, grid, smem, st)
+                             : launch_d<double, double, MODE_BAND>(P, A, grid, smem, st);
+    case MODE_TMAX:
+      return launch_d<double, double, MODE_TMAX>(P, A, grid, smem, st);
+    case MODE_TCOUNT:
+      return launch_d<double, double, MODE_TCOUNT>(P, A, grid, smem, st);
+    case MODE_TWRITE:
+      return out_bytes == 4 ? launch_d<double, float, MODE_TWRITE>(P, A, grid, smem, st)
+                            : launch_d<double, double, MODE_TWRITE>(P, A, grid, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+size_t unit_smem_limit() { return 200 * 1024; }
+
+cudaError_t launch_fill_band_rowptr(int64_t* row_ptr, int64_t rows, int64_t L, cudaStream_t st) {
+  fill_band_rowptr<<<grid_for(rows + 1), kBlock, 0, st>>>(row_ptr, rows, L);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_full(int64_t* row_ptr, int32_t* col, int64_t rows, int64_t N, cudaStream_t st) {
+  fill_full<<<grid_for(rows * N), kBlock, 0, st>>>(row_ptr, col, rows, N);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_counts(const int32_t* cnt, int64_t rows, int nsb, int64_t* rowcnt, cudaStream_t st) {
+  row_counts_kernel<<<grid_for(rows + 1), kBlock, 0, st>>>(cnt, rows, nsb, rowcnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_reduce(const double* x, int64_t n, double* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  max_reduce_kernel<<<grid_for(n), kBlock, 0, st>>>(x, n, reinterpret_cast<unsigned long long*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmv(const int64_t* row_ptr, const int32_t* col, const void* val, const void* x, void* y,
+                        int64_t rows, int64_t N, int transpose, int bytes, cudaStream_t st) {
+  const int grid = int((rows * 32 + kBlock - 1) / kBlock);
+  if (grid == 0) return cudaSuccess;
+  if (!transpose) {
+    if (bytes == 4) spmv_kernel<float><<<grid, kBlock, 0, st>>>(row_ptr, col, (const float*)val, (const float*)x, (float*)y, rows);
+    else spmv_kernel<double><<<grid, kBlock, 0, st>>>(row_ptr, col, (const double*)val, (const double*)x, (double*)y, rows);
+  } else {
+    cudaError_t e = cudaMemsetAsync(y, 0, size_t(N) * bytes, st);
+    if (e != cudaSuccess) return e;
+    if (bytes == 4) spmv_t_kernel<float><<<grid, kBlock, 0, st>>>(row_ptr, col, (const float*)val, (const float*)x, (float*)y, rows);
+    else spmv_t_kernel<double><<<grid, kBlock, 0, st>>>(row_ptr, col, (const double*)val, (const double*)x, (double*)y, rows);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* tmp, size_t* tmp_bytes,
+                               cudaStream_t st) {
+  return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, in, out, n, st);
+}
+
+}  // namespace pcwd

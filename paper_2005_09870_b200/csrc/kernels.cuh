@@ -1,0 +1,58 @@
+// kernels.cuh — launch interface of the sm_100a kernels (implemented in kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.h"
+
+namespace pcwd {
+
+struct UnitArgs {
+  const void* v;            // compute type, m × N
+  const void* T;            // compute type, templates
+  const int4* stencil;      // BAND: (sb, o0, o1, -)
+  void* gscratch;           // compute type, per-CTA slices (global-scratch launches)
+  int64_t gscratch_stride;  // elements per CTA slice
+  int64_t u0, u1;           // global unit range of this launch
+  int64_t row0;             // first unit of the shard (local row = unit - row0)
+  const int64_t* row_ptr;   // TWRITE
+  int32_t* col;
+  void* val;                // output type
+  double* unitmax;          // TMAX: per local row
+  int32_t* cnt;             // TCOUNT / TWRITE: [row][sb]
+  double tau;               // threshold (fp64)
+  int use_smem;
+};
+
+struct TmplArgs {
+  const double* phi_in;     // m × Win0 × Win1 (fp64)
+  double* Y;                // m × 2 × Win0 × Wout1
+  double* phi_out;          // m × Wout0 × Wout1
+  void* T;                  // compute type templates
+  int Sin[2], Win[2];       // input window per axis (W == n ⇒ whole line)
+  int Sout[2][2], Wout[2];  // output window per axis and orientation
+  int dil;                  // 2^{ℓ-1}
+  int64_t toff[4];          // destination offset per orientation code (-1 = not stored)
+  int64_t tstride;          // per-k stride of the destination sub-band templates
+};
+
+// dtype-dispatching launchers; return cudaError_t of the launch
+cudaError_t launch_phi0(const Plan& P, const double* u, double* phi0, int S0, int W0, int S1, int W1,
+                        cudaStream_t st);
+cudaError_t launch_tmpl_level(const Plan& P, const TmplArgs& A, int real_bytes, int coarse_level,
+                              cudaStream_t st);
+cudaError_t launch_cast(const double* src, void* dst, int64_t count, int real_bytes, cudaStream_t st);
+cudaError_t launch_units(const Plan& P, const UnitArgs& A, int mode, int real_bytes, int out_bytes,
+                         int grid, size_t smem, cudaStream_t st);
+size_t unit_smem_limit();
+cudaError_t set_unit_smem_attr(size_t bytes);
+cudaError_t launch_fill_band_rowptr(int64_t* row_ptr, int64_t rows, int64_t L, cudaStream_t st);
+cudaError_t launch_fill_full(int64_t* row_ptr, int32_t* col, int64_t rows, int64_t N, cudaStream_t st);
+cudaError_t launch_row_counts(const int32_t* cnt, int64_t rows, int nsb, int64_t* rowcnt, cudaStream_t st);
+cudaError_t launch_max_reduce(const double* x, int64_t n, double* out, cudaStream_t st);
+cudaError_t launch_spmv(const int64_t* row_ptr, const int32_t* col, const void* val, const void* x,
+                        void* y, int64_t rows, int64_t N, int transpose, int bytes, cudaStream_t st);
+cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* tmp, size_t* tmp_bytes,
+                               cudaStream_t st);
+
+}  // namespace pcwd

@@ -1,0 +1,364 @@
+// plan.cpp — validation, sub-band table, template / unit windows, band stencil, shard split.
+//
+// Passages: Λ and its layout P:113-125 (R2/R3); supports P:99-104 and the
+// recursion P:96 (R7); Lemma 6 P:1294-1301 for the cascade windows; Theorem 2 / Remark
+// P:1163-1180 for the band rule (R16); cost-balanced unit sharding.
+#include "plan.h"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <set>
+#include <tuple>
+
+namespace pcwd {
+
+static bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+static int ilog2(int64_t x) {
+  int l = 0;
+  while ((int64_t(1) << l) < x) ++l;
+  return l;
+}
+
+int validate_desc(const pcwd_desc* d, std::string* msg) {
+  if (!d) { *msg = "desc is NULL"; return PCWD_E_PARAM; }
+  if (d->d != 1 && d->d != 2) { *msg = "d must be 1 or 2"; return PCWD_E_SHAPE; }
+  if (!is_pow2(d->n) || d->n < 2) { *msg = "n must be a power of two >= 2"; return PCWD_E_SHAPE; }
+  if (d->d == 2 && d->n > (1 << 14)) { *msg = "n too large for d = 2 (max 16384)"; return PCWD_E_SHAPE; }
+  if (d->d == 1 && d->n > (1 << 24)) { *msg = "n too large for d = 1"; return PCWD_E_SHAPE; }
+  int lg = ilog2(d->n);
+  if (d->levels < 1 || d->levels > lg || d->levels > kMaxJ) { *msg = "levels must be in [1, log2 n]"; return PCWD_E_CONFIG; }
+  if (d->filter_len < 2 || d->filter_len > kMaxTaps || (d->filter_len & 1)) {
+    *msg = "filter_len must be even, 2..20"; return PCWD_E_CONFIG;
+  }
+  if (!d->h) { *msg = "h is NULL"; return PCWD_E_PARAM; }
+  if (d->m < 1) { *msg = "m must be >= 1"; return PCWD_E_PARAM; }
+  if (d->dtype != PCWD_F32 && d->dtype != PCWD_F64) { *msg = "dtype"; return PCWD_E_PARAM; }
+  int64_t N = d->d == 2 ? int64_t(d->n) * d->n : d->n;
+  if (d->retain == PCWD_RETAIN_THRESHOLD) {
+    if (!(d->tau_rel > 0.0)) { *msg = "tau_rel must be > 0"; return PCWD_E_PARAM; }
+  } else if (d->retain == PCWD_RETAIN_BAND) {
+    if (d->band_L < 1 || d->band_L > N) { *msg = "band_L must be in [1, N]"; return PCWD_E_PARAM; }
+    if (d->band_L > 4096) { *msg = "band_L > 4096 not supported"; return PCWD_E_UNSUPPORTED; }
+  } else if (d->retain != PCWD_RETAIN_FULL) {
+    *msg = "retain"; return PCWD_E_PARAM;
+  }
+  if (d->retain == PCWD_RETAIN_FULL && N > (1 << 16)) { *msg = "full retention limited to N <= 65536"; return PCWD_E_UNSUPPORTED; }
+  if (d->world < 1 || d->rank < 0 || d->rank >= d->world) { *msg = "rank must be in [0, world)"; return PCWD_E_PARAM; }
+  return PCWD_OK;
+}
+
+int sb_index(int d, int J, int level, int e) {
+  if (e == 0) return 0;
+  int ne = d == 2 ? 3 : 1;
+  return 1 + (J - level) * ne + (e - 1);
+}
+
+// Periodic bounding box [zlo, zhi] (zlo may be negative) of the nonzeros along one axis.
+static void axis_bbox(const std::vector<char>& occ, int n, int* zlo, int* zhi) {
+  int cnt = 0;
+  for (char c : occ) cnt += c != 0;
+  if (cnt == 0) { *zlo = 0; *zhi = 0; return; }
+  if (cnt == n) { *zlo = 0; *zhi = n - 1; return; }
+  // largest circular run of zeros
+  int best_len = 0, best_end = -1;  // run ends at best_end (inclusive)
+  for (int start = 0; start < n; ++start) {
+    if (occ[start] || !occ[(start - 1 + n) % n]) continue;  // run must start after a nonzero
+    int len = 0;
+    while (len < n && !occ[(start + len) % n]) ++len;
+    if (len > best_len) { best_len = len; best_end = (start + len - 1) % n; }
+  }
+  int first = (best_end + 1) % n;            // first occupied position of the arc
+  int arc = n - best_len;
+  int lo = first > n / 2 ? first - n : first;
+  *zlo = lo;
+  *zhi = lo + arc - 1;
+}
+
+// Window of one template axis after the à-trous step (dilation dil, orientation e).
+struct Win1 {
+  int S, W;  // W == n ⇒ whole line, S = 0
+};
+
+static Win1 win_next(Win1 in, int n, int dil, int L2, int e) {
+  int64_t W = int64_t(in.W) + int64_t(dil) * (L2 - 1);
+  if (in.W >= n || W >= n) return Win1{0, n};
+  int o = e ? 2 - L2 : 0;
+  int S = int(((int64_t(in.S) + int64_t(dil) * o) % n + n) % n);
+  return Win1{S, int(W)};
+}
+
+// ---------------------------------------------------------------- band rule (R16)
+namespace {
+struct Cand {
+  int key0, delta, rho, level, e, o2, o0, o1, sb;
+  bool operator<(const Cand& b) const {
+    return std::tie(key0, delta, rho, level, e, o2, o0, o1) <
+           std::tie(b.key0, b.delta, b.rho, b.level, b.e, b.o2, b.o0, b.o1);
+  }
+};
+inline int canon(int64_t raw, int nl) {   // [-nl/2, nl/2)
+  int64_t half = nl / 2;
+  int64_t r = ((raw + half) % nl + nl) % nl;
+  return int(r - half);
+}
+inline int pdist(int64_t q, int nc) {
+  int64_t r = ((q % nc) + nc) % nc;
+  return int(std::min<int64_t>(r, nc - r));
+}
+inline int64_t floordiv(int64_t a, int64_t b) {  // b > 0
+  return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+}  // namespace
+
+static void build_stencil(const Plan& P, int s_mu, int L, std::vector<Stencil>* out) {
+  const SubBand& mu = P.sb[s_mu];
+  int d = P.d;
+  for (int S = 0;; ++S) {
+    std::vector<Cand> cands;
+    for (int s = 0; s < P.nsb; ++s) {
+      const SubBand& lam = P.sb[s];
+      int delta = std::abs(lam.level - mu.level);
+      if (delta > S) continue;
+      int rmax = S - delta;
+      int nl = lam.nl;
+      int lc = std::max(lam.level, mu.level);
+      int nc = P.n >> lc;
+      bool finer = lam.level < mu.level;
+      // candidate offsets per axis
+      std::vector<int> offs;
+      {
+        std::set<int> seen;
+        int64_t lo, hi;
+        if (finer) { lo = -int64_t(rmax) << delta; hi = ((int64_t(rmax) + 1) << delta) - 1; }
+        else { lo = -rmax; hi = rmax; }
+        for (int64_t o = lo; o <= hi; ++o) {
+          int c = canon(o, nl);
+          if (seen.insert(c).second) offs.push_back(c);
+          if ((int64_t)seen.size() >= nl) break;
+        }
+      }
+      auto rho_of = [&](int o) {
+        int64_t q = finer ? floordiv(o, int64_t(1) << delta) : o;
+        return pdist(q, nc);
+      };
+      if (d == 1) {
+        for (int o1 : offs) {
+          int rho = rho_of(o1);
+          if (delta + rho > S) continue;
+          cands.push_back(Cand{delta + rho, delta, rho, lam.level, lam.e, o1 * o1, 0, o1, s});
+        }
+      } else {
+        for (int o0 : offs)
+          for (int o1 : offs) {
+            int rho = std::max(rho_of(o0), rho_of(o1));
+            if (delta + rho > S) continue;
+            cands.push_back(Cand{delta + rho, delta, rho, lam.level, lam.e, o0 * o0 + o1 * o1, o0, o1, s});
+          }
+      }
+    }
+    bool exhausted = S > P.J + P.n;
+    if ((int)cands.size() >= L || exhausted) {
+      std::sort(cands.begin(), cands.end());
+      for (int i = 0; i < L && i < (int)cands.size(); ++i)
+        out->push_back(Stencil{cands[i].sb, cands[i].o0, cands[i].o1, 0});
+      return;
+    }
+  }
+}
+
+int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::string* msg) {
+  int rc = validate_desc(d, msg);
+  if (rc) return rc;
+  Plan& P = hp->P;
+  std::memset(&P, 0, sizeof(Plan));
+  P.d = d->d;
+  P.n = d->n;
+  P.J = d->levels;
+  P.L2 = d->filter_len;
+  P.m = d->m;
+  P.N = d->d == 2 ? int64_t(d->n) * d->n : d->n;
+  P.retain = d->retain;
+  P.band_L = d->retain == PCWD_RETAIN_BAND ? d->band_L : 0;
+  P.band_Lpad = 1;
+  while (P.band_Lpad < P.band_L) P.band_Lpad <<= 1;
+  const int n = P.n, J = P.J, L2 = P.L2;
+  // taps: f_0 = h (o_0 = 0); f_1[j] = g[i], i = 2 - L2 + j, g[i] = (-1)^{1-i} h[1-i]
+  P.to[0] = 0;
+  P.to[1] = 2 - L2;
+  for (int j = 0; j < L2; ++j) {
+    int i = 2 - L2 + j;
+    double g = (((1 - i) % 2) == 0 ? 1.0 : -1.0) * d->h[1 - i];
+    P.td[0][j] = d->h[j];
+    P.td[1][j] = g;
+    P.tf[0][j] = float(d->h[j]);
+    P.tf[1][j] = float(g);
+  }
+  hp->real_bytes = (d->dtype == PCWD_F64 || d->retain == PCWD_RETAIN_THRESHOLD) ? 8 : 4;
+  hp->out_bytes = d->dtype == PCWD_F64 ? 8 : 4;
+
+  // periodic bounding box of supp u_k (union over k), per axis
+  if (u_host) {
+    std::vector<char> occ0(n, 0), occ1(n, 0);
+    for (int k = 0; k < P.m; ++k)
+      for (int64_t z = 0; z < P.N; ++z)
+        if (u_host[k * P.N + z] != 0.0) {
+          if (P.d == 2) { occ0[z / n] = 1; occ1[z % n] = 1; }
+          else occ1[z] = 1;
+        }
+    axis_bbox(occ1, n, &P.zlo[1], &P.zhi[1]);
+    if (P.d == 2) axis_bbox(occ0, n, &P.zlo[0], &P.zhi[0]);
+  } else {
+    P.zlo[1] = 0; P.zhi[1] = n - 1;
+    if (P.d == 2) { P.zlo[0] = 0; P.zhi[0] = n - 1; }
+  }
+
+  // sub-band table in Λ order
+  int ns = 0;
+  auto add = [&](int level, int e, int e0, int e1) {
+    SubBand& s = P.sb[ns++];
+    s.level = level; s.e = e; s.e0 = e0; s.e1 = e1;
+    s.nl = n >> level;
+    s.count = P.d == 2 ? int64_t(s.nl) * s.nl : s.nl;
+  };
+  add(J, 0, 0, 0);
+  for (int lev = J; lev >= 1; --lev) {
+    if (P.d == 2) { add(lev, 1, 0, 1); add(lev, 2, 1, 0); add(lev, 3, 1, 1); }
+    else add(lev, 1, 0, 1);
+  }
+  P.nsb = ns;
+  int64_t off = 0;
+  for (int s = 0; s < ns; ++s) { P.sb[s].offset = off; off += P.sb[s].count; }
+
+  // template windows: φ chain from ũ (window [-zhi, -zlo]) by the à-trous recursion
+  std::array<std::vector<Win1>, 2> phi;  // phi[a][ℓ] = window of ũ ⋆ φ_{ℓ,0} on axis a
+  for (int a = 0; a < 2; ++a) {
+    phi[a].resize(J + 1);
+    if (a == 0 && P.d == 1) { for (auto& w : phi[a]) w = Win1{0, 1}; continue; }
+    int W0 = P.zhi[a] - P.zlo[a] + 1;
+    phi[a][0] = W0 >= n ? Win1{0, n} : Win1{((-P.zhi[a]) % n + n) % n, W0};
+    for (int lev = 1; lev <= J; ++lev) phi[a][lev] = win_next(phi[a][lev - 1], n, 1 << (lev - 1), L2, 0);
+  }
+  for (int a = 0; a < 2; ++a)
+    for (int lev = 0; lev <= J; ++lev) {
+      hp->phiS[a][lev] = phi[a][lev].S;
+      hp->phiW[a][lev] = phi[a][lev].W;
+      hp->psiS[a][lev] = lev == 0 ? 0
+          : (a == 0 && P.d == 1 ? 0 : win_next(phi[a][lev - 1], n, 1 << (lev - 1), L2, 1).S);
+    }
+  int64_t toff = 0;
+  hp->phi_elems = 0;
+  hp->y_elems = 0;
+  hp->fma_templates = 0.0;
+  for (int lev = 1; lev <= J; ++lev) {
+    Win1 in0 = phi[0][lev - 1], in1 = phi[1][lev - 1];
+    Win1 o1 = win_next(in1, n, 1 << (lev - 1), L2, 0);
+    Win1 o0 = P.d == 2 ? win_next(in0, n, 1 << (lev - 1), L2, 0) : Win1{0, 1};
+    hp->phi_elems = std::max<int64_t>(hp->phi_elems, int64_t(in0.W) * in1.W);
+    hp->phi_elems = std::max<int64_t>(hp->phi_elems, int64_t(o0.W) * o1.W);
+    hp->y_elems = std::max<int64_t>(hp->y_elems, 2 * int64_t(in0.W) * o1.W);
+    hp->fma_templates += double(P.m) * L2 * (2.0 * in0.W * o1.W + (P.d == 2 ? 4.0 * o0.W * o1.W : 0.0));
+  }
+  for (int s = 0; s < ns; ++s) {
+    SubBand& S = P.sb[s];
+    int lev = S.level;
+    for (int a = 0; a < 2; ++a) {
+      if (a == 0 && P.d == 1) { S.tS[0] = 0; S.tW[0] = 1; continue; }
+      int e_a = a == 0 ? S.e0 : S.e1;
+      Win1 w = win_next(phi[a][lev - 1], n, 1 << (lev - 1), L2, e_a);
+      S.tS[a] = w.S;
+      S.tW[a] = w.W;
+    }
+    S.tstride = int64_t(S.tW[0]) * S.tW[1];
+    S.toff = toff;
+    toff += S.tstride * P.m;
+    toff = (toff + 3) & ~int64_t(3);
+  }
+  hp->tmpl_elems = toff;
+
+  // band stencils (per unit sub-band), then the steps each sub-band needs
+  hp->stencil.clear();
+  for (int s = 0; s < ns; ++s) {
+    P.sb[s].stencil_off = int(hp->stencil.size());
+    if (P.retain == PCWD_RETAIN_BAND) build_stencil(P, s, P.band_L, &hp->stencil);
+    int steps = J;
+    if (P.retain == PCWD_RETAIN_BAND) {
+      steps = 1;
+      for (int j = 0; j < P.band_L; ++j) {
+        const Stencil& st = hp->stencil[P.sb[s].stencil_off + j];
+        steps = std::max(steps, P.sb[st.sb].level);
+      }
+    }
+    P.sb[s].steps = steps;
+  }
+
+  // per-unit scratch layout and algorithmic FMA (max windows over the unit's parity)
+  const int rb = hp->real_bytes;
+  for (int s = 0; s < ns; ++s) {
+    SubBand& S = P.sb[s];
+    int64_t w0 = P.d == 2 ? std::min(S.tW[0], n) : 1;
+    int64_t w1 = std::min(S.tW[1], n);
+    int64_t nl0 = P.d == 2 ? n : 1, nl1 = n;
+    int64_t X0 = w0 * w1;
+    int64_t maxA = 0, maxY = 0, maxD = 0;
+    double fma = double(P.m) * X0;
+    S.any_full = (S.tW[1] >= n) || (P.d == 2 && S.tW[0] >= n);
+    for (int st = 1; st <= S.steps; ++st) {
+      int64_t o0 = P.d == 2 ? step_out_maxlen(int(w0), int(nl0), L2) : 1;
+      int64_t o1 = step_out_maxlen(int(w1), int(nl1), L2);
+      if (P.d == 2) {
+        maxY = std::max(maxY, w0 * 2 * o1);
+        maxA = std::max(maxA, o0 * o1);
+        maxD = std::max(maxD, 3 * o0 * o1);
+        fma += double(L2) * (w0 * 2.0 * o1 + 4.0 * o0 * o1);
+      } else {
+        maxA = std::max(maxA, o1);
+        maxD = std::max(maxD, o1);
+        fma += double(L2) * 2.0 * o1;
+      }
+      w0 = o0; w1 = o1;
+      nl0 = P.d == 2 ? nl0 / 2 : 1;
+      nl1 /= 2;
+    }
+    auto al = [](int64_t x) { return (x + 3) & ~int64_t(3); };
+    S.offX0 = 0;
+    S.offX1 = al(std::max(X0, maxA));
+    S.offY = S.offX1 + al(maxA);
+    S.offD = S.offY + al(maxY);
+    S.offStage = S.offD + al(maxD);
+    int64_t stage = 0;
+    if (P.retain == PCWD_RETAIN_BAND) stage = P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb;
+    S.scratch = S.offStage + al(stage);
+    S.fma = fma;
+  }
+
+  // shard: contiguous unit ranges with equal algorithmic cost (units in Λ order)
+  double total = 0.0;
+  for (int s = 0; s < ns; ++s) total += P.sb[s].fma * double(P.sb[s].count);
+  auto unit_at_cost = [&](double c) -> int64_t {   // first unit whose prefix cost ≥ c
+    double acc = 0.0;
+    for (int s = 0; s < ns; ++s) {
+      double sc = P.sb[s].fma * double(P.sb[s].count);
+      if (acc + sc >= c) {
+        int64_t k = int64_t(std::ceil((c - acc) / P.sb[s].fma - 1e-9));
+        k = std::max<int64_t>(0, std::min<int64_t>(k, P.sb[s].count));
+        return P.sb[s].offset + k;
+      }
+      acc += sc;
+    }
+    return P.N;
+  };
+  hp->row0 = d->rank == 0 ? 0 : unit_at_cost(total * d->rank / d->world);
+  hp->row1 = d->rank == d->world - 1 ? P.N : unit_at_cost(total * (d->rank + 1) / d->world);
+  double f = 0.0;
+  for (int s = 0; s < ns; ++s) {
+    int64_t a = std::max(hp->row0, P.sb[s].offset);
+    int64_t b = std::min(hp->row1, P.sb[s].offset + P.sb[s].count);
+    if (b > a) f += P.sb[s].fma * double(b - a);
+  }
+  hp->fma_shard = f + hp->fma_templates;
+  return PCWD_OK;
+}
+
+}  // namespace pcwd

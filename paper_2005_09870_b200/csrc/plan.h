@@ -1,0 +1,39 @@
+// plan.h — host-side planning for one handle (no CUDA calls).
+#pragma once
+#include <string>
+#include <vector>
+
+#include "../../include/pcwd.h"
+#include "common.h"
+
+namespace pcwd {
+
+struct Stencil {
+  int sb, o0, o1, pad;
+};
+
+struct HostPlan {
+  Plan P;
+  std::vector<Stencil> stencil;   // nsb × band_L (BAND only)
+  int real_bytes = 4;             // compute precision
+  int out_bytes = 4;              // stored value precision
+  int64_t row0 = 0, row1 = 0;     // shard
+  int64_t tmpl_elems = 0;         // template buffer size (elements of the compute type)
+  int64_t phi_elems = 0;          // per-k φ-chain window max (fp64 elements)
+  int64_t y_elems = 0;            // per-k template pass-A buffer max (fp64 elements)
+  double fma_shard = 0.0;         // algorithmic FMA of the shard (k-sum + cascade + templates)
+  // template φ-chain windows per axis and level (ℓ = 0..J), and the ψ-window start per level
+  int phiS[2][kMaxJ + 1] = {}, phiW[2][kMaxJ + 1] = {}, psiS[2][kMaxJ + 1] = {};
+  double fma_templates = 0.0;
+};
+
+// Returns a pcwd_status; msg receives the reason on error.
+int validate_desc(const pcwd_desc* d, std::string* msg);
+
+// u_host: m × N fp64 on the host (may be NULL: then the bounding box is the whole torus).
+int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::string* msg);
+
+// Λ order index of sub-band (level, e).
+int sb_index(int d, int J, int level, int e);
+
+}  // namespace pcwd

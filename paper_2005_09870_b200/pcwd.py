@@ -1,0 +1,264 @@
+"""Thin ctypes binding of libpcwd.so (include/pcwd.h) — argument marshalling only.
+
+Every step of the decomposition runs in the library's CUDA kernels; this module only
+passes pointers and sizes, allocates the torch tensors that receive copies of the CSR,
+and (for multi-process runs) does the one MAX all-reduce of the threshold rule through
+torch.distributed.  There is no CPU fallback: if the library is missing, loading fails.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpcwd.so")
+
+PCWD_F32, PCWD_F64 = 0, 1
+RETAIN = {"full": 0, "threshold": 1, "band": 2}
+STATUS = {0: "OK", 1: "E_SHAPE", 2: "E_CONFIG", 3: "E_PARAM", 4: "E_CUDA", 5: "E_OOM", 6: "E_STATE",
+          7: "E_UNSUPPORTED"}
+
+
+class PcwdError(RuntimeError):
+    def __init__(self, code: int, where: str, msg: str):
+        super().__init__(f"{where}: {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("n", ctypes.c_int32), ("levels", ctypes.c_int32),
+                ("filter_len", ctypes.c_int32), ("h", ctypes.c_void_p), ("m", ctypes.c_int32),
+                ("u", ctypes.c_void_p), ("v", ctypes.c_void_p), ("dtype", ctypes.c_int32),
+                ("retain", ctypes.c_int32), ("tau_rel", ctypes.c_double), ("band_L", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+class Csr(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int64), ("row0", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p), ("val", ctypes.c_void_p),
+                ("dtype", ctypes.c_int32)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("row0", ctypes.c_int64), ("row1", ctypes.c_int64),
+                ("nnz", ctypes.c_int64), ("global_max", ctypes.c_double),
+                ("fma_algorithmic", ctypes.c_double), ("bytes_algorithmic", ctypes.c_double),
+                ("kernel_launches", ctypes.c_int32), ("compute_dtype", ctypes.c_int32)]
+
+
+EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_max", "pcwd_get_csr",
+           "pcwd_copy_csr", "pcwd_apply", "pcwd_info", "pcwd_destroy", "pcwd_error_string",
+           "pcwd_last_error", "pcwd_validate", "pcwd_plan_shard", "pcwd_plan_stencil",
+           "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times"]
+
+_lib = None
+
+
+def lib():
+    """Load libpcwd.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64p, i32p = ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)
+        L.pcwd_create.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(vp)]
+        L.pcwd_decompose.argtypes = [vp, vp]
+        L.pcwd_local_max.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_double)]
+        L.pcwd_set_global_max.argtypes = [vp, ctypes.c_double]
+        L.pcwd_get_csr.argtypes = [vp, ctypes.POINTER(Csr)]
+        L.pcwd_copy_csr.argtypes = [vp, vp, vp, vp, vp]
+        L.pcwd_apply.argtypes = [vp, vp, vp, ctypes.c_int, vp]
+        L.pcwd_info.argtypes = [vp, ctypes.POINTER(Info)]
+        L.pcwd_destroy.argtypes = [vp]
+        L.pcwd_error_string.restype = ctypes.c_char_p
+        L.pcwd_error_string.argtypes = [ctypes.c_int]
+        L.pcwd_last_error.restype = ctypes.c_char_p
+        L.pcwd_validate.argtypes = [ctypes.POINTER(Desc)]
+        L.pcwd_plan_shard.argtypes = [ctypes.POINTER(Desc), i64p, i64p]
+        L.pcwd_plan_stencil.argtypes = [ctypes.POINTER(Desc), i32, i32p, i32p, i32p]
+        L.pcwd_plan_num_subbands.argtypes = [ctypes.POINTER(Desc), i32p]
+        L.pcwd_profile.argtypes = [vp, ctypes.c_int]
+        L.pcwd_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+        for f in EXPORTS:
+            getattr(L, f)  # every declared symbol must exist
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise PcwdError(rc, where, lib().pcwd_last_error().decode())
+
+
+def _ptr(a) -> int:
+    """Address of a contiguous numpy array or torch tensor."""
+    if a is None:
+        return 0
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return a.ctypes.data
+    assert a.is_contiguous()
+    return a.data_ptr()
+
+
+@dataclass
+class Spec:
+    """The problem statement of the ABI (R2-R16)."""
+    d: int
+    n: int
+    levels: int
+    h: np.ndarray
+    u: object            # (m, N) fp64 numpy array (host) or torch.float64 CUDA tensor
+    v: object
+    dtype: str = "f32"   # "f32" | "f64"
+    retain: str = "band"
+    tau_rel: float = 0.0
+    band_L: int = 0
+    rank: int = 0
+    world: int = 1
+    device: int = 0
+
+
+def make_desc(s: Spec, keep: list) -> Desc:
+    h = np.ascontiguousarray(np.asarray(s.h, dtype=np.float64))
+    keep.append(h)
+    for a in (s.u, s.v):
+        keep.append(a)
+    m = int(s.u.shape[0])
+    return Desc(s.d, s.n, s.levels, len(h), _ptr(h), m, _ptr(s.u), _ptr(s.v),
+                PCWD_F64 if s.dtype == "f64" else PCWD_F32, RETAIN[s.retain], float(s.tau_rel),
+                int(s.band_L), s.rank, s.world, s.device)
+
+
+class Decomposition:
+    """One handle: the shard of units (rank, world) of Θ = Ψ* H Ψ for the given operator."""
+
+    def __init__(self, spec: Spec):
+        self.spec = spec
+        keep = []
+        self._desc = make_desc(spec, keep)
+        h = ctypes.c_void_p()
+        _check(lib().pcwd_create(ctypes.byref(self._desc), ctypes.byref(h)), "pcwd_create")
+        self._h = h
+
+    # -- compute ------------------------------------------------------------------------
+    def decompose(self, stream: int = 0):
+        _check(lib().pcwd_decompose(self._h, ctypes.c_void_p(stream)), "pcwd_decompose")
+
+    def local_max(self, stream: int = 0) -> float:
+        out = ctypes.c_double()
+        _check(lib().pcwd_local_max(self._h, ctypes.c_void_p(stream), ctypes.byref(out)), "pcwd_local_max")
+        return out.value
+
+    def set_global_max(self, M: float):
+        _check(lib().pcwd_set_global_max(self._h, ctypes.c_double(M)), "pcwd_set_global_max")
+
+    def decompose_distributed(self, stream: int = 0):
+        """Multi-process decompose: the threshold rule's one exchange is a MAX all-reduce of
+        the per-rank maxima (torch.distributed, NCCL on GPUs); band/full need none."""
+        import torch
+        import torch.distributed as dist
+        if self.spec.retain == "threshold" and self.spec.world > 1:
+            m = self.local_max(stream)
+            dev = torch.device("cuda", self.spec.device) if dist.get_backend() == "nccl" else torch.device("cpu")
+            t = torch.tensor([m], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            self.set_global_max(float(t.item()))
+        self.decompose(stream)
+
+    # -- results ------------------------------------------------------------------------
+    def info(self) -> Info:
+        out = Info()
+        _check(lib().pcwd_info(self._h, ctypes.byref(out)), "pcwd_info")
+        return out
+
+    def profile(self, enable: bool = True):
+        _check(lib().pcwd_profile(self._h, int(enable)), "pcwd_profile")
+
+    def phase_times(self):
+        """(ms[3], fma[3]) of the last decompose: templates, unit kernels, rest."""
+        ms = (ctypes.c_double * 3)()
+        fm = (ctypes.c_double * 3)()
+        _check(lib().pcwd_phase_times(self._h, ms, fm), "pcwd_phase_times")
+        return list(ms), list(fm)
+
+    def csr_meta(self) -> Csr:
+        out = Csr()
+        _check(lib().pcwd_get_csr(self._h, ctypes.byref(out)), "pcwd_get_csr")
+        return out
+
+    def csr(self, device: str = "cuda", stream: int = 0, pin: bool = False):
+        """Copies of (row_ptr int64, col int32, val) as torch tensors on `device`."""
+        import torch
+        meta = self.csr_meta()
+        vdt = torch.float64 if self.spec.dtype == "f64" else torch.float32
+        kw = {"pin_memory": True} if (pin and device == "cpu") else {}
+        if device != "cpu":
+            kw = {"device": torch.device("cuda", self.spec.device)}
+        rp = torch.empty(meta.n_rows + 1, dtype=torch.int64, **kw)
+        col = torch.empty(meta.nnz, dtype=torch.int32, **kw)
+        val = torch.empty(meta.nnz, dtype=vdt, **kw)
+        _check(lib().pcwd_copy_csr(self._h, _ptr(rp), _ptr(col) if meta.nnz else 0, _ptr(val) if meta.nnz else 0,
+                                   ctypes.c_void_p(stream)), "pcwd_copy_csr")
+        if device == "cpu" or stream == 0:
+            torch.cuda.synchronize(self.spec.device)
+        return rp, col, val
+
+    def apply(self, x, transpose: bool = False, stream: int = 0):
+        """y = Θ_ret x (or Θ_retᵀ x) on the device, x a CUDA tensor of the value dtype."""
+        import torch
+        meta = self.csr_meta()
+        n_out = meta.n_rows if not transpose else int(self.info().N)
+        y = torch.empty(n_out, dtype=x.dtype, device=x.device)
+        _check(lib().pcwd_apply(self._h, _ptr(x), _ptr(y), int(transpose), ctypes.c_void_p(stream)), "pcwd_apply")
+        return y
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().pcwd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- host-only plan queries (no GPU) ---------------------------------------------------------
+
+def validate(spec: Spec) -> int:
+    keep = []
+    return lib().pcwd_validate(ctypes.byref(make_desc(spec, keep)))
+
+
+def plan_shard(spec: Spec) -> tuple[int, int]:
+    keep = []
+    d = make_desc(spec, keep)
+    r0, r1 = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().pcwd_plan_shard(ctypes.byref(d), ctypes.byref(r0), ctypes.byref(r1)), "pcwd_plan_shard")
+    return r0.value, r1.value
+
+
+def plan_stencil(spec: Spec, sb: int):
+    keep = []
+    d = make_desc(spec, keep)
+    L = spec.band_L
+    a = np.zeros(L, dtype=np.int32)
+    b = np.zeros(L, dtype=np.int32)
+    c = np.zeros(L, dtype=np.int32)
+    p = lambda x: x.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))  # noqa: E731
+    _check(lib().pcwd_plan_stencil(ctypes.byref(d), sb, p(a), p(b), p(c)), "pcwd_plan_stencil")
+    return a, b, c
+
+
+def num_subbands(spec: Spec) -> int:
+    keep = []
+    d = make_desc(spec, keep)
+    out = ctypes.c_int32()
+    _check(lib().pcwd_plan_num_subbands(ctypes.byref(d), ctypes.byref(out)), "pcwd_plan_num_subbands")
+    return out.value
