@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpcwd.so")
-SOURCES = ["api.cu", "kernels.cu", "plan.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "band_tile.cu", "batched.cu", "plan.cpp"]
 HEADERS = ["common.h", "kernels.cuh", "plan.h"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]

@@ -22,7 +22,13 @@ constexpr size_t kSmemBudget = 200 * 1024;  // dynamic smem per CTA for in-smem 
 struct Launch {
   int64_t u0, u1;
   int grid;
-  size_t smem;      // 0 ⇒ global scratch
+  size_t smem;      // 0 ⇒ global scratch (generic kernel)
+  int tile = 0;     // 1 ⇒ band_tile_kernel with the parameters below
+  TileArgs ta{};
+  int batched = 0;  // 1 ⇒ batched grid kernels (batched.cu)
+  BatchArgs ba{};
+  int64_t maxX0 = 0, maxY = 0, maxB = 0;
+  int steps = 0;
 };
 
 struct Handle {
@@ -34,8 +40,11 @@ struct Handle {
   double* phi[2] = {nullptr, nullptr};
   double* Ytmp = nullptr;
   int4* stencil_d = nullptr;
+  int4* box_d = nullptr;
   void* gscratch = nullptr;
   int64_t gstride = 0;
+  void* bscratch = nullptr;
+  size_t bscratch_bytes = 0;
   int ggrid = 0;
   std::vector<Launch> launches;
   int64_t* row_ptr = nullptr;
@@ -80,7 +89,7 @@ bool is_device_ptr(const void* p) {
 }
 
 void free_all(Handle* h) {
-  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->gscratch,
+  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->gscratch, h->bscratch,
                   h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -130,6 +139,53 @@ int build_templates(Handle* h, cudaStream_t st) {
 int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
   const Plan& P = h->hp.P;
   for (const Launch& L : h->launches) {
+    if (L.batched) {
+      if (mode != MODE_BAND) return fail(PCWD_E_STATE, "batched launch outside BAND mode");
+      BatchArgs B = L.ba;
+      B.v = h->v_d;
+      B.T = h->T_d;
+      B.stencil = h->stencil_d;
+      B.scratch = h->bscratch;
+      B.row0 = h->hp.row0;
+      B.col = h->col;
+      B.val = h->val;
+      int nl = 0;
+      CK(launch_band_batched(P, B, h->hp.real_bytes, L.maxX0, L.maxY, L.maxB, L.steps, st, &nl));
+      h->nlaunch += nl;
+      continue;
+    }
+    if (L.tile) {
+      if (mode != MODE_BAND) return fail(PCWD_E_STATE, "tile launch outside BAND mode");
+      TileArgs T = L.ta;
+      T.v = h->v_d;
+      T.T = h->T_d;
+      T.stencil = h->stencil_d;
+      T.box = h->box_d;
+      T.row0 = h->hp.row0;
+      T.col = h->col;
+      T.val = h->val;
+      T.dbg = nullptr;
+      static const bool dbg_on = getenv("PCWD_DEBUG_PHASES") != nullptr;
+      unsigned long long* dbg = nullptr;
+      if (dbg_on) {
+        CK(cudaMalloc(&dbg, 8 * sizeof(unsigned long long)));
+        CK(cudaMemset(dbg, 0, 8 * sizeof(unsigned long long)));
+        T.dbg = dbg;
+      }
+      CK(launch_band_tile(P, T, h->hp.real_bytes, L.grid, L.smem, st));
+      h->nlaunch++;
+      if (dbg_on) {
+        unsigned long long c[8];
+        CK(cudaMemcpy(c, dbg, sizeof(c), cudaMemcpyDeviceToHost));
+        double tot = 0;
+        for (int i = 2; i < 8; ++i) tot += double(c[i]);
+        fprintf(stderr, "[pcwd tile] level %d G %d grid %d smem %zu: geom %.1f%% ksum %.1f%% passA %.1f%% passB %.1f%% gather %.1f%% write %.1f%%\n",
+                P.sb[find_subband(P, L.u0)].level, L.ta.G, L.grid, L.smem, 100 * c[2] / tot, 100 * c[3] / tot,
+                100 * c[4] / tot, 100 * c[5] / tot, 100 * c[6] / tot, 100 * c[7] / tot);
+        cudaFree(dbg);
+      }
+      continue;
+    }
     UnitArgs A{};
     A.v = h->v_d;
     A.T = h->T_d;
@@ -281,7 +337,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
   if (!h->hp.stencil.empty()) {
     std::vector<int4> st(h->hp.stencil.size());
     for (size_t i = 0; i < st.size(); ++i)
-      st[i] = make_int4(h->hp.stencil[i].sb, h->hp.stencil[i].o0, h->hp.stencil[i].o1, 0);
+      st[i] = make_int4(h->hp.stencil[i].sb, h->hp.stencil[i].o0, h->hp.stencil[i].o1,
+                        P.sb[h->hp.stencil[i].sb].level);
     CKB(dalloc(&h->stencil_d, st.size() * sizeof(int4)));
     CKB(cudaMemcpy(h->stencil_d, st.data(), st.size() * sizeof(int4), cudaMemcpyHostToDevice));
   }
@@ -292,31 +349,157 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device);
   const size_t budget = std::min<size_t>(kSmemBudget, size_t(smem_optin > 0 ? smem_optin : 48 * 1024) - 8 * 1024);
+  if (!h->hp.stencil_box.empty()) {
+    std::vector<int4> bx(h->hp.stencil_box.size() / 4);
+    for (size_t i = 0; i < bx.size(); ++i)
+      bx[i] = make_int4(h->hp.stencil_box[4 * i], h->hp.stencil_box[4 * i + 1], h->hp.stencil_box[4 * i + 2],
+                        h->hp.stencil_box[4 * i + 3]);
+    CKB(dalloc(&h->box_d, bx.size() * sizeof(int4)));
+    CKB(cudaMemcpy(h->box_d, bx.data(), bx.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  }
   int64_t gmax = 0;
+  auto add_generic = [&](int64_t u0, int64_t u1, int64_t scr) {
+    if (u1 <= u0) return;
+    size_t bytes = size_t(scr) * rb;
+    Launch L{u0, u1, 0, 0};
+    if (bytes <= budget) {
+      L.smem = std::max<size_t>(bytes, 16);
+      int per_sm = int(std::min<size_t>(8, (228 * 1024) / (L.smem + 2048)));
+      per_sm = std::max(per_sm, 1);
+      L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * per_sm));
+    } else {
+      L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * 2));
+      gmax = std::max(gmax, scr);
+      h->ggrid = std::max(h->ggrid, L.grid);
+    }
+    h->launches.push_back(L);
+  };
   for (int s = 0; s < P.nsb;) {
     int lev = P.sb[s].level;
     int e = s;
     int64_t scr = 0;
-    while (e < P.nsb && P.sb[e].level == lev) { scr = std::max(scr, P.sb[e].scratch); ++e; }
+    bool tile_ok = P.retain == PCWD_RETAIN_BAND && P.d == 2 && lev <= P.J;
+    while (e < P.nsb && P.sb[e].level == lev) {
+      scr = std::max(scr, P.sb[e].scratch);
+      tile_ok = tile_ok && P.sb[e].wk_ok && P.sb[e].steps <= 6 && P.sb[e].e != 0;
+      ++e;
+    }
     int64_t u0 = std::max(h->hp.row0, P.sb[s].offset);
     int64_t u1 = std::min(h->hp.row1, P.sb[e - 1].offset + P.sb[e - 1].count);
-    if (u1 > u0) {
-      size_t bytes = size_t(scr) * rb;
-      Launch L{u0, u1, 0, 0};
-      if (bytes <= budget) {
-        L.smem = std::max<size_t>(bytes, 16);
-        int per_sm = int(std::min<size_t>(8, (228 * 1024) / (L.smem + 2048)));
-        per_sm = std::max(per_sm, 1);
-        L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * per_sm));
-      } else {
-        L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * 2));
-        gmax = std::max(gmax, scr);
-        h->ggrid = std::max(h->ggrid, L.grid);
+    if (u1 <= u0) { s = e; continue; }
+    Launch T{0, 0, 0, 0};
+    if (tile_ok && !getenv("PCWD_NO_TILE")) {
+      // per-unit scratch of the tile kernel: X (R window and approximations), Yt, D boxes, stage
+      const SubBand& S0 = P.sb[s];
+      const int VW = 16 / rb;
+      // row stride: window + alignment and vector-read slack, ≡ VW (mod 2·VW) so that 8
+      // consecutive rows hit distinct 16-byte bank groups
+      auto stride = [&](int w) {
+        int x = (w + P.L2 + 16 + VW - 1) / VW * VW;
+        while (x % (2 * VW) != VW) x += VW;
+        return x;
+      };
+      int W0 = S0.tW[0], W1 = S0.tW[1];
+      int XR = W0, XS = stride(W1), YS = stride(W0);
+      // Yt rows (pass-A outputs) and D boxes, per step: approximation width + stencil boxes
+      int YR = 0;
+      int64_t dmax = 0;
+      for (int q = s; q < e; ++q) {
+        int a1 = W1;
+        for (int st = 1; st <= P.sb[q].steps; ++st) {
+          a1 = (a1 >> 1) + (P.L2 >> 1);
+          int64_t area = 0;
+          int gw = 0, hw = 0;
+          for (int t = 0; t < P.nsb; ++t) {
+            if (P.sb[t].level != st) continue;
+            const int* b = &h->hp.stencil_box[(size_t(q) * P.nsb + t) * 4];
+            if (b[0] > b[1]) continue;
+            area += int64_t(b[1] - b[0] + 1) * (b[3] - b[2] + 1);
+            if (P.sb[t].e1) gw = std::max(gw, b[3] - b[2] + 1);
+            else hw = std::max(hw, b[3] - b[2] + 1);
+          }
+          const int hcols = (st < P.sb[q].steps || st == P.J) ? a1 : std::min(a1, hw);
+          YR = std::max(YR, hcols + std::min(a1, gw) + 1);
+          dmax = std::max(dmax, area);
+        }
       }
-      h->launches.push_back(L);
+      dmax = (dmax + VW - 1) / VW * VW;
+      int64_t stage = P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb;
+      int64_t per_unit = int64_t(XR) * XS + int64_t(YR) * YS + dmax + stage;
+      per_unit = (per_unit + VW - 1) / VW * VW;
+      int G = lev == 1 ? 8 : lev == 2 ? 4 : lev == 3 ? 2 : 1;
+      const int nl = P.sb[s].nl;
+      while (G > 1 && (size_t(G) * per_unit * rb > budget || nl % G)) G >>= 1;
+      const size_t st_bytes = size_t(e - s) * P.band_L * sizeof(int4);
+      while (G > 1 && size_t(G) * per_unit * rb + st_bytes > budget) G >>= 1;
+      size_t smem = size_t(G) * per_unit * rb + st_bytes;
+      if (smem <= budget && nl % G == 0) {
+        // whole rounds of G units inside [u0, u1); the ragged ends go to the generic kernel
+        int64_t a0 = (u0 + G - 1) / G * G, a1 = u1 / G * G;
+        if (a1 > a0) {
+          T.u0 = a0;
+          T.u1 = a1;
+          T.tile = 1;
+          T.smem = smem;
+          int per_sm = int(std::max<size_t>(1, std::min<size_t>(8, (228 * 1024) / (smem + 4096))));
+          T.grid = int(std::min<int64_t>((a1 - a0) / G, int64_t(nsm) * per_sm));
+          T.ta.u0 = a0;
+          T.ta.u1 = a1;
+          T.ta.G = G;
+          T.ta.XS = XS;
+          T.ta.YS = YS;
+          T.ta.XR = XR;
+          T.ta.YR = YR;
+          T.ta.DMAX = int(dmax);
+          T.ta.per_unit = int(per_unit);
+          add_generic(u0, a0, scr);
+          h->launches.push_back(T);
+          add_generic(a1, u1, scr);
+          s = e;
+          continue;
+        }
+      }
     }
+    if (P.retain == PCWD_RETAIN_BAND && P.d == 2 && !getenv("PCWD_NO_BATCHED")) {
+      // batched grid kernels: per-unit slots of the generic layout in one global buffer
+      Launch B{u0, u1, 0, 0};
+      B.batched = 1;
+      int64_t stride = (scr + 31) & ~int64_t(31);
+      const size_t cap = size_t(8) << 30;
+      int64_t batch = std::max<int64_t>(1, std::min<int64_t>(u1 - u0, int64_t(cap / (size_t(stride) * rb))));
+      batch = std::min<int64_t>(batch, 65535);
+      B.ba.stride = stride;
+      B.ba.u0 = u0;
+      B.ba.u1 = u1;
+      B.ba.batch = batch;
+      int steps = 0;
+      int64_t mx0 = 0, my = 0, mb = 0;
+      for (int q = s; q < e; ++q) {
+        const SubBand& S = P.sb[q];
+        steps = std::max(steps, S.steps);
+        int64_t w0 = std::min(S.tW[0], P.n), w1 = std::min(S.tW[1], P.n);
+        mx0 = std::max(mx0, w0 * w1);
+        int64_t nl0 = P.n, nl1 = P.n;
+        for (int st = 1; st <= S.steps; ++st) {
+          int64_t o0 = step_out_maxlen(int(w0), int(nl0), P.L2), o1 = step_out_maxlen(int(w1), int(nl1), P.L2);
+          my = std::max(my, w0 * 2 * o1);
+          mb = std::max(mb, 4 * o0 * o1);
+          w0 = o0; w1 = o1; nl0 >>= 1; nl1 >>= 1;
+        }
+      }
+      B.maxX0 = mx0;
+      B.maxY = my;
+      B.maxB = mb;
+      B.steps = steps;
+      h->bscratch_bytes = std::max(h->bscratch_bytes, size_t(batch) * stride * rb);
+      h->launches.push_back(B);
+      s = e;
+      continue;
+    }
+    add_generic(u0, u1, scr);
     s = e;
   }
+  if (h->bscratch_bytes) CKB(dalloc(&h->bscratch, h->bscratch_bytes));
   if (gmax > 0) {
     h->gstride = (gmax + 31) & ~int64_t(31);
     CKB(dalloc(&h->gscratch, size_t(h->gstride) * h->ggrid * rb));

@@ -88,6 +88,10 @@ struct SubBand {
   int64_t offX0, offX1, offY, offD, offStage, scratch;
   int stencil_off;  // BAND: first entry of this sub-band's stencil
   int any_full;     // some window of this sub-band covers a whole line (general path only)
+  int tSu[2];       // template window start, unwrapped: -zhi + (e_a ? 2^{ℓ-1}(2-2δ) : 0)
+  // warp-per-unit band kernel (band_warp.cu): eligibility and per-warp scratch layout
+  int wk_ok;
+  int64_t wk_offY, wk_offD, wk_offStage, wk_scratch;
   double fma;       // algorithmic FMA per unit (k-sum + cascade, max windows)
 };
 

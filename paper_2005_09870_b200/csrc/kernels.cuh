@@ -24,6 +24,42 @@ struct UnitArgs {
   int use_smem;
 };
 
+struct TileArgs {
+  const void* v;
+  const void* T;
+  const int4* stencil;
+  const int4* box;          // nsb × nsb stencil offset boxes
+  int64_t u0, u1;           // unit range (one level, whole rounds of G units)
+  int64_t row0;
+  int32_t* col;
+  void* val;
+  int G;                    // units per round
+  int XS, YS;               // row strides of X and Yt (elements)
+  int XR, YR;               // max rows of X and Yt
+  int DMAX;                 // D buffer elements per unit
+  int per_unit;             // scratch elements per unit
+  unsigned long long* dbg;  // optional per-phase clock counters (PCWD_DEBUG_PHASES)
+};
+
+cudaError_t launch_band_tile(const Plan& P, const TileArgs& A, int real_bytes, int grid, size_t smem,
+                             cudaStream_t st);
+
+struct BatchArgs {
+  const void* v;
+  const void* T;
+  const int4* stencil;      // .w = level of the partner sub-band
+  void* scratch;            // batch × stride elements (generic per-unit layout of SubBand)
+  int64_t stride;
+  int64_t u0, u1;           // unit range of this launch (one level)
+  int64_t batch;            // units per batch
+  int64_t row0;
+  int32_t* col;
+  void* val;
+};
+
+cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, int64_t maxY,
+                                int64_t maxB, int steps, cudaStream_t st, int* launches);
+
 struct TmplArgs {
   const double* phi_in;     // m × Win0 × Win1 (fp64)
   double* Y;                // m × 2 × Win0 × Wout1

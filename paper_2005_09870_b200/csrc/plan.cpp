@@ -161,8 +161,14 @@ static void build_stencil(const Plan& P, int s_mu, int L, std::vector<Stencil>* 
     bool exhausted = S > P.J + P.n;
     if ((int)cands.size() >= L || exhausted) {
       std::sort(cands.begin(), cands.end());
+      std::vector<Stencil> pick;
       for (int i = 0; i < L && i < (int)cands.size(); ++i)
-        out->push_back(Stencil{cands[i].sb, cands[i].o0, cands[i].o1, 0});
+        pick.push_back(Stencil{cands[i].sb, cands[i].o0, cands[i].o1, 0});
+      // storage order (sb, o0, o1): the CSR column order of every unit whose partners do not wrap
+      std::sort(pick.begin(), pick.end(), [](const Stencil& a, const Stencil& b) {
+        return std::tie(a.sb, a.o0, a.o1) < std::tie(b.sb, b.o0, b.o1);
+      });
+      out->insert(out->end(), pick.begin(), pick.end());
       return;
     }
   }
@@ -269,6 +275,7 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
       Win1 w = win_next(phi[a][lev - 1], n, 1 << (lev - 1), L2, e_a);
       S.tS[a] = w.S;
       S.tW[a] = w.W;
+      S.tSu[a] = -P.zhi[a] + (e_a ? (1 << (lev - 1)) * (2 - L2) : 0);
     }
     S.tstride = int64_t(S.tW[0]) * S.tW[1];
     S.toff = toff;
@@ -291,6 +298,22 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
       }
     }
     P.sb[s].steps = steps;
+  }
+  if (P.retain == PCWD_RETAIN_BAND) {
+    hp->stencil_box.assign(size_t(ns) * ns * 4, 0);
+    for (int s = 0; s < ns; ++s) {
+      for (int t = 0; t < ns; ++t) {
+        int* b = &hp->stencil_box[(size_t(s) * ns + t) * 4];
+        b[0] = b[2] = 1 << 30;
+        b[1] = b[3] = -(1 << 30);
+      }
+      for (int j = 0; j < P.band_L; ++j) {
+        const Stencil& st = hp->stencil[P.sb[s].stencil_off + j];
+        int* b = &hp->stencil_box[(size_t(s) * ns + st.sb) * 4];
+        b[0] = std::min(b[0], st.o0); b[1] = std::max(b[1], st.o0);
+        b[2] = std::min(b[2], st.o1); b[3] = std::max(b[3], st.o1);
+      }
+    }
   }
 
   // per-unit scratch layout and algorithmic FMA (max windows over the unit's parity)
@@ -331,6 +354,36 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
     if (P.retain == PCWD_RETAIN_BAND) stage = P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb;
     S.scratch = S.offStage + al(stage);
     S.fma = fma;
+
+    // warp kernel: band rule, d = 2, windows never cover a whole line, per-warp scratch small
+    S.wk_ok = 0;
+    if (P.retain == PCWD_RETAIN_BAND && P.d == 2 && (L2 == 2 || L2 == 4 || L2 == 6 || L2 == 8 || L2 == 12)) {
+      bool ok = S.tW[0] < n && S.tW[1] < n;
+      int64_t a0 = S.tW[0], a1 = S.tW[1];
+      int64_t nl = n;
+      int64_t maxY2 = 0, maxX = a0 * a1, maxD2 = 0;
+      for (int st = 1; st <= S.steps && ok; ++st) {
+        int64_t o0 = (a0 >> 1) + (L2 >> 1), o1 = (a1 >> 1) + (L2 >> 1);   // unclipped max lengths
+        nl >>= 1;
+        if (o0 >= nl || o1 >= nl) ok = false;
+        maxY2 = std::max(maxY2, a0 * 2 * o1);
+        maxX = std::max(maxX, o0 * o1);
+        maxD2 = std::max(maxD2, 3 * o0 * o1);
+        a0 = o0; a1 = o1;
+      }
+      // detail boxes are bounded by the stencil boxes
+      int64_t boxmax = 0;
+      for (int t = 0; t < ns; ++t) {
+        const int* b = &hp->stencil_box[(size_t(s) * ns + t) * 4];
+        if (b[0] <= b[1]) boxmax += int64_t(b[1] - b[0] + 1) * (b[3] - b[2] + 1);
+      }
+      int64_t dmax = std::min(maxD2, boxmax);
+      S.wk_offY = al(maxX);
+      S.wk_offD = S.wk_offY + al(maxY2);
+      S.wk_offStage = S.wk_offD + al(dmax);
+      S.wk_scratch = S.wk_offStage + al(P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb);
+      if (ok && S.wk_scratch * rb <= 200 * 1024) S.wk_ok = 1;
+    }
   }
 
   // shard: contiguous unit ranges with equal algorithmic cost (units in Λ order)

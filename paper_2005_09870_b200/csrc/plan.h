@@ -14,7 +14,9 @@ struct Stencil {
 
 struct HostPlan {
   Plan P;
-  std::vector<Stencil> stencil;   // nsb × band_L (BAND only)
+  std::vector<Stencil> stencil;   // nsb × band_L (BAND only), each sub-band's entries sorted by (sb, o0, o1)
+  std::vector<int> stencil_box;   // BAND: nsb × nsb × 4 (omin0, omax0, omin1, omax1) of μ-sub-band × λ-sub-band
+                                  //       (omin > omax: no entry)
   int real_bytes = 4;             // compute precision
   int out_bytes = 4;              // stored value precision
   int64_t row0 = 0, row1 = 0;     // shard

@@ -44,6 +44,11 @@ class Problem:
     dtypes: tuple = ("f64",)
     meta: dict = field(default_factory=dict)
 
+    def __post_init__(self):
+        self.u = np.ascontiguousarray(self.u, dtype=np.float64)
+        self.v = np.ascontiguousarray(self.v, dtype=np.float64)
+        self.h = np.ascontiguousarray(self.h, dtype=np.float64)
+
     @property
     def m(self) -> int:
         return self.u.shape[0]

@@ -29,8 +29,8 @@ def _gpu():
 
 
 def run(p, dtype, world=1, rank=0, host_inputs=False, retain=None):
-    u = p.u if host_inputs else torch.from_numpy(p.u).cuda()
-    v = p.v if host_inputs else torch.from_numpy(p.v).cuda()
+    u = p.u if host_inputs else torch.from_numpy(np.ascontiguousarray(p.u)).cuda()
+    v = p.v if host_inputs else torch.from_numpy(np.ascontiguousarray(p.v)).cuda()
     dec = Decomposition(Spec(p.d, p.n, p.J, p.h, u, v, dtype=dtype, retain=retain or p.retain,
                              tau_rel=p.tau_rel, band_L=p.band_L, rank=rank, world=world))
     dec.decompose()
