@@ -128,7 +128,8 @@ int build_templates(Handle* h, cudaStream_t st) {
     } else {
       A.toff[1] = P.sb[sb_index(1, P.J, lev, 1)].toff;
     }
-    A.tstride = int64_t(A.Wout[0]) * A.Wout[1];
+    A.trs = A.Wout[1] >= P.n ? A.Wout[1] : (A.Wout[1] + 3) / 4 * 4;
+    A.tstride = int64_t(A.Wout[0]) * A.trs;
     CK(launch_tmpl_level(P, A, hp.real_bytes, lev, st));
     h->nlaunch += P.d == 2 ? 2 : 1;
     cur ^= 1;
@@ -179,9 +180,9 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
         CK(cudaMemcpy(c, dbg, sizeof(c), cudaMemcpyDeviceToHost));
         double tot = 0;
         for (int i = 2; i < 8; ++i) tot += double(c[i]);
-        fprintf(stderr, "[pcwd tile] level %d G %d grid %d smem %zu: geom %.1f%% ksum %.1f%% passA %.1f%% passB %.1f%% gather %.1f%% write %.1f%%\n",
+        fprintf(stderr, "[pcwd tile] level %d G %d grid %d smem %zu: geom %.1f%% ksum %.1f%% cascade %.1f%% gather+write %.1f%%\n",
                 P.sb[find_subband(P, L.u0)].level, L.ta.G, L.grid, L.smem, 100 * c[2] / tot, 100 * c[3] / tot,
-                100 * c[4] / tot, 100 * c[5] / tot, 100 * c[6] / tot, 100 * c[7] / tot);
+                100 * c[4] / tot, 100 * c[5] / tot);
         cudaFree(dbg);
       }
       continue;
@@ -423,16 +424,44 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           dmax = std::max(dmax, area);
         }
       }
+      // D keeps every step's boxes (gather at the end): total stencil box area of the sub-band
+      dmax = 0;
+      for (int q = s; q < e; ++q) {
+        int64_t area = 0;
+        for (int t = 0; t < P.nsb; ++t) {
+          const int* b = &h->hp.stencil_box[(size_t(q) * P.nsb + t) * 4];
+          if (b[0] <= b[1]) area += int64_t(b[1] - b[0] + 1) * (b[3] - b[2] + 1);
+        }
+        dmax = std::max(dmax, area);
+      }
       dmax = (dmax + VW - 1) / VW * VW;
       int64_t stage = P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb;
-      int64_t per_unit = int64_t(XR) * XS + int64_t(YR) * YS + dmax + stage;
-      per_unit = (per_unit + VW - 1) / VW * VW;
-      int G = lev == 1 ? 8 : lev == 2 ? 4 : lev == 3 ? 2 : 1;
+      const int SL = 32;   // kSL of band_tile.cu
+      const int64_t Xsz = int64_t(XR) * XS + 2 * SL, Ysz = int64_t(YR) * YS + 2 * SL;
+      const int64_t Dsz = (dmax + stage + VW - 1) / VW * VW;
+      int G = lev == 1 ? 4 : lev <= 3 ? 2 : 1;
       const int nl = P.sb[s].nl;
-      while (G > 1 && (size_t(G) * per_unit * rb > budget || nl % G)) G >>= 1;
       const size_t st_bytes = size_t(e - s) * P.band_L * sizeof(int4);
-      while (G > 1 && size_t(G) * per_unit * rb + st_bytes > budget) G >>= 1;
-      size_t smem = size_t(G) * per_unit * rb + st_bytes;
+      auto layout = [&](int g, int64_t* regY, int64_t* regD, int64_t* regEnd, int* TS, int* VS, int* RC) {
+        const int step = 1 << lev;
+        const int groups = (W1 + 3) / 4;
+        *RC = std::max(1, std::min(W0, (2 * 256) / groups));
+        *TS = (W1 + 3) / 4 * 4;
+        *VS = (W1 + (g - 1) * step + 3 + 4) / 4 * 4;
+        const int64_t stg = 2 * int64_t(*RC) * (*TS + *VS);
+        *regY = g * Xsz;
+        *regD = *regY + std::max<int64_t>(g * Ysz, stg);
+        *regD = (*regD + VW - 1) / VW * VW;
+        *regEnd = *regD + g * Dsz;
+        *regEnd = (*regEnd + 3) / 4 * 4;
+        return size_t(*regEnd) * rb + st_bytes;
+      };
+      int64_t regY = 0, regD = 0, regEnd = 0;
+      int TS = 0, VS = 0, RC = 0;
+      const size_t two_per_sm = 110 * 1024;
+      while (G > 1 && (layout(G, &regY, &regD, &regEnd, &TS, &VS, &RC) > two_per_sm || nl % G)) G >>= 1;
+      size_t smem = layout(G, &regY, &regD, &regEnd, &TS, &VS, &RC);
+      int64_t per_unit = Xsz + Ysz + Dsz;
       if (smem <= budget && nl % G == 0) {
         // whole rounds of G units inside [u0, u1); the ragged ends go to the generic kernel
         int64_t a0 = (u0 + G - 1) / G * G, a1 = u1 / G * G;
@@ -452,6 +481,15 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           T.ta.YR = YR;
           T.ta.DMAX = int(dmax);
           T.ta.per_unit = int(per_unit);
+          T.ta.Xsz = int(Xsz);
+          T.ta.Ysz = int(Ysz);
+          T.ta.Dsz = int(Dsz);
+          T.ta.regY = regY;
+          T.ta.regD = regD;
+          T.ta.regEnd = regEnd;
+          T.ta.TS = TS;
+          T.ta.VS = VS;
+          T.ta.RC = RC;
           add_generic(u0, a0, scr);
           h->launches.push_back(T);
           add_generic(a1, u1, scr);

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kB) bk_ksum(const __grid_constant__ Plan P, co
   const Real* __restrict__ T = reinterpret_cast<const Real*>(A.T) + S.toff;
   const int n = P.n, mask = n - 1;
   const bool f0 = S.tW[0] >= n, f1 = S.tW[1] >= n;
-  const int tw1 = f1 ? n : S.tW[1];
+  const int tw1 = S.tRS;
   for (int idx = blockIdx.x * kB + threadIdx.x; idx < total; idx += gridDim.x * kB) {
     const int i0 = idx / r1.len, i1 = idx - i0 * r1.len;
     const int y0 = (r0.lo + i0) & mask, y1 = (r1.lo + i1) & mask;
@@ -73,78 +73,96 @@ __global__ void __launch_bounds__(kB) bk_ksum(const __grid_constant__ Plan P, co
   }
 }
 
-// pass A of step s: Y[i0][j] = Σ_t f_{e1}[t] X[i0][2 l + o_{e1} + t], j over (approx cols, detail cols)
+// Only the approximation chain is carried through the whole window (the stencil's coarse
+// partners need all of it); the stencil's detail coefficients are computed directly in
+// bk_gather from the step's input window (2δ × 2δ taps each).
+//
+// 4 consecutive outputs along a line from a window `in` stored contiguously (stride `st`
+// between consecutive samples): out[q] = Σ_t f[t] x[2(lo+j0+q) + t]; contiguous fast path,
+// periodic (full-line or wrapping) slow path.
+template <typename Real>
+__device__ __forceinline__ void line4(const Plan& P, const Real* __restrict__ x, int64_t st, const Range& in,
+                                      int pos0, int nout, Real out[4]) {
+  const int L2 = P.L2;
+  int d = (2 * pos0 - in.lo) & (in.nl - 1);            // local index of the first tap, mod nl
+  if (d > in.nl / 2) d -= in.nl;
+  const bool fast = in.len < in.nl && d >= 0 && d + 2 * (nout - 1) + L2 <= in.len;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) out[q] = Real(0);
+  if (fast) {
+    const Real* xp = x + int64_t(d) * st;
+    for (int t = 0; t < L2; ++t) {
+      const Real f = TapsOf<Real>::get(P, 0, t);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) out[q] = fmaB(f, xp[int64_t(2 * q + t) * st], out[q]);
+    }
+  } else {
+    for (int q = 0; q < nout; ++q)
+      for (int t = 0; t < L2; ++t) {
+        const int li = local_index(in, 2 * (pos0 + q) + t);
+        if (li >= 0) out[q] = fmaB(TapsOf<Real>::get(P, 0, t), x[int64_t(li) * st], out[q]);
+      }
+  }
+}
+
+// pass A of step s (approximation along axis 1): Y[i0][jj], jj < a1.len
 template <typename Real>
 __global__ void __launch_bounds__(kB) bk_passA(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
                                                int s) {
   const int64_t unit = A.u0 + blockIdx.y;
   const UnitPos up = unit_pos(P, unit);
   const SubBand& S = P.sb[up.sbi];
+  if (!(s < S.steps || s == P.J)) return;
   Range in0, in1;
   step_in(P, S, up, s, in0, in1);
-  const Range a1 = step_out(in1, P.L2, 0), d1 = step_out(in1, P.L2, 1);
-  const int ycols = a1.len + d1.len;
-  const int total = in0.len * ycols;
+  const Range a1 = step_out(in1, P.L2, 0);
+  const int ng = (a1.len + 3) >> 2;
+  const int total = in0.len * ng;
   Real* base = reinterpret_cast<Real*>(A.scratch) + int64_t(blockIdx.y) * A.stride;
   const Real* X = base + ((s & 1) ? S.offX0 : S.offX1);
   Real* Y = base + S.offY;
   for (int idx = blockIdx.x * kB + threadIdx.x; idx < total; idx += gridDim.x * kB) {
-    const int i0 = idx / ycols, j = idx - i0 * ycols;
-    const int e1 = j >= a1.len;
-    const int jj = e1 ? j - a1.len : j;
-    const Range& R = e1 ? d1 : a1;
-    const int q = 2 * (R.lo + jj) + P.to[e1];
-    const Real* line = X + int64_t(i0) * in1.len;
-    Real acc = Real(0);
-    for (int t = 0; t < P.L2; ++t) {
-      const int c = local_index(in1, q + t);
-      if (c >= 0) acc = fmaB(TapsOf<Real>::get(P, e1, t), line[c], acc);
-    }
-    Y[idx] = acc;
+    const int i0 = idx / ng, g = idx - i0 * ng;
+    const int jj = 4 * g, nout = min(4, a1.len - jj);
+    Real out[4];
+    line4<Real>(P, X + int64_t(i0) * in1.len, 1, in1, a1.lo + jj, nout, out);
+    Real* yd = Y + int64_t(i0) * a1.len + jj;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < nout) yd[q] = out[q];
   }
 }
 
-// pass B of step s: approximation -> the other X buffer; details -> D (3 windows)
+// pass B of step s (approximation along axis 0): next X = a0 × a1
 template <typename Real>
 __global__ void __launch_bounds__(kB) bk_passB(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
                                                int s) {
   const int64_t unit = A.u0 + blockIdx.y;
   const UnitPos up = unit_pos(P, unit);
   const SubBand& S = P.sb[up.sbi];
+  if (!(s < S.steps || s == P.J)) return;
   Range in0, in1;
   step_in(P, S, up, s, in0, in1);
-  const Range a0 = step_out(in0, P.L2, 0), d0 = step_out(in0, P.L2, 1);
-  const Range a1 = step_out(in1, P.L2, 0), d1 = step_out(in1, P.L2, 1);
-  const int ycols = a1.len + d1.len;
-  const int s00 = a0.len * a1.len, s01 = a0.len * d1.len, s10 = d0.len * a1.len, s11 = d0.len * d1.len;
-  const bool need_approx = s < S.steps || s == P.J;
-  const int total = (need_approx ? s00 : 0) + s01 + s10 + s11;
+  const Range a0 = step_out(in0, P.L2, 0), a1 = step_out(in1, P.L2, 0);
+  const int ng = (a0.len + 3) >> 2;
+  const int total = ng * a1.len;
   Real* base = reinterpret_cast<Real*>(A.scratch) + int64_t(blockIdx.y) * A.stride;
   const Real* Y = base + S.offY;
   Real* Xn = base + ((s & 1) ? S.offX1 : S.offX0);
-  Real* Dd = base + S.offD;
-  const int skip = need_approx ? 0 : s00;
-  for (int idx0 = blockIdx.x * kB + threadIdx.x; idx0 < total; idx0 += gridDim.x * kB) {
-    const int idx = idx0 + skip;
-    int e0, e1, j0, j1, rem;
-    Real* dst;
-    if (idx < s00) { e0 = 0; e1 = 0; rem = idx; j0 = rem / a1.len; j1 = rem - j0 * a1.len; dst = Xn + rem; }
-    else if (idx < s00 + s01) { e0 = 0; e1 = 1; rem = idx - s00; j0 = rem / d1.len; j1 = rem - j0 * d1.len; dst = Dd + rem; }
-    else if (idx < s00 + s01 + s10) { e0 = 1; e1 = 0; rem = idx - s00 - s01; j0 = rem / a1.len; j1 = rem - j0 * a1.len; dst = Dd + s01 + rem; }
-    else { e0 = 1; e1 = 1; rem = idx - s00 - s01 - s10; j0 = rem / d1.len; j1 = rem - j0 * d1.len; dst = Dd + s01 + s10 + rem; }
-    const Range& R = e0 ? d0 : a0;
-    const int q = 2 * (R.lo + j0) + P.to[e0];
-    const int colY = (e1 ? a1.len : 0) + j1;
-    Real acc = Real(0);
-    for (int t = 0; t < P.L2; ++t) {
-      const int r = local_index(in0, q + t);
-      if (r >= 0) acc = fmaB(TapsOf<Real>::get(P, e0, t), Y[int64_t(r) * ycols + colY], acc);
-    }
-    *dst = acc;
+  for (int idx = blockIdx.x * kB + threadIdx.x; idx < total; idx += gridDim.x * kB) {
+    const int g = idx / a1.len, j1 = idx - g * a1.len;
+    const int j0 = 4 * g, nout = min(4, a0.len - j0);
+    Real out[4];
+    line4<Real>(P, Y + j1, a1.len, in0, a0.lo + j0, nout, out);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q < nout) Xn[int64_t(j0 + q) * a1.len + j1] = out[q];
   }
 }
 
-// gather the stencil entries of level s (details; the coarse block at s == J) into the stage
+// gather the stencil entries of level s: details computed directly from the step's input
+// window X (level s-1): d(l0,l1) = Σ_{t0,t1} f_{e0}[t0] f_{e1}[t1] X[2l0+o_{e0}+t0][2l1+o_{e1}+t1];
+// the coarse block (e = 0, s = J) is read from the approximation output.
 template <typename Real>
 __global__ void __launch_bounds__(kB) bk_gather(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
                                                 int s) {
@@ -153,15 +171,14 @@ __global__ void __launch_bounds__(kB) bk_gather(const __grid_constant__ Plan P, 
   const SubBand& S = P.sb[up.sbi];
   Range in0, in1;
   step_in(P, S, up, s, in0, in1);
-  const Range a0 = step_out(in0, P.L2, 0), d0 = step_out(in0, P.L2, 1);
-  const Range a1 = step_out(in1, P.L2, 0), d1 = step_out(in1, P.L2, 1);
-  const int s01 = a0.len * d1.len, s10 = d0.len * a1.len;
+  const Range a0 = step_out(in0, P.L2, 0), a1 = step_out(in1, P.L2, 0);
   Real* base = reinterpret_cast<Real*>(A.scratch) + int64_t(blockIdx.y) * A.stride;
-  const Real* Dd = base + S.offD;
+  const Real* X = base + ((s & 1) ? S.offX0 : S.offX1);
   const Real* Xn = base + ((s & 1) ? S.offX1 : S.offX0);
   Real* sv = base + S.offStage;
   int* sc = reinterpret_cast<int*>(sv + P.band_Lpad);
   const int4* st = A.stencil + S.stencil_off;
+  const int L2 = P.L2;
   for (int j = blockIdx.x * kB + threadIdx.x; j < P.band_Lpad; j += gridDim.x * kB) {
     if (j >= P.band_L) {
       if (s == 1) { sc[j] = INT_MAX; sv[j] = Real(0); }
@@ -175,14 +192,24 @@ __global__ void __launch_bounds__(kB) bk_gather(const __grid_constant__ Plan P, 
     else if (L.level < S.level) { b0 = up.p0 << (S.level - L.level); b1 = up.p1 << (S.level - L.level); }
     else { b0 = up.p0 >> (L.level - S.level); b1 = up.p1 >> (L.level - S.level); }
     const int l0 = (b0 + e.y) & (L.nl - 1), l1 = (b1 + e.z) & (L.nl - 1);
-    const Real* buf;
-    Range w0, w1;
-    if (L.e == 0) { buf = Xn; w0 = a0; w1 = a1; }
-    else if (L.e == 1) { buf = Dd; w0 = a0; w1 = d1; }
-    else if (L.e == 2) { buf = Dd + s01; w0 = d0; w1 = a1; }
-    else { buf = Dd + s01 + s10; w0 = d0; w1 = d1; }
-    const int li0 = local_index(w0, l0), li1 = local_index(w1, l1);
-    sv[j] = (li0 >= 0 && li1 >= 0) ? buf[int64_t(li0) * w1.len + li1] : Real(0);
+    Real val = Real(0);
+    if (L.e == 0) {
+      const int li0 = local_index(a0, l0), li1 = local_index(a1, l1);
+      if (li0 >= 0 && li1 >= 0) val = Xn[int64_t(li0) * a1.len + li1];
+    } else {
+      const int e0 = L.e0, e1 = L.e1;
+      for (int t0 = 0; t0 < L2; ++t0) {
+        const int r = local_index(in0, 2 * l0 + P.to[e0] + t0);
+        if (r < 0) continue;
+        Real row = Real(0);
+        for (int t1 = 0; t1 < L2; ++t1) {
+          const int c = local_index(in1, 2 * l1 + P.to[e1] + t1);
+          if (c >= 0) row = fmaB(TapsOf<Real>::get(P, e1, t1), X[int64_t(r) * in1.len + c], row);
+        }
+        val = fmaB(TapsOf<Real>::get(P, e0, t0), row, val);
+      }
+    }
+    sv[j] = val;
     sc[j] = int(L.offset + int64_t(l0) * L.nl + l1);
   }
 }
@@ -240,8 +267,8 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
     bk_ksum<Real><<<dim3(gx(maxX0), nb), kB, 0, st>>>(P, A);
     ++*launches;
     for (int s = 1; s <= steps; ++s) {
-      bk_passA<Real><<<dim3(gx(maxY), nb), kB, 0, st>>>(P, A, s);
-      bk_passB<Real><<<dim3(gx(maxB), nb), kB, 0, st>>>(P, A, s);
+      bk_passA<Real><<<dim3(gx(maxY / 8), nb), kB, 0, st>>>(P, A, s);
+      bk_passB<Real><<<dim3(gx(maxB / 16), nb), kB, 0, st>>>(P, A, s);
       bk_gather<Real><<<dim3(1, nb), kB, 0, st>>>(P, A, s);
       *launches += 3;
     }

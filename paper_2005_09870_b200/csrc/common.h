@@ -83,7 +83,8 @@ struct SubBand {
   // convolved template T_{k,s} = ũ_k ⋆ ψ_{s,0}: window per axis (tW == n ⇒ whole line, tS = 0)
   int tS[2], tW[2];
   int64_t toff;     // template buffer offset of k = 0 (elements); k-th at toff + k * tstride
-  int64_t tstride;
+  int64_t tstride;  // = tW[0] * tRS
+  int tRS;          // template row stride (tW[1] rounded up to 4 unless the row is a whole line)
   // per-unit scratch layout (elements of the compute type)
   int64_t offX0, offX1, offY, offD, offStage, scratch;
   int stencil_off;  // BAND: first entry of this sub-band's stencil

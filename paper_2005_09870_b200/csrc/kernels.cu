@@ -105,9 +105,9 @@ __global__ void tmpl_passB(const __grid_constant__ Plan P, const __grid_constant
       acc = fma(P.td[e0][j], win_read(col, y0 - A.dil * (P.to[e0] + j), A.Sin[0], Win0, mask, Wout1), acc);
     if (ec == 0) {
       A.phi_out[k * per + r] = acc;
-      if (level == coarse_level && A.toff[0] >= 0) T[A.toff[0] + k * A.tstride + r] = Real(acc);
+      if (level == coarse_level && A.toff[0] >= 0) T[A.toff[0] + k * A.tstride + int64_t(j0) * A.trs + j1] = Real(acc);
     } else if (A.toff[ec] >= 0) {
-      T[A.toff[ec] + k * A.tstride + r] = Real(acc);
+      T[A.toff[ec] + k * A.tstride + int64_t(j0) * A.trs + j1] = Real(acc);
     }
   }
 }
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
       const Real* __restrict__ T = reinterpret_cast<const Real*>(A.T) + S.toff;
       const bool f0 = D == 2 && S.tW[0] >= n;
       const bool f1 = S.tW[1] >= n;
-      const int tw1 = f1 ? n : S.tW[1];
+      const int tw1 = S.tRS;
       const int total = r0.len * r1.len;
       for (int idx = tid; idx < total; idx += kBlock) {
         const int i0 = idx / r1.len, i1 = idx - i0 * r1.len;

@@ -37,7 +37,10 @@ struct TileArgs {
   int XS, YS;               // row strides of X and Yt (elements)
   int XR, YR;               // max rows of X and Yt
   int DMAX;                 // D buffer elements per unit
-  int per_unit;             // scratch elements per unit
+  int per_unit;             // (unused by the kernel)
+  int Xsz, Ysz, Dsz;        // per-unit region sizes (elements)
+  int64_t regY, regD, regEnd;  // region offsets of the CTA scratch layout (elements)
+  int TS, VS, RC;           // k-sum staging: T / v tile row strides, rows per chunk
   unsigned long long* dbg;  // optional per-phase clock counters (PCWD_DEBUG_PHASES)
 };
 
@@ -70,6 +73,7 @@ struct TmplArgs {
   int dil;                  // 2^{ℓ-1}
   int64_t toff[4];          // destination offset per orientation code (-1 = not stored)
   int64_t tstride;          // per-k stride of the destination sub-band templates
+  int trs;                  // row stride of the destination templates
 };
 
 // dtype-dispatching launchers; return cudaError_t of the launch

@@ -277,7 +277,8 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
       S.tW[a] = w.W;
       S.tSu[a] = -P.zhi[a] + (e_a ? (1 << (lev - 1)) * (2 - L2) : 0);
     }
-    S.tstride = int64_t(S.tW[0]) * S.tW[1];
+    S.tRS = S.tW[1] >= n ? S.tW[1] : (S.tW[1] + 3) / 4 * 4;
+    S.tstride = int64_t(S.tW[0]) * S.tRS;
     S.toff = toff;
     toff += S.tstride * P.m;
     toff = (toff + 3) & ~int64_t(3);
