@@ -160,14 +160,8 @@ class Decomposition:
     def decompose_distributed(self, stream: int = 0):
         """Multi-process decompose: the threshold rule's one exchange is a MAX all-reduce of
         the per-rank maxima (torch.distributed, NCCL on GPUs); band/full need none."""
-        import torch
-        import torch.distributed as dist
         if self.spec.retain == "threshold" and self.spec.world > 1:
-            m = self.local_max(stream)
-            dev = torch.device("cuda", self.spec.device) if dist.get_backend() == "nccl" else torch.device("cpu")
-            t = torch.tensor([m], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            self.set_global_max(float(t.item()))
+            self.set_global_max(allreduce_max(self.local_max(stream), self.spec.device))
         self.decompose(stream)
 
     # -- results ------------------------------------------------------------------------
@@ -227,6 +221,28 @@ class Decomposition:
             self.close()
         except Exception:
             pass
+
+
+# ---- multi-process plumbing (torch.distributed; NCCL on GPUs, gloo in the CPU tests) ----------
+
+def allreduce_max(x: float, device: int = 0) -> float:
+    """MAX over ranks of one fp64 scalar — the threshold rule's only exchange."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", device) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(x: float, device: int = 0) -> float:
+    """SUM over ranks of one fp64 scalar (e.g. retained entries of all shards)."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", device) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 # ---- host-only plan queries (no GPU) ---------------------------------------------------------

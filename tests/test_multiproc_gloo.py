@@ -1,0 +1,67 @@
+"""World-size-2 multi-process checks of the N > 1 host path on CPU (gloo backend, no GPU).
+
+The data path has no collective (units are independent); what crosses ranks is
+(a) the cost-balanced shard plan each rank derives on its own, which must partition Λ, (b) the
+threshold rule's MAX all-reduce of the per-rank maxima (P:1179 threshold, reading R15), and
+(c) the bench's max-over-ranks timing and sum of retained entries.  The per-rank maxima here come
+from the oracle (the GPU computes them in the real run) — the exchange is what is tested.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, out):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import operator as op
+        from paper_2005_09870_b200 import pcwd as P
+        from synth import configs as C
+        p = C.micro(16, 2, 4, 3, 2, 2, 31, retain="threshold", tau_rel=1e-4)
+        spec = P.Spec(p.d, p.n, p.J, p.h, p.u, p.v, dtype="f64", retain="threshold", tau_rel=1e-4,
+                      rank=rank, world=world)
+        r0, r1 = P.plan_shard(spec)
+        T = op.theta_dense(p)
+        local = float(np.abs(T[r0:r1]).max()) if r1 > r0 else 0.0
+        M = P.allreduce_max(local)
+        nnz_local = int(np.count_nonzero(np.abs(T[r0:r1]) >= 1e-4 * M))
+        nnz_all = P.allreduce_sum(nnz_local)
+        t_all = P.allreduce_max(float(rank + 1))          # bench: max over ranks of the step time
+        out[rank] = (r0, r1, M, nnz_all, t_all, float(np.abs(T).max()),
+                     int(np.count_nonzero(np.abs(T) >= 1e-4 * np.abs(T).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_world2_shards_and_threshold_exchange(world):
+    from paper_2005_09870_b200 import _build
+    _build.build()
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    res = [out[r] for r in range(world)]
+    assert res[0][0] == 0 and res[-1][1] == 256
+    for a, b in zip(res, res[1:]):
+        assert a[1] == b[0]
+    for r in res:
+        assert r[2] == r[5]               # all-reduced max = global max of Θ
+        assert r[3] == r[6]               # summed shard counts = global retained count
+        assert r[4] == float(world)       # max over ranks
