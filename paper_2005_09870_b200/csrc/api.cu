@@ -25,9 +25,14 @@ struct Launch {
   size_t smem;      // 0 ⇒ global scratch (generic kernel)
   int tile = 0;     // 1 ⇒ band_tile_kernel with the parameters below
   TileArgs ta{};
+  int fine = 0;     // 1 ⇒ fine_kernel (fine.cu) for level `level`
+  int level = 0;
+  int box[3] = {0, 0, 0};   // fine: TMA box rows R0, T box width TS, v box width VS
+  FineArgs fa{};
   int batched = 0;  // 1 ⇒ batched grid kernels (batched.cu)
   BatchArgs ba{};
   int64_t maxX0 = 0, maxY = 0, maxB = 0;
+  int64_t workA[kMaxJ + 1] = {}, workB[kMaxJ + 1] = {};   // batched: per-step work items of pass A / B
   int steps = 0;
 };
 
@@ -41,6 +46,9 @@ struct Handle {
   double* Ytmp = nullptr;
   int4* stencil_d = nullptr;
   int4* box_d = nullptr;
+  FGeom* fgeom_d = nullptr;
+  void* vpad_d = nullptr;   // periodically padded v (fine path TMA source)
+  int vpad = 0;
   void* gscratch = nullptr;
   int64_t gstride = 0;
   void* bscratch = nullptr;
@@ -89,7 +97,7 @@ bool is_device_ptr(const void* p) {
 }
 
 void free_all(Handle* h) {
-  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->gscratch, h->bscratch,
+  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->gscratch, h->bscratch,
                   h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -98,6 +106,30 @@ void free_all(Handle* h) {
 template <typename T>
 cudaError_t dalloc(T** p, size_t bytes) {
   return cudaMalloc(reinterpret_cast<void**>(p), bytes < 16 ? 16 : bytes);
+}
+
+// 3-D tiled TMA descriptor over a row-major (z, y, x) array of rb-byte reals: extents (dx, dy, dz), strides in
+// elements (sy, sz), box (bx, by, 1), out-of-range elements read as zero.  Returns 0 or the CUresult.
+int encode_map3(CUtensorMap* map, void* base, int rb, int64_t dx, int64_t dy, int64_t dz, int64_t sy, int64_t sz, int bx,
+                int by) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p) return -1;
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  const cuuint64_t dims[3] = {cuuint64_t(dx), cuuint64_t(dy), cuuint64_t(dz)};
+  const cuuint64_t strides[2] = {cuuint64_t(sy * rb), cuuint64_t(sz * rb)};
+  const cuuint32_t box[3] = {cuuint32_t(bx), cuuint32_t(by), 1u};
+  const cuuint32_t es[3] = {1u, 1u, 1u};
+  CUresult r = fn(map, rb == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return int(r);
 }
 
 // Templates T_{k,s} for every sub-band (a1).
@@ -151,8 +183,36 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
       B.col = h->col;
       B.val = h->val;
       int nl = 0;
-      CK(launch_band_batched(P, B, h->hp.real_bytes, L.maxX0, L.maxY, L.maxB, L.steps, st, &nl));
+      CK(launch_band_batched(P, B, h->hp.real_bytes, L.maxX0, L.workA, L.workB, L.steps, st, &nl));
       h->nlaunch += nl;
+      continue;
+    }
+    if (L.fine) {
+      if (mode != MODE_BAND) return fail(PCWD_E_STATE, "fine launch outside BAND mode");
+      FineArgs F = L.fa;
+      F.v = h->v_d;
+      F.T = h->T_d;
+      F.stencil = h->stencil_d;
+      F.geom = h->fgeom_d;
+      F.row0 = h->hp.row0;
+      F.col = h->col;
+      F.val = h->val;
+      static const bool dbg_on = getenv("PCWD_DEBUG_PHASES") != nullptr;
+      unsigned long long* dbg = nullptr;
+      if (dbg_on) {
+        CK(cudaMalloc(&dbg, 2 * sizeof(unsigned long long)));
+        CK(cudaMemset(dbg, 0, 2 * sizeof(unsigned long long)));
+      }
+      F.dbg = dbg;
+      CK(launch_fine(P, F, h->hp.real_bytes, L.level, L.grid, L.smem, st));
+      h->nlaunch++;
+      if (dbg_on) {
+        unsigned long long c[2];
+        CK(cudaMemcpy(c, dbg, sizeof(c), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[pcwd fine] level %d grid %d: ksum %.1f%% cascade+gather %.1f%%\n", L.level, L.grid,
+                100.0 * c[0] / double(c[0] + c[1]), 100.0 * c[1] / double(c[0] + c[1]));
+        cudaFree(dbg);
+      }
       continue;
     }
     if (L.tile) {
@@ -358,6 +418,10 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     CKB(dalloc(&h->box_d, bx.size() * sizeof(int4)));
     CKB(cudaMemcpy(h->box_d, bx.data(), bx.size() * sizeof(int4), cudaMemcpyHostToDevice));
   }
+  if (!h->hp.fgeom.empty()) {
+    CKB(dalloc(&h->fgeom_d, h->hp.fgeom.size() * sizeof(FGeom)));
+    CKB(cudaMemcpy(h->fgeom_d, h->hp.fgeom.data(), h->hp.fgeom.size() * sizeof(FGeom), cudaMemcpyHostToDevice));
+  }
   int64_t gmax = 0;
   auto add_generic = [&](int64_t u0, int64_t u1, int64_t scr) {
     if (u1 <= u0) return;
@@ -388,6 +452,91 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     int64_t u0 = std::max(h->hp.row0, P.sb[s].offset);
     int64_t u1 = std::min(h->hp.row1, P.sb[e - 1].offset + P.sb[e - 1].count);
     if (u1 <= u0) { s = e; continue; }
+    // fine kernel (fine.cu): levels 1..3 whose every sub-band has a class geometry table
+    {
+      FineCfg fc{};
+      bool ok = P.retain == PCWD_RETAIN_BAND && P.d == 2 && fine_config(rb, lev, P.L2, &fc) && !getenv("PCWD_NO_FINE");
+      for (int q = s; q < e && ok; ++q) ok = P.sb[q].fg_m > 0 && P.sb[q].e != 0 && P.sb[q].nl % fc.GU == 0;
+      if (ok) {
+        const int VW = 16 / rb, SH = 1 << lev;
+        const SubBand& S0 = P.sb[s];
+        const int R0 = S0.tW[0], R1 = S0.tW[1];
+        for (int q = s; q < e; ++q) ok = ok && P.sb[q].tW[0] == R0 && P.sb[q].tW[1] == R1;
+        const int NZB = ((R1 + SH - 1) / SH + fc.GZ - 1) / fc.GZ;
+        ok = ok && int64_t(R0) * SH * NZB <= int64_t(fc.NT) * 256;
+        // strides: multiples of VW with an odd vector count (8 consecutive rows -> distinct bank groups)
+        auto odd_stride = [&](int w) { int x = (w + VW - 1) / VW * VW; if ((x / VW) % 2 == 0) x += VW; return x; };
+        int arl = 0, ycols = 0, dsz = 0;
+        for (int q = s; q < e && ok; ++q) {
+          const SubBand& Sq = P.sb[q];
+          for (int c = 0; c < Sq.fg_m * Sq.fg_m; ++c) {
+            const FGeom& g = h->hp.fgeom[Sq.fg_off + c];
+            dsz = std::max(dsz, g.dsize);
+            for (int st = 0; st < g.steps; ++st) {
+              arl = std::max(arl, g.st[st].arl);
+              ycols = std::max(ycols, g.st[st].hlen + g.st[st].glen);
+              // the approximations of steps ≥ 1 are stored in the unit's R region (row stride RS)
+              if (st > 0) ok = ok && g.st[st].xcl + VW - 1 <= ((R1 + VW - 1) / VW * VW) && g.st[st].xrl <= R0;
+            }
+          }
+        }
+        const int RS = odd_stride(R1);
+        const int zmaxT = (SH - 1) + SH * fc.GZ * (NZB - 1) + SH * (fc.GZ - 1);
+        const int zmaxV = zmaxT + SH * (fc.GU - 1);
+        const int TS = odd_stride(std::max(S0.tRS, zmaxT + 1));
+        const int VS = odd_stride(VW - 1 + std::max(R1 + SH * (fc.GU - 1), zmaxV + 1));
+        const int YS = odd_stride(arl + VW - 1);
+        const int64_t lpad = P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb;
+        const int64_t YSZ = (std::max<int64_t>(int64_t(ycols) * YS, lpad) + VW - 1) / VW * VW;
+        const int64_t RSZ = int64_t(R0) * RS;
+        const int64_t DS = (dsz + VW - 1) / VW * VW;
+        const int SLK = 32;
+        const int64_t regR = SLK + fc.GU * RSZ + SLK;
+        const int al = 128 / rb;   // TMA destinations: 128-byte aligned boxes
+        const int TSZ = (R0 * TS + al - 1) / al * al, VSZ = (R0 * VS + al - 1) / al * al;
+        const int64_t stg = int64_t(fc.NST) * (TSZ + VSZ) + al;
+        const int64_t regS = SLK + std::max<int64_t>(stg, fc.CG * YSZ) + SLK;
+        const int64_t regD = regR + regS;
+        const size_t smem = size_t(regD + fc.CG * DS) * rb;
+        ok = ok && smem + 1024 <= size_t(smem_optin > 0 ? smem_optin : 48 * 1024);
+        int64_t a0 = (u0 + fc.GU - 1) / fc.GU * fc.GU, a1 = u1 / fc.GU * fc.GU;
+        if (getenv("PCWD_DEBUG_PLAN"))
+          fprintf(stderr, "[pcwd fine] level %d ok %d GU %d R %dx%d RS %d TS %d VS %d YS %d ycols %d arl %d dsz %d "
+                  "regR %lld stg %lld yt %lld smem %zu\n", lev, int(ok), fc.GU, R0, R1, RS, TS, VS, YS, ycols, arl, dsz,
+                  (long long)regR, (long long)stg, (long long)(fc.CG * YSZ), smem);
+        if (ok && a1 > a0) {
+          Launch F{a0, a1, 0, 0};
+          F.fine = 1;
+          F.level = lev;
+          F.smem = smem;
+          const int per_sm = int(std::max<size_t>(1, std::min<size_t>(2, (228 * 1024) / (smem + 1024))));
+          F.grid = int(std::min<int64_t>((a1 - a0) / fc.GU, int64_t(nsm) * per_sm));
+          FineArgs& A = F.fa;
+          A.u0 = a0; A.u1 = a1;
+          A.regS = regR; A.regD = regD;
+          A.TSZ = TSZ; A.VSZ = VSZ;
+          A.sb_first = s;
+          // halo of the padded v that every round's boxes stay inside
+          int tmin0 = 1 << 30, tmax0 = -(1 << 30), tmin1 = 1 << 30, tmax1 = -(1 << 30);
+          for (int q = s; q < e; ++q) {
+            tmin0 = std::min(tmin0, P.sb[q].tSu[0]); tmax0 = std::max(tmax0, P.sb[q].tSu[0]);
+            tmin1 = std::min(tmin1, P.sb[q].tSu[1]); tmax1 = std::max(tmax1, P.sb[q].tSu[1]);
+          }
+          const int nl = S0.nl;
+          auto fl = [&](int x) { return x >= 0 ? x / VW * VW : -((-x + VW - 1) / VW) * VW; };
+          const int need = std::max({-tmin0, -fl(tmin1), ((nl - 1) << lev) + tmax0 + R0 - P.n,
+                                     fl(((nl - fc.GU) << lev) + tmax1) + VS - P.n, 0});
+          h->vpad = std::max(h->vpad, (need + 3) / 4 * 4);
+          F.box[0] = R0; F.box[1] = TS; F.box[2] = VS;
+          A.RS = RS; A.RSZ = int(RSZ); A.TS = TS; A.VS = VS; A.YS = YS; A.YSZ = int(YSZ); A.DS = int(DS);
+          add_generic(u0, a0, scr);
+          h->launches.push_back(F);
+          add_generic(a1, u1, scr);
+          s = e;
+          continue;
+        }
+      }
+    }
     Launch T{0, 0, 0, 0};
     if (tile_ok && !getenv("PCWD_NO_TILE")) {
       // per-unit scratch of the tile kernel: X (R window and approximations), Yt, D boxes, stage
@@ -503,7 +652,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       Launch B{u0, u1, 0, 0};
       B.batched = 1;
       int64_t stride = (scr + 31) & ~int64_t(31);
-      const size_t cap = size_t(8) << 30;
+      // batch so that the per-unit slots stay L2-resident next to v and the templates
+      static const size_t cap = size_t(getenv("PCWD_BATCH_MB") ? atol(getenv("PCWD_BATCH_MB")) : 8192) << 20;
       int64_t batch = std::max<int64_t>(1, std::min<int64_t>(u1 - u0, int64_t(cap / (size_t(stride) * rb))));
       batch = std::min<int64_t>(batch, 65535);
       B.ba.stride = stride;
@@ -522,6 +672,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           int64_t o0 = step_out_maxlen(int(w0), int(nl0), P.L2), o1 = step_out_maxlen(int(w1), int(nl1), P.L2);
           my = std::max(my, w0 * 2 * o1);
           mb = std::max(mb, 4 * o0 * o1);
+          B.workA[st] = std::max(B.workA[st], w0 * ((o1 + 3) / 4));
+          B.workB[st] = std::max(B.workB[st], ((o0 + 3) / 4) * o1);
           w0 = o0; w1 = o1; nl0 >>= 1; nl1 >>= 1;
         }
       }
@@ -538,6 +690,27 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     s = e;
   }
   if (h->bscratch_bytes) CKB(dalloc(&h->bscratch, h->bscratch_bytes));
+  // fine path: periodically padded v (K1) and the TMA descriptors of every fine launch
+  bool any_fine = false;
+  for (const Launch& L : h->launches) any_fine = any_fine || L.fine;
+  if (any_fine) {
+    const int W = P.n + 2 * h->vpad;
+    CKB(dalloc(&h->vpad_d, size_t(P.m) * W * W * rb));
+    CKB(launch_pad_v(h->v_d, h->vpad_d, P.n, h->vpad, P.m, rb, 0));
+    CKB(cudaDeviceSynchronize());
+    for (Launch& L : h->launches) {
+      if (!L.fine) continue;
+      int rc2 = encode_map3(&L.fa.tmV, h->vpad_d, rb, W, W, P.m, int64_t(W), int64_t(W) * W, L.box[2], L.box[0]);
+      if (rc2) return bail(PCWD_E_CUDA, "cuTensorMapEncodeTiled (v) failed: " + std::to_string(rc2));
+      L.fa.vpad = h->vpad;
+      for (int q = L.fa.sb_first, i = 0; q < P.nsb && i < 3 && P.sb[q].level == L.level; ++q, ++i) {
+        const SubBand& Sq = P.sb[q];
+        rc2 = encode_map3(&L.fa.tmT[i], static_cast<char*>(h->T_d) + Sq.toff * rb, rb, Sq.tRS, Sq.tW[0], P.m, Sq.tRS,
+                          Sq.tstride, L.box[1], L.box[0]);
+        if (rc2) return bail(PCWD_E_CUDA, "cuTensorMapEncodeTiled (T) failed: " + std::to_string(rc2));
+      }
+    }
+  }
   if (gmax > 0) {
     h->gstride = (gmax + 31) & ~int64_t(31);
     CKB(dalloc(&h->gscratch, size_t(h->gstride) * h->ggrid * rb));

@@ -255,8 +255,8 @@ __global__ void __launch_bounds__(kB) bk_write(const __grid_constant__ Plan P, c
 // ----------------------------------------------------------------------------------- launcher
 
 template <typename Real>
-static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0, int64_t maxY, int64_t maxB,
-                               int steps, cudaStream_t st, int* launches) {
+static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0, const int64_t* workA,
+                               const int64_t* workB, int steps, cudaStream_t st, int* launches) {
   const int64_t units = A0.u1 - A0.u0;
   for (int64_t b0 = 0; b0 < units; b0 += A0.batch) {
     BatchArgs A = A0;
@@ -267,8 +267,8 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
     bk_ksum<Real><<<dim3(gx(maxX0), nb), kB, 0, st>>>(P, A);
     ++*launches;
     for (int s = 1; s <= steps; ++s) {
-      bk_passA<Real><<<dim3(gx(maxY / 8), nb), kB, 0, st>>>(P, A, s);
-      bk_passB<Real><<<dim3(gx(maxB / 16), nb), kB, 0, st>>>(P, A, s);
+      bk_passA<Real><<<dim3(gx(workA[s]), nb), kB, 0, st>>>(P, A, s);
+      bk_passB<Real><<<dim3(gx(workB[s]), nb), kB, 0, st>>>(P, A, s);
       bk_gather<Real><<<dim3(1, nb), kB, 0, st>>>(P, A, s);
       *launches += 3;
     }
@@ -281,10 +281,10 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
   return cudaSuccess;
 }
 
-cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, int64_t maxY,
-                                int64_t maxB, int steps, cudaStream_t st, int* launches) {
-  return real_bytes == 4 ? run_batch_t<float>(P, A, maxX0, maxY, maxB, steps, st, launches)
-                         : run_batch_t<double>(P, A, maxX0, maxY, maxB, steps, st, launches);
+cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, const int64_t* workA,
+                                const int64_t* workB, int steps, cudaStream_t st, int* launches) {
+  return real_bytes == 4 ? run_batch_t<float>(P, A, maxX0, workA, workB, steps, st, launches)
+                         : run_batch_t<double>(P, A, maxX0, workA, workB, steps, st, launches);
 }
 
 }  // namespace pcwd

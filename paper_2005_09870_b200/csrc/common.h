@@ -94,6 +94,7 @@ struct SubBand {
   int wk_ok;
   int64_t wk_offY, wk_offD, wk_offStage, wk_scratch;
   double fma;       // algorithmic FMA per unit (k-sum + cascade, max windows)
+  int fg_off, fg_m; // fine path: first geometry record of this sub-band, class modulus per axis (geom.h)
 };
 
 struct Plan {

@@ -1,0 +1,485 @@
+// fine.cu — band rule, fine levels (windows fit in shared memory): kernel K3f.
+//
+// One CTA (256 threads) processes rounds of GU units of one sub-band that are adjacent along axis 1
+// (positions p1 .. p1+GU-1 of one row p0; their R windows are shifted by 2^ℓ columns).
+//
+//   a2 k-sum    R_j(y) = Σ_k v_k(c_j + y) T_k(y) for the GU windows at once (k-sum fused
+//               before the cascade).  T_k and the v_k strip the GU windows read are staged in shared
+//               memory by cp.async, double-buffered over k.  A thread owns one template row r and GZ
+//               template columns z_i = res + 2^ℓ(zb·GZ + i) of one residue class mod 2^ℓ; unit j reads
+//               v at column z_i + 2^ℓ j = res + 2^ℓ(zb·GZ + i + j), so the GU·GZ products of one k need
+//               only GZ template values and GU+GZ-1 v values (register blocking along the shift).
+//   a3 cascade  one thread group per unit (warp at ℓ = 1), restricted to the stencil's needs (geom.h):
+//               pass A filters input rows along axis 1 into a transposed buffer, pass B filters those
+//               along axis 0; each task computes 8 consecutive outputs of one 2δ-tap filter from one run
+//               of 16-byte loads (taps are compile-time indices into the kernel-parameter bank).
+//   a4 gather   the stencil entries, written in CSR column order (rank sort when a partner wraps).
+//
+// Geometry comes from the host plan (one record per sub-band and class p mod 2^{steps-ℓ}, geom.h),
+// translated to the unit's position.
+#include <climits>
+
+#include "geom.h"
+#include "kernels.cuh"
+
+namespace pcwd {
+
+namespace {
+
+constexpr int kFT = 256;   // threads per CTA
+constexpr int kSlack = 32; // elements of slack before / after each region (vector over-reads)
+
+template <typename Real>
+struct FVec;
+template <>
+struct FVec<float> {
+  static constexpr int W = 4;
+  using T = float4;
+};
+template <>
+struct FVec<double> {
+  static constexpr int W = 2;
+  using T = double2;
+};
+
+__device__ __forceinline__ float ffma_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double ffma_(double a, double b, double c) { return fma(a, b, c); }
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (async proxy, TMA engine); completion counted on `bar` in bytes.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// 3-D tiled TMA load of one box of `map` at coordinates (x, y, z) into shared memory.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void bar_group(int id, int nthreads) {
+  if (nthreads == 32) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// 8 consecutive outputs out[q] = Σ_t f_TY[t] x[2(j0+q) + o_TY + t - base] of a row whose valid entries are
+// the local indices [vlo, vhi) (zero elsewhere).  Loads NV aligned vectors starting at align_down(s0);
+// `off` = s0 mod VW selects the register window.  Rows carry slack so the over-reads stay in bounds.
+template <typename Real, int L2, int TY>
+__device__ __forceinline__ void filt8(const Plan& P, const Real* __restrict__ row, int base, int j0, int nout,
+                                      int vlo, int vhi, Real out[8]) {
+  constexpr int VW = FVec<Real>::W;
+  constexpr int o = TY ? 2 - L2 : 0;
+  constexpr int SPAN = 14 + L2;                                 // inputs of 8 outputs
+  constexpr int NV = (SPAN + VW - 1 + VW - 1) / VW;            // vectors incl. misalignment
+  const int s0 = 2 * j0 + o - base;
+  const int a = s0 & ~(VW - 1);
+  const int off = s0 - a;
+  Real x[NV * VW];
+  const typename FVec<Real>::T* p = reinterpret_cast<const typename FVec<Real>::T*>(row + a);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const typename FVec<Real>::T t = p[i];
+    if constexpr (VW == 4) {
+      x[4 * i] = t.x; x[4 * i + 1] = t.y; x[4 * i + 2] = t.z; x[4 * i + 3] = t.w;
+    } else {
+      x[2 * i] = t.x; x[2 * i + 1] = t.y;
+    }
+  }
+  // zero the loaded values outside [vlo, vhi) that the nout needed outputs read
+  const int lo = vlo - a, hi = vhi - a;
+  if (lo > off || hi < off + 2 * (nout - 1) + L2) {
+#pragma unroll
+    for (int i = 0; i < NV * VW; ++i) x[i] = (i >= lo && i < hi) ? x[i] : Real(0);
+  }
+#define PCWD_FILT8(OFF)                                                                        \
+  _Pragma("unroll") for (int q = 0; q < 8; ++q) {                                              \
+    Real acc = Real(0);                                                                        \
+    _Pragma("unroll") for (int t = 0; t < L2; ++t) acc = ffma_(TapsOf<Real>::get(P, TY, t), x[(OFF) + 2 * q + t], acc); \
+    out[q] = acc;                                                                              \
+  }
+  if constexpr (VW == 4) {
+    if (off == 0) { PCWD_FILT8(0) }
+    else if (off == 1) { PCWD_FILT8(1) }
+    else if (off == 2) { PCWD_FILT8(2) }
+    else { PCWD_FILT8(3) }
+  } else {
+    if (off == 0) { PCWD_FILT8(0) }
+    else { PCWD_FILT8(1) }
+  }
+#undef PCWD_FILT8
+}
+
+}  // namespace
+
+// Shared-memory layout (elements of Real), all offsets from the dynamic smem base:
+//   [slack] R_0 .. R_{GU-1} (RS × R0 each; later the approximation of each step, row stride RS) [slack]
+//   [slack] staging: NST × (T_k tile R0 × TS, v_k strip R0 × VS)  ∪  Yt_0 .. Yt_{GU-1} (YC × YS)  [slack]
+//   D_0 .. D_{GU-1} (DS each)
+template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG>
+__global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Plan P, const __grid_constant__ FineArgs A) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  __shared__ int wflag[CG];
+  Real* sm = reinterpret_cast<Real*>(fsm);
+  constexpr int SH = 1 << LEV;           // window shift between adjacent units (2^ℓ)
+  constexpr int VW = FVec<Real>::W;
+  const int tid = threadIdx.x;
+  const int n = P.n, mask = n - 1;
+  constexpr int GT = kFT / CG;           // threads per unit group in the cascade (CG units at a time)
+  const int slot = tid / GT, gt = tid - slot * GT;
+  Real* Rbase = sm + kSlack;
+  // staging base aligned to 128 bytes (TMA destinations); derived from `sm` by an integer offset so the
+  // compiler keeps the shared-memory address space (LDS, not generic LD)
+  const unsigned s_raw = smem_u32(sm + A.regS + kSlack);
+  Real* Sbase = sm + A.regS + kSlack + (((s_raw + 127u) & ~127u) - s_raw) / sizeof(Real);
+  Real* Dbase = sm + A.regD;
+  const int64_t rounds = (A.u1 - A.u0) / GU;
+  __shared__ __align__(8) unsigned long long fullbar[2];
+  if (tid == 0) {
+    mbar_init(&fullbar[0], 1);
+    mbar_init(&fullbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned phase = 0u;   // bit b: parity of the next completion of fullbar[b]
+
+  long long t_ksum = 0, t_casc = 0, t_last = 0;
+  for (int64_t rd = blockIdx.x; rd < rounds; rd += gridDim.x) {
+    if (A.dbg && tid == 0) t_last = clock64();
+    const int64_t ufirst = A.u0 + rd * GU;
+    const int sbi = find_subband(P, ufirst);
+    const SubBand& S = P.sb[sbi];
+    const int64_t pos = ufirst - S.offset;
+    const int p0 = int(pos / S.nl), p1f = int(pos - int64_t(p0) * S.nl);
+    const int R0 = S.tW[0], R1 = S.tW[1];
+    const int c0 = (p0 << LEV) + S.tSu[0];
+    const int c1f = (p1f << LEV) + S.tSu[1];
+    const Real* __restrict__ T = reinterpret_cast<const Real*>(A.T) + S.toff;
+
+    // ------------------------------------------------------------------ a2: k-sum
+    {
+      const int c1a = c1f & ~(VW - 1);                      // aligned strip start (may be < 0: padded v)
+      const int sh = c1f - c1a;
+      // stage T_k (template box) and the v_k strip (box of the periodically padded v) into buffer `buf`:
+      // two TMA tile loads issued by one thread, completion counted in bytes on fullbar[buf].
+      const unsigned stage_bytes = unsigned((R0 * A.TS + R0 * A.VS) * sizeof(Real));
+      auto stage = [&](int k, int buf) {
+        if (tid == kFT - 1) {
+          Real* Ts = Sbase + buf * (A.TSZ + A.VSZ);
+          Real* Vs = Ts + A.TSZ;
+          fence_proxy_async();
+          mbar_expect_tx(&fullbar[buf], stage_bytes);
+          tma_load_3d(Ts, &A.tmT[sbi - A.sb_first], 0, 0, k, &fullbar[buf]);
+          tma_load_3d(Vs, &A.tmV, c1a + A.vpad, c0 + A.vpad, k, &fullbar[buf]);
+        }
+      };
+      // task t of this thread: q = t % Q (residue, z-block), r = t / Q
+      const int NZB = ((R1 + SH - 1) / SH + GZ - 1) / GZ;
+      const int Q = SH * NZB;
+      Real acc[NT][GU][GZ];
+#pragma unroll
+      for (int a = 0; a < NT; ++a)
+#pragma unroll
+        for (int j = 0; j < GU; ++j)
+#pragma unroll
+          for (int i = 0; i < GZ; ++i) acc[a][j][i] = Real(0);
+      stage(0, 0);
+      if (NST == 2 && P.m > 1) stage(1, 1);
+      for (int k = 0; k < P.m; ++k) {
+        const int b = NST == 2 ? (k & 1) : 0;
+        mbar_wait(&fullbar[b], (phase >> b) & 1u);
+        phase ^= 1u << b;
+        const Real* Ts = Sbase + b * (A.TSZ + A.VSZ);
+        const Real* Vs = Ts + A.TSZ;
+#pragma unroll
+        for (int a = 0; a < NT; ++a) {
+          const int t = tid + a * kFT;
+          const int r = t / Q;
+          if (r < R0) {
+            const int q = t - r * Q;
+            const int res = q % SH, zb = q / SH;
+            const int z0 = res + SH * zb * GZ;
+            const Real* tr = Ts + r * A.TS + z0;
+            const Real* vr = Vs + r * A.VS + sh + z0;
+            Real tv[GZ];
+#pragma unroll
+            for (int i = 0; i < GZ; ++i) tv[i] = tr[SH * i];
+#pragma unroll
+            for (int mm = 0; mm < GU + GZ - 1; ++mm) {
+              const Real vm = vr[SH * mm];
+#pragma unroll
+              for (int j = 0; j < GU; ++j) {
+                const int i = mm - j;
+                if (i >= 0 && i < GZ) acc[a][j][i] = ffma_(vm, tv[i], acc[a][j][i]);
+              }
+            }
+          }
+        }
+        __syncthreads();
+        if (k + NST < P.m) stage(k + NST, b);
+      }
+      // R_j[r][z] (row stride RS), z < R1
+#pragma unroll
+      for (int a = 0; a < NT; ++a) {
+        const int t = tid + a * kFT;
+        const int r = t / Q;
+        if (r < R0) {
+          const int q = t - r * Q;
+          const int res = q % SH, zb = q / SH;
+          const int z0 = res + SH * zb * GZ;
+#pragma unroll
+          for (int j = 0; j < GU; ++j) {
+            Real* dst = Rbase + j * A.RSZ + r * A.RS;
+#pragma unroll
+            for (int i = 0; i < GZ; ++i)
+              if (z0 + SH * i < R1) dst[z0 + SH * i] = acc[a][j][i];
+          }
+        }
+      }
+      __syncthreads();
+    }
+
+    if (A.dbg && tid == 0) { const long long t = clock64(); t_ksum += t - t_last; t_last = t; }
+    // ------------------------------------------------------------------ a3: cascade of unit u
+    // (CG units at a time, one thread group each; Yt and D are per group slot)
+    for (int w0 = 0; w0 < GU; w0 += CG) {
+    const int u = w0 + slot;
+    if (gt == 0) wflag[slot] = 0;
+    const int p1 = p1f + u;
+    const int cls0 = p0 & (S.fg_m - 1), cls1 = p1 & (S.fg_m - 1);
+    const FGeom& G = A.geom[S.fg_off + cls0 * S.fg_m + cls1];
+    const int d0 = p0 - cls0, d1 = p1 - cls1;
+    const int steps = S.steps;
+    Real* X = Rbase + u * A.RSZ;                 // step input (R, then each step's approximation)
+    Real* Yt = Sbase + slot * A.YSZ;
+    Real* Dd = Dbase + slot * A.DS;
+    int xb = (p1 << LEV) + S.tSu[1];             // column of X's local index 0 (R: the window start)
+    int xr0 = c0;                                // row of X's local index 0
+    for (int s = 1; s <= steps; ++s) {
+      // this step's geometry, translated to the unit (fields read from the class record as needed)
+      const FStep& f = G.st[s - 1];
+      const int sa0 = g_shift(d0, LEV, s - 1), sa1 = g_shift(d1, LEV, s - 1);
+      const int sb0 = g_shift(d0, LEV, s), sb1 = g_shift(d1, LEV, s);
+      const int ar = f.ar + sa0, arl = f.arl;
+      const int hlo = f.hlo + sb1, hlen = f.hlen, glo = f.glo + sb1, glen = f.glen;
+      // pass A: rows of X (axis 1) -> Yt[col][row - yb]; task = (output block, row), row fastest
+      const int yb = ar & ~(VW - 1);
+      {
+        const int hb = (hlen + 7) >> 3, gb = (glen + 7) >> 3;
+        const int rows = arl;
+        const int ntask = (hb + gb) * rows;
+        const int vlo = f.xc + sa1 - xb, vhi = vlo + f.xcl;
+        const float inv = 1.0f / float(max(rows, 1));
+        for (int t = gt; t < ntask; t += GT) {
+          const int q = __float2int_rz((float(t) + 0.5f) * inv);   // t / rows (exact for t < 2^20)
+          const int rr = t - q * rows;
+          const int ty = q >= hb;
+          const int j0 = ty ? glo + 8 * (q - hb) : hlo + 8 * q;
+          const int jend = ty ? glo + glen : hlo + hlen;
+          const int nout = min(8, jend - j0);
+          const int r = ar + rr;
+          const Real* xrow = X + (r - xr0) * A.RS;
+          Real out[8];
+          if (ty) filt8<Real, L2, 1>(P, xrow, xb, j0, nout, vlo, vhi, out);
+          else filt8<Real, L2, 0>(P, xrow, xb, j0, nout, vlo, vhi, out);
+          const int ycol0 = ty ? hlen + (j0 - glo) : (j0 - hlo);
+          Real* yd = Yt + ycol0 * A.YS + (r - yb);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i < nout) yd[i * A.YS] = out[i];
+        }
+      }
+      bar_group(1 + slot, GT);
+      // pass B: Yt rows (axis 0) -> approximation box (next X) and detail boxes (D);
+      // task = (box, row block, column), column fastest
+      int nxb = 0, nxr = 0;
+      if (s < steps) {
+        const FStep& fn = G.st[s];
+        nxb = (fn.xc + g_shift(d1, LEV, s)) & ~(VW - 1);
+        nxr = fn.xr + g_shift(d0, LEV, s);
+      }
+      {
+        const bool want0 = s < steps || s == P.J;
+        const int vlo = ar - yb, vhi = vlo + arl;
+        int tbase = 0;
+#pragma unroll
+        for (int ec = 0; ec < 4; ++ec) {
+          const int e0 = ec >> 1, e1 = ec & 1;
+          const int bl0 = f.blen0[ec], bl1 = f.blen1[ec];
+          const int cnt = (ec == 0 && !want0) ? 0 : ((bl0 + 7) >> 3) * bl1;
+          // continue the lane rotation across boxes so small boxes do not all start at lane 0
+          const int first = (gt - tbase % GT + GT) % GT;
+          tbase += cnt;
+          const int lo0 = f.blo0[ec] + sb0, lo1 = f.blo1[ec] + sb1;
+          const int ycb = e1 ? hlen - glo : -hlo;
+          const float inv = 1.0f / float(max(bl1, 1));
+          for (int t = first; t < cnt; t += GT) {
+            const int q = __float2int_rz((float(t) + 0.5f) * inv);   // t / bl1
+            const int cc = t - q * bl1;
+            const int l0 = lo0 + 8 * q;
+            const int nrow = min(8, bl0 - 8 * q);
+            const int j = lo1 + cc;
+            Real out[8];
+            if (e0) filt8<Real, L2, 1>(P, Yt + (ycb + j) * A.YS, yb, l0, nrow, vlo, vhi, out);
+            else filt8<Real, L2, 0>(P, Yt + (ycb + j) * A.YS, yb, l0, nrow, vlo, vhi, out);
+            if (ec == 0 && s < steps) {
+              Real* xd = X + (l0 - nxr) * A.RS + (j - nxb);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (i < nrow) xd[i * A.RS] = out[i];
+            } else {
+              Real* dd = Dd + f.doff[ec] + (8 * q) * bl1 + cc;
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (i < nrow) dd[i * bl1] = out[i];
+            }
+          }
+        }
+      }
+      bar_group(1 + slot, GT);
+      xb = nxb;
+      xr0 = nxr;
+    }
+
+    // ------------------------------------------------------------------ a4: gather + write row
+    {
+      const int lev = LEV;
+      const int4* st = A.stencil + S.stencil_off;
+      const int L = P.band_L;
+      const int64_t base = (ufirst + u - A.row0) * L;
+      Real* outv = reinterpret_cast<Real*>(A.val);
+      Real* sv = Yt;                              // wrap-case stage (Yt is dead now)
+      int* sc = reinterpret_cast<int*>(sv + P.band_Lpad);
+      int wrap = 0;
+      for (int jj = gt; jj < L; jj += GT) {
+        const int4 e = st[jj];
+        const int s = e.w;                        // level of the partner sub-band
+        const SubBand& Lb = P.sb[e.x];
+        const int D = s - lev;
+        const int b0 = D == 0 ? p0 : (D < 0 ? (p0 << -D) : (p0 >> D));
+        const int b1 = D == 0 ? p1 : (D < 0 ? (p1 << -D) : (p1 >> D));
+        const int l0 = b0 + e.y, l1 = b1 + e.z;
+        const FStep& f = G.st[s - 1];
+        const int ec = Lb.e;
+        const int lo0 = f.blo0[ec] + g_shift(d0, lev, s), lo1 = f.blo1[ec] + g_shift(d1, lev, s);
+        const int i0 = l0 - lo0, i1 = l1 - lo1;
+        Real x = Real(0);
+        if (i0 >= 0 && i0 < f.blen0[ec] && i1 >= 0 && i1 < f.blen1[ec]) x = Dd[f.doff[ec] + i0 * f.blen1[ec] + i1];
+        wrap |= (l0 < 0) | (l0 >= Lb.nl) | (l1 < 0) | (l1 >= Lb.nl);
+        const int c = int(Lb.offset + int64_t(l0 & (Lb.nl - 1)) * Lb.nl + (l1 & (Lb.nl - 1)));
+        sv[jj] = x;
+        sc[jj] = c;
+      }
+      // any partner wraps around the torus -> place by rank of the column
+      if (wrap) wflag[slot] = 1;
+      bar_group(1 + slot, GT);
+      wrap = wflag[slot];
+      for (int jj = gt; jj < L; jj += GT) {
+        const int c = sc[jj];
+        int rank = jj;
+        if (wrap) {
+          rank = 0;
+          for (int i = 0; i < L; ++i) rank += sc[i] < c;
+        }
+        A.col[base + rank] = c;
+        outv[base + rank] = sv[jj];
+      }
+    }
+    __syncthreads();
+    }
+    if (A.dbg && tid == 0) { const long long t = clock64(); t_casc += t - t_last; t_last = t; }
+  }
+  if (A.dbg && tid == 0) {
+    atomicAdd(A.dbg, (unsigned long long)t_ksum);
+    atomicAdd(A.dbg + 1, (unsigned long long)t_casc);
+  }
+}
+
+// ---------------------------------------------------------------------------------- launcher
+
+bool fine_config(int real_bytes, int level, int L2, FineCfg* c) {
+  if (L2 != 2 && L2 != 4 && L2 != 8 && L2 != 12) return false;
+  if (real_bytes == 4) {
+    if (level == 1) { *c = FineCfg{8, 11, 1, 2, 4}; return true; }
+    if (level == 2) { *c = FineCfg{4, 15, 1, 1, 4}; return true; }
+    if (level == 3) { *c = FineCfg{2, 11, 3, 1, 2}; return true; }
+  } else {
+    if (level == 1) { *c = FineCfg{4, 11, 1, 1, 4}; return true; }
+    if (level == 2) { *c = FineCfg{2, 15, 1, 1, 2}; return true; }
+    if (level == 3) { *c = FineCfg{1, 11, 3, 1, 1}; return true; }
+  }
+  return false;
+}
+
+template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG>
+static cudaError_t launch_fine_t(const Plan& P, const FineArgs& A, int grid, size_t smem, cudaStream_t st) {
+  auto k = fine_kernel<Real, L2, LEV, GU, GZ, NT, NST, CG>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k<<<grid, kFT, smem, st>>>(P, A);
+  return cudaGetLastError();
+}
+
+template <int L2>
+static cudaError_t launch_fine_l2(const Plan& P, const FineArgs& A, int real_bytes, int level, int grid, size_t smem,
+                                  cudaStream_t st) {
+  if (real_bytes == 4) {
+    if (level == 1) return launch_fine_t<float, L2, 1, 8, 11, 1, 2, 4>(P, A, grid, smem, st);
+    if (level == 2) return launch_fine_t<float, L2, 2, 4, 15, 1, 1, 4>(P, A, grid, smem, st);
+    if (level == 3) return launch_fine_t<float, L2, 3, 2, 11, 3, 1, 2>(P, A, grid, smem, st);
+  } else {
+    if (level == 1) return launch_fine_t<double, L2, 1, 4, 11, 1, 1, 4>(P, A, grid, smem, st);
+    if (level == 2) return launch_fine_t<double, L2, 2, 2, 15, 1, 1, 2>(P, A, grid, smem, st);
+    if (level == 3) return launch_fine_t<double, L2, 3, 1, 11, 3, 1, 1>(P, A, grid, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_fine(const Plan& P, const FineArgs& A, int real_bytes, int level, int grid, size_t smem,
+                        cudaStream_t st) {
+  switch (P.L2) {
+    case 2: return launch_fine_l2<2>(P, A, real_bytes, level, grid, smem, st);
+    case 4: return launch_fine_l2<4>(P, A, real_bytes, level, grid, smem, st);
+    case 8: return launch_fine_l2<8>(P, A, real_bytes, level, grid, smem, st);
+    case 12: return launch_fine_l2<12>(P, A, real_bytes, level, grid, smem, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace pcwd

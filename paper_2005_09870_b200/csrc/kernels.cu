@@ -113,6 +113,19 @@ __global__ void tmpl_passB(const __grid_constant__ Plan P, const __grid_constant
 }
 
 template <typename Real>
+__global__ void pad_v_kernel(const Real* __restrict__ v, Real* __restrict__ vp, int n, int P, int m) {
+  const int w = n + 2 * P;
+  const int64_t total = int64_t(m) * w * w;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = i / (int64_t(w) * w);
+    const int64_t r = i - k * w * w;
+    const int y = int(r / w), x = int(r - int64_t(y) * w);
+    const int sy = ((y - P) % n + n) % n, sx = ((x - P) % n + n) % n;
+    vp[i] = v[k * int64_t(n) * n + int64_t(sy) * n + sx];
+  }
+}
+
+template <typename Real>
 __global__ void cast_kernel(const double* __restrict__ src, Real* __restrict__ dst, int64_t n) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     dst[i] = Real(src[i]);
@@ -495,6 +508,13 @@ cudaError_t launch_tmpl_level(const Plan& P, const TmplArgs& A, int real_bytes, 
     tmpl_passA<double><<<grid_for(totA), kBlock, 0, st>>>(P, A, P.J, level);
     if (P.d == 2) tmpl_passB<double><<<grid_for(totB), kBlock, 0, st>>>(P, A, P.J, level);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad_v(const void* v, void* vpad, int n, int P, int m, int real_bytes, cudaStream_t st) {
+  const int64_t total = int64_t(m) * (n + 2 * P) * (n + 2 * P);
+  if (real_bytes == 4) pad_v_kernel<float><<<grid_for(total), kBlock, 0, st>>>((const float*)v, (float*)vpad, n, P, m);
+  else pad_v_kernel<double><<<grid_for(total), kBlock, 0, st>>>((const double*)v, (double*)vpad, n, P, m);
   return cudaGetLastError();
 }
 

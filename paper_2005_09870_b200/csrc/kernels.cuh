@@ -1,5 +1,6 @@
 // kernels.cuh — launch interface of the sm_100a kernels (implemented in kernels.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -47,6 +48,39 @@ struct TileArgs {
 cudaError_t launch_band_tile(const Plan& P, const TileArgs& A, int real_bytes, int grid, size_t smem,
                              cudaStream_t st);
 
+struct FGeom;
+
+struct FineArgs {
+  CUtensorMap tmV;          // TMA map of the periodically padded v (3-D: x, y, k), box VS × R0 × 1
+  CUtensorMap tmT[3];       // TMA maps of the templates of the level's sub-bands (x, y, k), box TS × R0 × 1
+  int vpad;                 // halo width P of the padded v (v_pad[y + P][x + P] = v[y mod n][x mod n])
+  int sb_first;             // first sub-band of the launch (tmT index = sbi - sb_first)
+  int TSZ, VSZ;             // staged T / v tile sizes (elements, multiples of 128 bytes)
+  const void* v;
+  const void* T;
+  const int4* stencil;      // .w = level of the partner sub-band
+  const FGeom* geom;        // class geometry records (plan), indexed by SubBand::fg_off
+  int64_t u0, u1;           // unit range (one level, whole rounds of GU units)
+  int64_t row0;
+  int32_t* col;
+  void* val;
+  int64_t regS, regD;       // region offsets (elements): staging / Yt, D
+  int RS, RSZ;              // R / approximation row stride, per-unit R region size
+  int TS, VS;               // staged T row stride, staged v row stride
+  int YS, YSZ;              // Yt row stride, per-unit Yt size
+  int DS;                   // per-unit D size
+  unsigned long long* dbg;  // optional phase clock counters (PCWD_DEBUG_PHASES): k-sum, cascade
+};
+
+// Template configuration of the fine kernel for (real_bytes, level): units per round GU, template
+// columns per thread GZ, tasks per thread NT, staging buffers NST, concurrent cascades CG (fine.cu).
+struct FineCfg {
+  int GU, GZ, NT, NST, CG;   // CG: units whose cascades run concurrently (256 / CG threads each)
+};
+bool fine_config(int real_bytes, int level, int L2, FineCfg* cfg);
+cudaError_t launch_fine(const Plan& P, const FineArgs& A, int real_bytes, int level, int grid, size_t smem,
+                        cudaStream_t st);
+
 struct BatchArgs {
   const void* v;
   const void* T;
@@ -60,8 +94,8 @@ struct BatchArgs {
   void* val;
 };
 
-cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, int64_t maxY,
-                                int64_t maxB, int steps, cudaStream_t st, int* launches);
+cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, const int64_t* workA,
+                                const int64_t* workB, int steps, cudaStream_t st, int* launches);
 
 struct TmplArgs {
   const double* phi_in;     // m × Win0 × Win1 (fp64)
@@ -82,6 +116,8 @@ cudaError_t launch_phi0(const Plan& P, const double* u, double* phi0, int S0, in
 cudaError_t launch_tmpl_level(const Plan& P, const TmplArgs& A, int real_bytes, int coarse_level,
                               cudaStream_t st);
 cudaError_t launch_cast(const double* src, void* dst, int64_t count, int real_bytes, cudaStream_t st);
+// K1: v_pad[k][y][x] = v[k][(y - P) mod n][(x - P) mod n], side n + 2P (compute type)
+cudaError_t launch_pad_v(const void* v, void* vpad, int n, int P, int m, int real_bytes, cudaStream_t st);
 cudaError_t launch_units(const Plan& P, const UnitArgs& A, int mode, int real_bytes, int out_bytes,
                          int grid, size_t smem, cudaStream_t st);
 size_t unit_smem_limit();

@@ -387,6 +387,29 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
     }
   }
 
+  // fine-path geometry: one record per sub-band and class q = p mod 2^{steps-ℓ} (geom.h)
+  hp->fgeom.clear();
+  for (int s = 0; s < ns; ++s) {
+    SubBand& S = P.sb[s];
+    S.fg_off = 0;
+    S.fg_m = 0;
+    if (!(P.retain == PCWD_RETAIN_BAND && P.d == 2 && S.e != 0 && S.level <= 3 && S.steps <= kFMS && S.wk_ok)) continue;
+    const int M = 1 << std::max(0, S.steps - S.level);
+    S.fg_off = int(hp->fgeom.size());
+    S.fg_m = M;
+    auto boxfn = [&](int t, int* b) {
+      const int* q = &hp->stencil_box[(size_t(s) * ns + t) * 4];
+      b[0] = q[0]; b[1] = q[1]; b[2] = q[2]; b[3] = q[3];
+    };
+    for (int q0 = 0; q0 < M; ++q0)
+      for (int q1 = 0; q1 < M; ++q1) {
+        FGeom g;
+        std::memset(&g, 0, sizeof(g));
+        compute_fgeom(P, S, q0, q1, boxfn, g);
+        hp->fgeom.push_back(g);
+      }
+  }
+
   // shard: contiguous unit ranges with equal algorithmic cost (units in Λ order)
   double total = 0.0;
   for (int s = 0; s < ns; ++s) total += P.sb[s].fma * double(P.sb[s].count);

@@ -5,6 +5,7 @@
 
 #include "../../include/pcwd.h"
 #include "common.h"
+#include "geom.h"
 
 namespace pcwd {
 
@@ -27,6 +28,7 @@ struct HostPlan {
   // template φ-chain windows per axis and level (ℓ = 0..J), and the ψ-window start per level
   int phiS[2][kMaxJ + 1] = {}, phiW[2][kMaxJ + 1] = {}, psiS[2][kMaxJ + 1] = {};
   double fma_templates = 0.0;
+  std::vector<FGeom> fgeom;       // BAND, fine levels: class geometry records (SubBand::fg_off / fg_m)
 };
 
 // Returns a pcwd_status; msg receives the reason on error.
