@@ -480,12 +480,15 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
             }
           }
         }
-        const int RS = odd_stride(R1);
+        // R rows: [roff, roff + R1) valid, zero pad of ≥ 2δ + 2 after (serves as the next row's left pad);
+        // even stride with an odd number of pairs (16 lanes of 8-byte loads hit distinct banks)
+        auto pair_stride = [&](int w) { int x = (w + 1) / 2 * 2; if ((x / 2) % 2 == 0) x += 2; return x; };
+        const int RS = pair_stride(R1 + 1 + P.L2 + 2);
         const int zmaxT = (SH - 1) + SH * fc.GZ * (NZB - 1) + SH * (fc.GZ - 1);
         const int zmaxV = zmaxT + SH * (fc.GU - 1);
         const int TS = odd_stride(std::max(S0.tRS, zmaxT + 1));
         const int VS = odd_stride(VW - 1 + std::max(R1 + SH * (fc.GU - 1), zmaxV + 1));
-        const int YS = odd_stride(arl + VW - 1);
+        const int YS = pair_stride(arl + VW - 1);
         const int64_t lpad = P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb;
         const int64_t YSZ = (std::max<int64_t>(int64_t(ycols) * YS, lpad) + VW - 1) / VW * VW;
         const int64_t RSZ = int64_t(R0) * RS;
@@ -495,7 +498,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         const int al = 128 / rb;   // TMA destinations: 128-byte aligned boxes
         const int TSZ = (R0 * TS + al - 1) / al * al, VSZ = (R0 * VS + al - 1) / al * al;
         const int64_t stg = int64_t(fc.NST) * (TSZ + VSZ) + al;
-        const int64_t regS = SLK + std::max<int64_t>(stg, fc.CG * YSZ) + SLK;
+        ok = ok && stg <= fc.GU * RSZ;          // the k-sum staging aliases the R region
+        const int64_t regS = SLK + fc.CG * YSZ + SLK;
         const int64_t regD = regR + regS;
         const size_t smem = size_t(regD + fc.CG * DS) * rb;
         ok = ok && smem + 1024 <= size_t(smem_optin > 0 ? smem_optin : 48 * 1024);

@@ -18,6 +18,7 @@
 // Geometry comes from the host plan (one record per sub-band and class p mod 2^{steps-ℓ}, geom.h),
 // translated to the unit's position.
 #include <climits>
+#include <type_traits>
 
 #include "geom.h"
 #include "kernels.cuh"
@@ -96,52 +97,40 @@ __device__ __forceinline__ void bar_group(int id, int nthreads) {
   else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// 8 consecutive outputs out[q] = Σ_t f_TY[t] x[2(j0+q) + o_TY + t - base] of a row whose valid entries are
-// the local indices [vlo, vhi) (zero elsewhere).  Loads NV aligned vectors starting at align_down(s0);
-// `off` = s0 mod VW selects the register window.  Rows carry slack so the over-reads stay in bounds.
-template <typename Real, int L2, int TY>
+// 8 consecutive outputs out[q] = Σ_t f_TY[t] x[2(j0+q) + o_TY + t - base] of a row (taps are compile-time
+// indices into the kernel-parameter bank).  `base` is even, so the 14 + 2δ inputs start at an even local
+// index and are read as pairs (8-byte float2 / 16-byte double2 loads).  MASK: the row's valid entries are
+// [vlo, vhi) and everything else must read as zero; without MASK the caller guarantees zeros around the
+// valid entries (zero-padded rows), so no select is needed.
+template <typename Real, int L2, int TY, bool MASK>
 __device__ __forceinline__ void filt8(const Plan& P, const Real* __restrict__ row, int base, int j0, int nout,
                                       int vlo, int vhi, Real out[8]) {
-  constexpr int VW = FVec<Real>::W;
+  using V2 = typename std::conditional<sizeof(Real) == 4, float2, double2>::type;
   constexpr int o = TY ? 2 - L2 : 0;
-  constexpr int SPAN = 14 + L2;                                 // inputs of 8 outputs
-  constexpr int NV = (SPAN + VW - 1 + VW - 1) / VW;            // vectors incl. misalignment
+  constexpr int SPAN = 14 + L2;                                 // inputs of 8 outputs (even)
   const int s0 = 2 * j0 + o - base;
-  const int a = s0 & ~(VW - 1);
-  const int off = s0 - a;
-  Real x[NV * VW];
-  const typename FVec<Real>::T* p = reinterpret_cast<const typename FVec<Real>::T*>(row + a);
+  Real x[SPAN];
+  const V2* p = reinterpret_cast<const V2*>(row + s0);
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const typename FVec<Real>::T t = p[i];
-    if constexpr (VW == 4) {
-      x[4 * i] = t.x; x[4 * i + 1] = t.y; x[4 * i + 2] = t.z; x[4 * i + 3] = t.w;
-    } else {
-      x[2 * i] = t.x; x[2 * i + 1] = t.y;
+  for (int i = 0; i < SPAN / 2; ++i) {
+    const V2 t = p[i];
+    x[2 * i] = t.x;
+    x[2 * i + 1] = t.y;
+  }
+  if constexpr (MASK) {
+    const int lo = vlo - s0, hi = vhi - s0;
+    if (lo > 0 || hi < 2 * (nout - 1) + L2) {
+#pragma unroll
+      for (int i = 0; i < SPAN; ++i) x[i] = (i >= lo && i < hi) ? x[i] : Real(0);
     }
   }
-  // zero the loaded values outside [vlo, vhi) that the nout needed outputs read
-  const int lo = vlo - a, hi = vhi - a;
-  if (lo > off || hi < off + 2 * (nout - 1) + L2) {
 #pragma unroll
-    for (int i = 0; i < NV * VW; ++i) x[i] = (i >= lo && i < hi) ? x[i] : Real(0);
+  for (int q = 0; q < 8; ++q) {
+    Real acc = Real(0);
+#pragma unroll
+    for (int t = 0; t < L2; ++t) acc = ffma_(TapsOf<Real>::get(P, TY, t), x[2 * q + t], acc);
+    out[q] = acc;
   }
-#define PCWD_FILT8(OFF)                                                                        \
-  _Pragma("unroll") for (int q = 0; q < 8; ++q) {                                              \
-    Real acc = Real(0);                                                                        \
-    _Pragma("unroll") for (int t = 0; t < L2; ++t) acc = ffma_(TapsOf<Real>::get(P, TY, t), x[(OFF) + 2 * q + t], acc); \
-    out[q] = acc;                                                                              \
-  }
-  if constexpr (VW == 4) {
-    if (off == 0) { PCWD_FILT8(0) }
-    else if (off == 1) { PCWD_FILT8(1) }
-    else if (off == 2) { PCWD_FILT8(2) }
-    else { PCWD_FILT8(3) }
-  } else {
-    if (off == 0) { PCWD_FILT8(0) }
-    else { PCWD_FILT8(1) }
-  }
-#undef PCWD_FILT8
 }
 
 }  // namespace
@@ -162,10 +151,12 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
   constexpr int GT = kFT / CG;           // threads per unit group in the cascade (CG units at a time)
   const int slot = tid / GT, gt = tid - slot * GT;
   Real* Rbase = sm + kSlack;
-  // staging base aligned to 128 bytes (TMA destinations); derived from `sm` by an integer offset so the
-  // compiler keeps the shared-memory address space (LDS, not generic LD)
-  const unsigned s_raw = smem_u32(sm + A.regS + kSlack);
-  Real* Sbase = sm + A.regS + kSlack + (((s_raw + 127u) & ~127u) - s_raw) / sizeof(Real);
+  // k-sum staging aliases the R region (R is written only after the last k); base aligned to 128 bytes for
+  // the TMA boxes, derived from `sm` by an integer offset so the compiler keeps the shared address space
+  const unsigned s_raw = smem_u32(sm + kSlack);
+  Real* Sbase = sm + kSlack + (((s_raw + 127u) & ~127u) - s_raw) / sizeof(Real);
+  Real* Ybase = sm + A.regS + kSlack;
+  for (int i = tid; i < kSlack; i += kFT) sm[i] = Real(0);   // zero rows before R_0 row 0 (left pad)
   Real* Dbase = sm + A.regD;
   const int64_t rounds = (A.u1 - A.u0) / GU;
   __shared__ __align__(8) unsigned long long fullbar[2];
@@ -188,6 +179,7 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
     const int R0 = S.tW[0], R1 = S.tW[1];
     const int c0 = (p0 << LEV) + S.tSu[0];
     const int c1f = (p1f << LEV) + S.tSu[1];
+    const int roff = c1f & 1;                     // R row offset: makes every row base even (pair loads)
     const Real* __restrict__ T = reinterpret_cast<const Real*>(A.T) + S.toff;
 
     // ------------------------------------------------------------------ a2: k-sum
@@ -263,12 +255,18 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
           const int z0 = res + SH * zb * GZ;
 #pragma unroll
           for (int j = 0; j < GU; ++j) {
-            Real* dst = Rbase + j * A.RSZ + r * A.RS;
+            Real* dst = Rbase + j * A.RSZ + r * A.RS + roff;
 #pragma unroll
             for (int i = 0; i < GZ; ++i)
               if (z0 + SH * i < R1) dst[z0 + SH * i] = acc[a][j][i];
           }
         }
+      }
+      // zero the row pads (the staging boxes overwrote them): columns [0, roff) and [roff + R1, RS)
+      for (int i = tid; i < GU * R0; i += kFT) {     // rows of all units are contiguous (RSZ = R0·RS)
+        Real* row = Rbase + i * A.RS;
+        if (roff) row[0] = Real(0);
+        for (int c = roff + R1; c < A.RS; ++c) row[c] = Real(0);
       }
       __syncthreads();
     }
@@ -285,9 +283,9 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
     const int d0 = p0 - cls0, d1 = p1 - cls1;
     const int steps = S.steps;
     Real* X = Rbase + u * A.RSZ;                 // step input (R, then each step's approximation)
-    Real* Yt = Sbase + slot * A.YSZ;
+    Real* Yt = Ybase + slot * A.YSZ;
     Real* Dd = Dbase + slot * A.DS;
-    int xb = (p1 << LEV) + S.tSu[1];             // column of X's local index 0 (R: the window start)
+    int xb = (p1 << LEV) + S.tSu[1] - roff;      // column of X's local index 0 (even)
     int xr0 = c0;                                // row of X's local index 0
     for (int s = 1; s <= steps; ++s) {
       // this step's geometry, translated to the unit (fields read from the class record as needed)
@@ -314,8 +312,13 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
           const int r = ar + rr;
           const Real* xrow = X + (r - xr0) * A.RS;
           Real out[8];
-          if (ty) filt8<Real, L2, 1>(P, xrow, xb, j0, nout, vlo, vhi, out);
-          else filt8<Real, L2, 0>(P, xrow, xb, j0, nout, vlo, vhi, out);
+          if (s == 1) {   // R rows are zero-padded
+            if (ty) filt8<Real, L2, 1, false>(P, xrow, xb, j0, nout, vlo, vhi, out);
+            else filt8<Real, L2, 0, false>(P, xrow, xb, j0, nout, vlo, vhi, out);
+          } else {
+            if (ty) filt8<Real, L2, 1, true>(P, xrow, xb, j0, nout, vlo, vhi, out);
+            else filt8<Real, L2, 0, true>(P, xrow, xb, j0, nout, vlo, vhi, out);
+          }
           const int ycol0 = ty ? hlen + (j0 - glo) : (j0 - hlo);
           Real* yd = Yt + ycol0 * A.YS + (r - yb);
 #pragma unroll
@@ -354,8 +357,8 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
             const int nrow = min(8, bl0 - 8 * q);
             const int j = lo1 + cc;
             Real out[8];
-            if (e0) filt8<Real, L2, 1>(P, Yt + (ycb + j) * A.YS, yb, l0, nrow, vlo, vhi, out);
-            else filt8<Real, L2, 0>(P, Yt + (ycb + j) * A.YS, yb, l0, nrow, vlo, vhi, out);
+            if (e0) filt8<Real, L2, 1, true>(P, Yt + (ycb + j) * A.YS, yb, l0, nrow, vlo, vhi, out);
+            else filt8<Real, L2, 0, true>(P, Yt + (ycb + j) * A.YS, yb, l0, nrow, vlo, vhi, out);
             if (ec == 0 && s < steps) {
               Real* xd = X + (l0 - nxr) * A.RS + (j - nxb);
 #pragma unroll
