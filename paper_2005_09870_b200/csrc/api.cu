@@ -502,7 +502,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         const int64_t regS = SLK + fc.CG * YSZ + SLK;
         const int64_t regD = regR + regS;
         const size_t smem = size_t(regD + fc.CG * DS) * rb;
-        ok = ok && smem + 1024 <= size_t(smem_optin > 0 ? smem_optin : 48 * 1024);
+        ok = ok && smem + 4096 <= size_t(smem_optin > 0 ? smem_optin : 48 * 1024);
         int64_t a0 = (u0 + fc.GU - 1) / fc.GU * fc.GU, a1 = u1 / fc.GU * fc.GU;
         if (getenv("PCWD_DEBUG_PLAN"))
           fprintf(stderr, "[pcwd fine] level %d ok %d GU %d R %dx%d RS %d TS %d VS %d YS %d ycols %d arl %d dsz %d "
@@ -513,7 +513,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           F.fine = 1;
           F.level = lev;
           F.smem = smem;
-          const int per_sm = int(std::max<size_t>(1, std::min<size_t>(2, (228 * 1024) / (smem + 1024))));
+          const int per_sm = int(std::max<size_t>(1, std::min<size_t>(2, (228 * 1024) / (smem + 4096))));
           F.grid = int(std::min<int64_t>((a1 - a0) / fc.GU, int64_t(nsm) * per_sm));
           FineArgs& A = F.fa;
           A.u0 = a0; A.u1 = a1;

@@ -9,6 +9,7 @@
 //   bk_write   sort the stage by column (CSR order), write the row
 // Windows use the periodic Range arithmetic of common.h (a window may cover a whole line).
 #include <climits>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -19,6 +20,12 @@ constexpr int kB = 256;
 
 __device__ __forceinline__ float fmaB(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fmaB(double a, double b, double c) { return fma(a, b, c); }
+
+inline int find_subband_host(const Plan& P, int64_t unit) {
+  int s = P.nsb - 1;
+  while (s > 0 && unit < P.sb[s].offset) --s;
+  return s;
+}
 
 struct UnitPos {
   int sbi, p0, p1;
@@ -46,6 +53,17 @@ __device__ __forceinline__ void step_in(const Plan& P, const SubBand& S, const U
 }
 }  // namespace
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+template <typename Real>
+__device__ __forceinline__ void cp_async_el(Real* smem, const Real* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if constexpr (sizeof(Real) == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
 template <typename Real>
 __global__ void __launch_bounds__(kB) bk_ksum(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A) {
   const int64_t unit = A.u0 + blockIdx.y;
@@ -70,6 +88,100 @@ __global__ void __launch_bounds__(kB) bk_ksum(const __grid_constant__ Plan P, co
 #pragma unroll 5
     for (int k = 0; k < P.m; ++k) acc = fmaB(__ldg(v + k * P.N + vy), __ldg(T + k * S.tstride + ti), acc);
     X0[idx] = acc;
+  }
+}
+
+// Tiled k-sum for windows that do not cover a whole line (levels whose shift 2^ℓ ≥ 8): one CTA computes a
+// (256/2^ℓ rows) × (2^ℓ·GZ columns) tile of template positions z for G units adjacent along axis 1.  Their
+// windows are shifted by 2^ℓ columns, so unit u reads v at column z + 2^ℓ u: a thread owning template row r
+// and columns res + 2^ℓ i (i < GZ) needs GZ template values and GZ+G-1 v values per k for G·GZ products.
+// T_k and v_k tiles are staged in shared memory by cp.async, double-buffered over k; v columns wrap
+// periodically (4-byte copies where the strip crosses the torus seam).
+template <typename Real, int LEV, int G, int GZ>
+__global__ void __launch_bounds__(kB) bk_ksum_tiled(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
+                                                    int ntile1) {
+  constexpr int SH = 1 << LEV;
+  constexpr int TR = kB / SH;                 // template rows per tile
+  constexpr int TW = SH * GZ;                 // template columns per tile
+  constexpr int VW = 16 / int(sizeof(Real));  // elements per 16-byte vector
+  constexpr int VWID = SH * (GZ + G - 1);     // v columns the G windows read
+  constexpr int VS = VWID + VW;               // staged v row (aligned start + misalignment)
+  __shared__ __align__(16) Real Ts[2][TR][TW];
+  __shared__ __align__(16) Real Vs[2][TR][VS];
+  const int tid = threadIdx.x;
+  const int n = P.n, mask = n - 1;
+  const int64_t ug = A.u0 + int64_t(blockIdx.y) * G;            // first unit of the group
+  const UnitPos up = unit_pos(P, ug);
+  const SubBand& S = P.sb[up.sbi];
+  const int R0 = S.tW[0], R1 = S.tW[1];
+  const int t0 = blockIdx.x / ntile1, t1 = blockIdx.x - t0 * ntile1;
+  const int z0 = t0 * TR, zc = t1 * TW;
+  const int c0 = (up.p0 << LEV) + S.tSu[0];
+  const int x0 = (up.p1 << LEV) + S.tSu[1] + zc;                // unwrapped first v column of the tile
+  const int xa = x0 & ~(VW - 1), sh = x0 - xa;
+  const bool nowrap = xa >= 0 && xa + VS <= n;
+  const Real* __restrict__ v = reinterpret_cast<const Real*>(A.v);
+  const Real* __restrict__ T = reinterpret_cast<const Real*>(A.T) + S.toff;
+  auto stage = [&](int k, int b) {
+    const Real* Tk = T + int64_t(k) * S.tstride;
+    for (int i = tid; i < TR * (TW / VW); i += kB) {
+      const int r = i / (TW / VW), c = (i - r * (TW / VW)) * VW;
+      if (z0 + r < R0 && zc + c < S.tRS) cp_async16(&Ts[b][r][c], Tk + int64_t(z0 + r) * S.tRS + zc + c);
+    }
+    const Real* vk = v + int64_t(k) * P.N;
+    if (nowrap) {
+      for (int i = tid; i < TR * (VS / VW); i += kB) {
+        const int r = i / (VS / VW), c = (i - r * (VS / VW)) * VW;
+        cp_async16(&Vs[b][r][c], vk + int64_t((c0 + z0 + r) & mask) * n + xa + c);
+      }
+    } else {
+      for (int i = tid; i < TR * VWID; i += kB) {
+        const int r = i / VWID, c = i - r * VWID;
+        cp_async_el(&Vs[b][r][sh + c], vk + int64_t((c0 + z0 + r) & mask) * n + ((x0 + c) & mask));
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int r = tid / SH, res = tid - r * SH;
+  Real acc[G][GZ];
+#pragma unroll
+  for (int u = 0; u < G; ++u)
+#pragma unroll
+    for (int i = 0; i < GZ; ++i) acc[u][i] = Real(0);
+  stage(0, 0);
+  for (int k = 0; k < P.m; ++k) {
+    if (k + 1 < P.m) {
+      stage(k + 1, (k + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const int b = k & 1;
+    Real tv[GZ];
+#pragma unroll
+    for (int i = 0; i < GZ; ++i) tv[i] = Ts[b][r][res + SH * i];
+#pragma unroll
+    for (int mm = 0; mm < GZ + G - 1; ++mm) {
+      const Real vm = Vs[b][r][sh + res + SH * mm];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int i = mm - u;
+        if (i >= 0 && i < GZ) acc[u][i] = fmaB(vm, tv[i], acc[u][i]);
+      }
+    }
+    __syncthreads();
+  }
+  if (z0 + r < R0) {
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      Real* X0 = reinterpret_cast<Real*>(A.scratch) + (ug + u - A.u0) * A.stride + S.offX0 + int64_t(z0 + r) * R1;
+#pragma unroll
+      for (int i = 0; i < GZ; ++i) {
+        const int z = zc + res + SH * i;
+        if (z < R1) X0[z] = acc[u][i];
+      }
+    }
   }
 }
 
@@ -254,6 +366,33 @@ __global__ void __launch_bounds__(kB) bk_write(const __grid_constant__ Plan P, c
 
 // ----------------------------------------------------------------------------------- launcher
 
+// Tiled k-sum when every window of the launch's level stays inside one period per axis, the shift 2^ℓ is
+// in [8, 128], and groups of G units stay in one sub-band row.  Returns false to use bk_ksum instead.
+template <typename Real>
+static bool launch_ksum_tiled(const Plan& P, const BatchArgs& A, int nb, cudaStream_t st) {
+  constexpr int G = sizeof(Real) == 4 ? 8 : 4, GZ = sizeof(Real) == 4 ? 8 : 4;   // static smem < 48 KB
+  if (getenv("PCWD_NO_TILED_KSUM")) return false;
+  const int s0 = find_subband_host(P, A.u0), s1 = find_subband_host(P, A.u1 - 1);
+  const SubBand& S = P.sb[s0];
+  const int lev = S.level;
+  if (lev < 3 || lev > 7 || S.nl % G || nb % G || (A.u0 - S.offset) % G) return false;
+  for (int q = s0; q <= s1; ++q)
+    if (P.sb[q].level != lev || P.sb[q].tW[0] >= P.n || P.sb[q].tW[1] >= P.n || P.sb[q].tW[0] != S.tW[0] ||
+        P.sb[q].tW[1] != S.tW[1] || P.sb[q].e == 0)
+      return false;
+  const int SH = 1 << lev, TR = kB / SH, TW = SH * GZ;
+  const int ntile0 = (S.tW[0] + TR - 1) / TR, ntile1 = (S.tW[1] + TW - 1) / TW;
+  const dim3 grid(ntile0 * ntile1, nb / G);
+  switch (lev) {
+    case 3: bk_ksum_tiled<Real, 3, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
+    case 4: bk_ksum_tiled<Real, 4, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
+    case 5: bk_ksum_tiled<Real, 5, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
+    case 6: bk_ksum_tiled<Real, 6, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
+    case 7: bk_ksum_tiled<Real, 7, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
+  }
+  return true;
+}
+
 template <typename Real>
 static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0, const int64_t* workA,
                                const int64_t* workB, int steps, cudaStream_t st, int* launches) {
@@ -264,7 +403,7 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
     const int nb = int(std::min<int64_t>(A0.batch, units - b0));
     A.u1 = A.u0 + nb;
     auto gx = [](int64_t elems) { return int(std::max<int64_t>(1, std::min<int64_t>((elems + kB - 1) / kB, 64))); };
-    bk_ksum<Real><<<dim3(gx(maxX0), nb), kB, 0, st>>>(P, A);
+    if (!launch_ksum_tiled<Real>(P, A, nb, st)) bk_ksum<Real><<<dim3(gx(maxX0), nb), kB, 0, st>>>(P, A);
     ++*launches;
     for (int s = 1; s <= steps; ++s) {
       bk_passA<Real><<<dim3(gx(workA[s]), nb), kB, 0, st>>>(P, A, s);

@@ -133,6 +133,52 @@ __device__ __forceinline__ void filt8(const Plan& P, const Real* __restrict__ ro
   }
 }
 
+// Both filters of one analysis step on the same 8 output positions j0..j0+7 of a row (pass A, where the
+// detail columns lie inside the approximation columns): one run of loads covers the union of the inputs,
+// x[i] = row[2 j0 + (2 - L2) + i - base]; the g outputs read x[2q + t], the h outputs x[L2 - 2 + 2q + t].
+template <typename Real, int L2, bool MASK>
+__device__ __forceinline__ void filt8hg(const Plan& P, const Real* __restrict__ row, int base, int j0, bool doh,
+                                        bool dog, int nh, int ng, int vlo, int vhi, Real oh[8], Real og[8]) {
+  using V2 = typename std::conditional<sizeof(Real) == 4, float2, double2>::type;
+  constexpr int SPAN = 12 + 2 * L2;
+  const int s0 = 2 * j0 + 2 - L2 - base;
+  Real x[SPAN];
+  const V2* p = reinterpret_cast<const V2*>(row + s0);
+#pragma unroll
+  for (int i = 0; i < SPAN / 2; ++i) {
+    const V2 t = p[i];
+    x[2 * i] = t.x;
+    x[2 * i + 1] = t.y;
+  }
+  if constexpr (MASK) {
+    const int lo = vlo - s0, hi = vhi - s0;
+    if (lo > 0 || hi < SPAN) {
+#pragma unroll
+      for (int i = 0; i < SPAN; ++i) x[i] = (i >= lo && i < hi) ? x[i] : Real(0);
+    }
+  }
+  (void)nh;
+  (void)ng;
+  if (doh) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      Real acc = Real(0);
+#pragma unroll
+      for (int t = 0; t < L2; ++t) acc = ffma_(TapsOf<Real>::get(P, 0, t), x[L2 - 2 + 2 * q + t], acc);
+      oh[q] = acc;
+    }
+  }
+  if (dog) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      Real acc = Real(0);
+#pragma unroll
+      for (int t = 0; t < L2; ++t) acc = ffma_(TapsOf<Real>::get(P, 1, t), x[2 * q + t], acc);
+      og[q] = acc;
+    }
+  }
+}
+
 }  // namespace
 
 // Shared-memory layout (elements of Real), all offsets from the dynamic smem base:
@@ -143,6 +189,7 @@ template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int C
 __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Plan P, const __grid_constant__ FineArgs A) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int wflag[CG];
+  __shared__ int sdesc[CG][kFMS][32];   // per slot: translated step geometry (FStep fields)
   Real* sm = reinterpret_cast<Real*>(fsm);
   constexpr int SH = 1 << LEV;           // window shift between adjacent units (2^ℓ)
   constexpr int VW = FVec<Real>::W;
@@ -159,14 +206,15 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
   for (int i = tid; i < kSlack; i += kFT) sm[i] = Real(0);   // zero rows before R_0 row 0 (left pad)
   Real* Dbase = sm + A.regD;
   const int64_t rounds = (A.u1 - A.u0) / GU;
-  __shared__ __align__(8) unsigned long long fullbar[2];
+  __shared__ __align__(8) unsigned long long fullbar[NST];
   if (tid == 0) {
-    mbar_init(&fullbar[0], 1);
-    mbar_init(&fullbar[1], 1);
+#pragma unroll
+    for (int q = 0; q < NST; ++q) mbar_init(&fullbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   unsigned phase = 0u;   // bit b: parity of the next completion of fullbar[b]
+  static_assert(NST >= 1 && NST <= 8, "staging depth");
 
   long long t_ksum = 0, t_casc = 0, t_last = 0;
   for (int64_t rd = blockIdx.x; rd < rounds; rd += gridDim.x) {
@@ -210,9 +258,11 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
 #pragma unroll
           for (int i = 0; i < GZ; ++i) acc[a][j][i] = Real(0);
       stage(0, 0);
-      if (NST == 2 && P.m > 1) stage(1, 1);
+#pragma unroll
+      for (int q = 1; q < NST; ++q)
+        if (q < P.m) stage(q, q);
       for (int k = 0; k < P.m; ++k) {
-        const int b = NST == 2 ? (k & 1) : 0;
+        const int b = k % NST;
         mbar_wait(&fullbar[b], (phase >> b) & 1u);
         phase ^= 1u << b;
         const Real* Ts = Sbase + b * (A.TSZ + A.VSZ);
@@ -273,10 +323,9 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
 
     if (A.dbg && tid == 0) { const long long t = clock64(); t_ksum += t - t_last; t_last = t; }
     // ------------------------------------------------------------------ a3: cascade of unit u
-    // (CG units at a time, one thread group each; Yt and D are per group slot)
+    // (CG units at a time, one thread group each; Yt, D and the step descriptors are per group slot)
     for (int w0 = 0; w0 < GU; w0 += CG) {
     const int u = w0 + slot;
-    if (gt == 0) wflag[slot] = 0;
     const int p1 = p1f + u;
     const int cls0 = p0 & (S.fg_m - 1), cls1 = p1 & (S.fg_m - 1);
     const FGeom& G = A.geom[S.fg_off + cls0 * S.fg_m + cls1];
@@ -285,91 +334,101 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
     Real* X = Rbase + u * A.RSZ;                 // step input (R, then each step's approximation)
     Real* Yt = Ybase + slot * A.YSZ;
     Real* Dd = Dbase + slot * A.DS;
+    int* sd = &sdesc[slot][0][0];
+    // step descriptors: the class record's FStep fields translated to this unit (lane-parallel).
+    // field layout (FStep): 0 xr 1 xrl 2 xc 3 xcl 4 ar 5 arl 6 hlo 7 hlen 8 glo 9 glen
+    //                       10+ec blo0  14+ec blen0  18+ec blo1  22+ec blen1  26+ec doff
+    for (int i = gt; i < steps * 32; i += GT) {
+      const int si = i >> 5, fi = i & 31;
+      int val = 0;
+      if (fi < 30) {
+        val = reinterpret_cast<const int*>(&G.st[si])[fi];
+        if (fi == 0 || fi == 4) val += g_shift(d0, LEV, si);
+        else if (fi == 2) val += g_shift(d1, LEV, si);
+        else if (fi == 6 || fi == 8 || (fi >= 18 && fi < 22)) val += g_shift(d1, LEV, si + 1);
+        else if (fi >= 10 && fi < 14) val += g_shift(d0, LEV, si + 1);
+      }
+      sd[i] = val;
+    }
+    if (gt == 0) wflag[slot] = 0;
+    bar_group(1 + slot, GT);
     int xb = (p1 << LEV) + S.tSu[1] - roff;      // column of X's local index 0 (even)
     int xr0 = c0;                                // row of X's local index 0
     for (int s = 1; s <= steps; ++s) {
-      // this step's geometry, translated to the unit (fields read from the class record as needed)
-      const FStep& f = G.st[s - 1];
-      const int sa0 = g_shift(d0, LEV, s - 1), sa1 = g_shift(d1, LEV, s - 1);
-      const int sb0 = g_shift(d0, LEV, s), sb1 = g_shift(d1, LEV, s);
-      const int ar = f.ar + sa0, arl = f.arl;
-      const int hlo = f.hlo + sb1, hlen = f.hlen, glo = f.glo + sb1, glen = f.glen;
-      // pass A: rows of X (axis 1) -> Yt[col][row - yb]; task = (output block, row), row fastest
+      const int* d = sd + (s - 1) * 32;
+      const int ar = d[4], arl = d[5];
+      const int hlo = d[6], hlen = d[7], glo = d[8], glen = d[9];
+      // pass A: rows of X (axis 1) -> Yt[col][row - yb]; task = (8-column block of the union of the h and
+      // g output ranges, row), row fastest; a block inside both ranges computes both filters from one load
       const int yb = ar & ~(VW - 1);
       {
-        const int hb = (hlen + 7) >> 3, gb = (glen + 7) >> 3;
+        const int gend = glo + glen, hend = hlo + hlen;
+        const int ulo = glen ? (hlen ? min(hlo, glo) : glo) : hlo;
+        const int uhi = glen ? (hlen ? max(hend, gend) : gend) : hend;
+        const int nb = (uhi - ulo + 7) >> 3;
         const int rows = arl;
-        const int ntask = (hb + gb) * rows;
-        const int vlo = f.xc + sa1 - xb, vhi = vlo + f.xcl;
+        const int ntask = (hlen + glen) ? nb * rows : 0;
+        const int vlo = d[2] - xb, vhi = vlo + d[3];
         const float inv = 1.0f / float(max(rows, 1));
         for (int t = gt; t < ntask; t += GT) {
           const int q = __float2int_rz((float(t) + 0.5f) * inv);   // t / rows (exact for t < 2^20)
           const int rr = t - q * rows;
-          const int ty = q >= hb;
-          const int j0 = ty ? glo + 8 * (q - hb) : hlo + 8 * q;
-          const int jend = ty ? glo + glen : hlo + hlen;
-          const int nout = min(8, jend - j0);
+          const int j0 = ulo + 8 * q;
+          const bool doh = j0 < hend && j0 + 8 > hlo, dog = j0 < gend && j0 + 8 > glo;
           const int r = ar + rr;
           const Real* xrow = X + (r - xr0) * A.RS;
-          Real out[8];
-          if (s == 1) {   // R rows are zero-padded
-            if (ty) filt8<Real, L2, 1, false>(P, xrow, xb, j0, nout, vlo, vhi, out);
-            else filt8<Real, L2, 0, false>(P, xrow, xb, j0, nout, vlo, vhi, out);
-          } else {
-            if (ty) filt8<Real, L2, 1, true>(P, xrow, xb, j0, nout, vlo, vhi, out);
-            else filt8<Real, L2, 0, true>(P, xrow, xb, j0, nout, vlo, vhi, out);
-          }
-          const int ycol0 = ty ? hlen + (j0 - glo) : (j0 - hlo);
-          Real* yd = Yt + ycol0 * A.YS + (r - yb);
+          Real oh[8], og[8];
+          if (s == 1) filt8hg<Real, L2, false>(P, xrow, xb, j0, doh, dog, 8, 8, vlo, vhi, oh, og);
+          else filt8hg<Real, L2, true>(P, xrow, xb, j0, doh, dog, 8, 8, vlo, vhi, oh, og);
+          Real* yh = Yt + (j0 - hlo) * A.YS + (r - yb);
+          Real* yg = Yt + (hlen + j0 - glo) * A.YS + (r - yb);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (i < nout) yd[i * A.YS] = out[i];
+          for (int i = 0; i < 8; ++i) {
+            const int j = j0 + i;
+            if (doh && j >= hlo && j < hend) yh[i * A.YS] = oh[i];
+            if (dog && j >= glo && j < gend) yg[i * A.YS] = og[i];
+          }
         }
       }
       bar_group(1 + slot, GT);
-      // pass B: Yt rows (axis 0) -> approximation box (next X) and detail boxes (D);
-      // task = (box, row block, column), column fastest
+      // pass B: Yt rows (axis 0) -> approximation box (next X) and detail boxes (D); one flat task index
+      // over the four boxes (box, row block, column), column fastest
       int nxb = 0, nxr = 0;
       if (s < steps) {
-        const FStep& fn = G.st[s];
-        nxb = (fn.xc + g_shift(d1, LEV, s)) & ~(VW - 1);
-        nxr = fn.xr + g_shift(d0, LEV, s);
+        nxb = d[32 + 2] & ~(VW - 1);
+        nxr = d[32 + 0];
       }
       {
         const bool want0 = s < steps || s == P.J;
         const int vlo = ar - yb, vhi = vlo + arl;
-        int tbase = 0;
-#pragma unroll
-        for (int ec = 0; ec < 4; ++ec) {
+        const int n0 = want0 ? ((d[14] + 7) >> 3) * d[22] : 0;
+        const int n1 = n0 + ((d[15] + 7) >> 3) * d[23];
+        const int n2 = n1 + ((d[16] + 7) >> 3) * d[24];
+        const int n3 = n2 + ((d[17] + 7) >> 3) * d[25];
+        for (int t = gt; t < n3; t += GT) {
+          const int ec = (t >= n0) + (t >= n1) + (t >= n2);
+          const int idx = t - (ec == 0 ? 0 : ec == 1 ? n0 : ec == 2 ? n1 : n2);
+          const int bl0 = d[14 + ec], bl1 = d[22 + ec];
+          const int q = __float2int_rz((float(idx) + 0.5f) * __frcp_rn(float(bl1)));   // idx / bl1
+          const int cc = idx - q * bl1;
+          const int l0 = d[10 + ec] + 8 * q;
+          const int nrow = min(8, bl0 - 8 * q);
+          const int j = d[18 + ec] + cc;
           const int e0 = ec >> 1, e1 = ec & 1;
-          const int bl0 = f.blen0[ec], bl1 = f.blen1[ec];
-          const int cnt = (ec == 0 && !want0) ? 0 : ((bl0 + 7) >> 3) * bl1;
-          // continue the lane rotation across boxes so small boxes do not all start at lane 0
-          const int first = (gt - tbase % GT + GT) % GT;
-          tbase += cnt;
-          const int lo0 = f.blo0[ec] + sb0, lo1 = f.blo1[ec] + sb1;
-          const int ycb = e1 ? hlen - glo : -hlo;
-          const float inv = 1.0f / float(max(bl1, 1));
-          for (int t = first; t < cnt; t += GT) {
-            const int q = __float2int_rz((float(t) + 0.5f) * inv);   // t / bl1
-            const int cc = t - q * bl1;
-            const int l0 = lo0 + 8 * q;
-            const int nrow = min(8, bl0 - 8 * q);
-            const int j = lo1 + cc;
-            Real out[8];
-            if (e0) filt8<Real, L2, 1, true>(P, Yt + (ycb + j) * A.YS, yb, l0, nrow, vlo, vhi, out);
-            else filt8<Real, L2, 0, true>(P, Yt + (ycb + j) * A.YS, yb, l0, nrow, vlo, vhi, out);
-            if (ec == 0 && s < steps) {
-              Real* xd = X + (l0 - nxr) * A.RS + (j - nxb);
+          const int ycol = e1 ? hlen + (j - glo) : (j - hlo);
+          Real out[8];
+          if (e0) filt8<Real, L2, 1, true>(P, Yt + ycol * A.YS, yb, l0, nrow, vlo, vhi, out);
+          else filt8<Real, L2, 0, true>(P, Yt + ycol * A.YS, yb, l0, nrow, vlo, vhi, out);
+          if (ec == 0 && s < steps) {
+            Real* xd = X + (l0 - nxr) * A.RS + (j - nxb);
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (i < nrow) xd[i * A.RS] = out[i];
-            } else {
-              Real* dd = Dd + f.doff[ec] + (8 * q) * bl1 + cc;
+            for (int i = 0; i < 8; ++i)
+              if (i < nrow) xd[i * A.RS] = out[i];
+          } else {
+            Real* dd = Dd + d[26 + ec] + (8 * q) * bl1 + cc;
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (i < nrow) dd[i * bl1] = out[i];
-            }
+            for (int i = 0; i < 8; ++i)
+              if (i < nrow) dd[i * bl1] = out[i];
           }
         }
       }
@@ -396,12 +455,12 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
         const int b0 = D == 0 ? p0 : (D < 0 ? (p0 << -D) : (p0 >> D));
         const int b1 = D == 0 ? p1 : (D < 0 ? (p1 << -D) : (p1 >> D));
         const int l0 = b0 + e.y, l1 = b1 + e.z;
-        const FStep& f = G.st[s - 1];
         const int ec = Lb.e;
-        const int lo0 = f.blo0[ec] + g_shift(d0, lev, s), lo1 = f.blo1[ec] + g_shift(d1, lev, s);
-        const int i0 = l0 - lo0, i1 = l1 - lo1;
+        const int* dl = sd + (s - 1) * 32;
+        const int i0 = l0 - dl[10 + ec], i1 = l1 - dl[18 + ec];
+        const int bl1 = dl[22 + ec];
         Real x = Real(0);
-        if (i0 >= 0 && i0 < f.blen0[ec] && i1 >= 0 && i1 < f.blen1[ec]) x = Dd[f.doff[ec] + i0 * f.blen1[ec] + i1];
+        if (i0 >= 0 && i0 < dl[14 + ec] && i1 >= 0 && i1 < bl1) x = Dd[dl[26 + ec] + i0 * bl1 + i1];
         wrap |= (l0 < 0) | (l0 >= Lb.nl) | (l1 < 0) | (l1 >= Lb.nl);
         const int c = int(Lb.offset + int64_t(l0 & (Lb.nl - 1)) * Lb.nl + (l1 & (Lb.nl - 1)));
         sv[jj] = x;
@@ -437,8 +496,8 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
 bool fine_config(int real_bytes, int level, int L2, FineCfg* c) {
   if (L2 != 2 && L2 != 4 && L2 != 8 && L2 != 12) return false;
   if (real_bytes == 4) {
-    if (level == 1) { *c = FineCfg{8, 11, 1, 2, 4}; return true; }
-    if (level == 2) { *c = FineCfg{4, 15, 1, 1, 4}; return true; }
+    if (level == 1) { *c = FineCfg{8, 11, 1, 4, 4}; return true; }
+    if (level == 2) { *c = FineCfg{4, 15, 1, 2, 4}; return true; }
     if (level == 3) { *c = FineCfg{2, 11, 3, 1, 2}; return true; }
   } else {
     if (level == 1) { *c = FineCfg{4, 11, 1, 1, 4}; return true; }
@@ -463,8 +522,8 @@ template <int L2>
 static cudaError_t launch_fine_l2(const Plan& P, const FineArgs& A, int real_bytes, int level, int grid, size_t smem,
                                   cudaStream_t st) {
   if (real_bytes == 4) {
-    if (level == 1) return launch_fine_t<float, L2, 1, 8, 11, 1, 2, 4>(P, A, grid, smem, st);
-    if (level == 2) return launch_fine_t<float, L2, 2, 4, 15, 1, 1, 4>(P, A, grid, smem, st);
+    if (level == 1) return launch_fine_t<float, L2, 1, 8, 11, 1, 4, 4>(P, A, grid, smem, st);
+    if (level == 2) return launch_fine_t<float, L2, 2, 4, 15, 1, 2, 4>(P, A, grid, smem, st);
     if (level == 3) return launch_fine_t<float, L2, 3, 2, 11, 3, 1, 2>(P, A, grid, smem, st);
   } else {
     if (level == 1) return launch_fine_t<double, L2, 1, 4, 11, 1, 1, 4>(P, A, grid, smem, st);
