@@ -95,8 +95,12 @@ def dist_env():
 
 
 def cpu_oracle_rate(p, budget_s: float = 20.0, seed: int = 0):
-    """Oracle (oracle/rows.c + brute-force band ranking) timed on a bounded stratified sample of
-    units: per level, a few units are computed and timed; entries/s = L·N / Σ_level count·t̄."""
+    """Oracle (oracle/rows.c + brute-force band ranking) timed on a bounded stratified sample of units.
+
+    Per level, a few units are computed (one batch, OpenMP over units) and timed; the per-unit wall time
+    with all threads busy is extrapolated to every unit of the level: entries/s = nnz / Σ_level count·t̄.
+    Fine levels take one unit per thread; levels whose units cost more (window ≥ n/4) take one unit
+    each, computed together in a single batch so the threads stay busy."""
     from oracle import basis
     from oracle import retention as ret
     from oracle import rows as R
@@ -105,18 +109,23 @@ def cpu_oracle_rate(p, budget_s: float = 20.0, seed: int = 0):
     levels = {}
     for (lev, e, off, nl) in basis.subbands(p.d, p.n, p.J):
         levels.setdefault(lev, []).append((off, nl ** p.d))
-    t_total_est = 0.0
-    sampled = 0
-    spent = 0.0
+    lev_order = sorted(levels)
+    R_ = int(p.meta.get("R", 0)) if hasattr(p, "meta") else 0
+    fine = [l for l in lev_order if ((2 ** l - 1) * (len(p.h) - 1) + 1 + 2 * R_) < p.n // 4]
+    coarse = [l for l in lev_order if l not in fine]
+    t_total_est, sampled, spent = 0.0, 0, 0.0
     per_level = {}
-    for lev in sorted(levels):                       # finest (cheapest) first
+
+    def pick(lev, k):
         offs = levels[lev]
-        count = sum(c for _, c in offs)
-        k = nthreads if spent < budget_s else 1
-        units = []
+        out = []
         for _ in range(k):
             off, c = offs[int(rng.integers(len(offs)))]
-            units.append(off + int(rng.integers(c)))
+            out.append(off + int(rng.integers(c)))
+        return out
+
+    for lev in fine:
+        units = pick(lev, nthreads if spent < budget_s else 1)
         t0 = time.perf_counter()
         rows = R.rows(p, units, nthreads=nthreads)
         for i, mu in enumerate(units):
@@ -124,9 +133,23 @@ def cpu_oracle_rate(p, budget_s: float = 20.0, seed: int = 0):
         dt = time.perf_counter() - t0
         spent += dt
         sampled += len(units)
-        per_unit = dt / len(units)                   # wall seconds per unit with `nthreads` workers
-        per_level[lev] = per_unit
-        t_total_est += per_unit * count
+        per_level[lev] = dt / len(units) * min(1.0, len(units) / nthreads) if len(units) < nthreads else dt / len(units)
+    if coarse:
+        units = [u for lev in coarse for u in pick(lev, 1)]
+        t0 = time.perf_counter()
+        rows = R.rows(p, units, nthreads=nthreads)
+        for i, mu in enumerate(units):
+            ret.retained_row(p, mu, rows[i])
+        dt = time.perf_counter() - t0
+        spent += dt
+        sampled += len(units)
+        # units ran concurrently (≤ 1 thread each): a unit's cost with every thread busy is dt / nthreads
+        # when there are at least as many units as threads, else dt·(units/threads) / units = dt / threads
+        for lev in coarse:
+            per_level[lev] = dt / max(nthreads, len(units))
+    for lev in lev_order:
+        count = sum(c for _, c in levels[lev])
+        t_total_est += per_level[lev] * count
     nnz = p.N * p.band_L if p.retain == "band" else p.N * p.N
     return {"value": nnz / t_total_est, "unit": "entries/s", "cores": nthreads, "kind": "oracle",
             "sample": (f"{sampled} units stratified over {len(levels)} levels ({spent:.1f} s wall on "
@@ -183,6 +206,7 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     phase = np.zeros(3)
+    lp_acc = []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -195,6 +219,7 @@ def run_ours(args):
             ev[i][1].synchronize()
             ms3, fma3 = dec.phase_times()
             phase += np.array(ms3)
+            lp_acc.append(dec.launch_profile())
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -203,31 +228,40 @@ def run_ours(args):
     nnz = info.nnz
     launches = info.kernel_launches
     if world > 1:
-        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_ms = float(t.item())
-        tot = torch.tensor([nnz], dtype=torch.float64, device=dev)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        nnz_all = int(tot.item())
+        from paper_2005_09870_b200 import pcwd as PW
+        t_ms = PW.allreduce_max(t_ms, dev)          # max over ranks
+        nnz_all = int(PW.allreduce_sum(float(nnz), dev))
     else:
         nnz_all = nnz
     ms_per_step = t_ms / args.steps
     value = nnz_all / (ms_per_step * 1e-3)
 
-    # dominant kernel: the fused unit kernels (phase 1), FP32 FMA pipe roofline
+    # dominant kernel: the unit-kernel launch with the largest time (CUDA events around each launch on the
+    # decompose stream), FP32 FMA-pipe roofline; achieved = its algorithmic FMAs (SURVEY §8(d) per-unit
+    # figure × its units) / its mean duration
+    klist = [[0.0, 0.0, "", 0] for _ in lp_acc[0]] if lp_acc else []
+    for lp in lp_acc:
+        for i, (ms, fma, kind, lev) in enumerate(lp):
+            klist[i][0] += ms / len(lp_acc)
+            klist[i][1], klist[i][2], klist[i][3] = fma, kind, lev
+    dom = max(klist, key=lambda x: x[0])
     ms_units = phase[1] / args.steps
     ms_tmpl = phase[0] / args.steps
-    fma_units = fma3[1]
-    achieved = 2.0 * fma_units / (ms_units * 1e-3) / 1e12
     peaks = _peaks()
     sm_max = peaks.get("sm_max_mhz", 1965.0)
-    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # derived (DESIGN.md §5): SMs × lanes × 2 × clock
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # derived (DESIGN.md §8): SMs × lanes × 2 × clock
+    achieved = 2.0 * dom[1] / (dom[0] * 1e-3) / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": None,
-                "kernel": "unit_kernel<float,float,2,BAND> launches (a2+a3+a4)",
-                "kernel_ms": ms_units, "templates_ms": ms_tmpl,
-                "fma_per_launch_set": fma_units,
+                "kernel": f"{dom[2]} unit kernel, level {dom[3]} (a2 k-sum + a3 cascade + a4 gather)",
+                "kernel_ms": dom[0], "kernel_share_of_step": dom[0] / ms_per_step,
+                "fma_per_launch": dom[1],
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz of MEASURED_PEAKS.json",
+                "all_unit_kernels": {"ms": ms_units, "tflops": 2.0 * fma3[1] / (ms_units * 1e-3) / 1e12,
+                                     "frac": 2.0 * fma3[1] / (ms_units * 1e-3) / 1e12 / fp32_peak},
+                "templates_ms": ms_tmpl,
+                "launches": [{"kind": k, "level": lv, "ms": round(m, 4), "tflops": round(2 * f / (m * 1e-3) / 1e12, 2)}
+                             for (m, f, k, lv) in klist],
                 "hbm_achieved_gbs": info.bytes_algorithmic / (ms_per_step * 1e-3) / 1e9,
                 "hbm_peak_gbs": peaks.get("hbm_gbs")}
 

@@ -122,6 +122,12 @@ int pcwd_info(void* handle, pcwd_info_t* out);
  * threshold max/count passes).  out_ms[3] receives milliseconds of the last decompose;
  * out_fma[3] the algorithmic FMAs of phases 0 and 1 (phase 2: 0). */
 int pcwd_profile(void* handle, int enable);
+/* Per unit-kernel launch of the last decompose (profiling enabled): *count = launches; for the first
+ * `max` of them, out_ms = duration (CUDA events on the decompose stream), out_fma = algorithmic FMAs of
+ * the units it processed, out_kind = 0 generic / 1 tile / 2 fine / 3 batched (coarse),
+ * out_level = wavelet level ℓ of its units.  Any output pointer may be NULL.  Synchronous. */
+int pcwd_launch_profile(void* handle, int max, int* count, double* out_ms, double* out_fma, int* out_kind,
+                        int* out_level);
 int pcwd_phase_times(void* handle, double* out_ms, double* out_fma);
 int pcwd_destroy(void* handle);
 

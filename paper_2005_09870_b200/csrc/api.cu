@@ -70,6 +70,7 @@ struct Handle {
   int nlaunch = 0;
   bool profile = false;
   cudaEvent_t ev[8] = {};
+  std::vector<cudaEvent_t> lev;     // profile: one event pair per unit launch (run_units)
   int64_t rows() const { return hp.row1 - hp.row0; }
 };
 
@@ -169,9 +170,31 @@ int build_templates(Handle* h, cudaStream_t st) {
   return PCWD_OK;
 }
 
+// Algorithmic FMA (SURVEY §8(d) per-unit figure, SubBand::fma) of the units [u0, u1).
+double units_fma(const Plan& P, int64_t u0, int64_t u1) {
+  double f = 0.0;
+  for (int s = 0; s < P.nsb; ++s) {
+    const int64_t a = std::max(u0, P.sb[s].offset), b = std::min(u1, P.sb[s].offset + P.sb[s].count);
+    if (b > a) f += P.sb[s].fma * double(b - a);
+  }
+  return f;
+}
+
 int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
   const Plan& P = h->hp.P;
+  if (h->profile && h->lev.size() < 2 * h->launches.size()) {
+    for (auto& e : h->lev) cudaEventDestroy(e);
+    h->lev.assign(2 * h->launches.size(), nullptr);
+    for (auto& e : h->lev) CK(cudaEventCreate(&e));
+  }
+  int li = -1;
   for (const Launch& L : h->launches) {
+    ++li;
+    if (h->profile) cudaEventRecord(h->lev[2 * li], st);
+    struct Rec {   // record the launch's end event on every path out of this iteration
+      Handle* h; int i; cudaStream_t st;
+      ~Rec() { if (h->profile) cudaEventRecord(h->lev[2 * i + 1], st); }
+    } rec_end{h, li, st};
     if (L.batched) {
       if (mode != MODE_BAND) return fail(PCWD_E_STATE, "batched launch outside BAND mode");
       BatchArgs B = L.ba;
@@ -918,11 +941,34 @@ int pcwd_phase_times(void* handle, double* out_ms, double* out_fma) {
   return PCWD_OK;
 }
 
+int pcwd_launch_profile(void* handle, int max, int* count, double* out_ms, double* out_fma, int* out_kind,
+                        int* out_level) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !count) return fail(PCWD_E_PARAM, "NULL argument");
+  if (!h->profile || h->lev.size() < 2 * h->launches.size())
+    return fail(PCWD_E_STATE, "profiling not enabled before the last decompose");
+  CK(cudaSetDevice(h->desc.device));
+  const int n = int(h->launches.size());
+  *count = n;
+  for (int i = 0; i < n && i < max; ++i) {
+    const Launch& L = h->launches[i];
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->lev[2 * i], h->lev[2 * i + 1]));
+    if (out_ms) out_ms[i] = ms;
+    if (out_fma) out_fma[i] = units_fma(h->hp.P, L.u0, L.u1);
+    if (out_kind) out_kind[i] = L.fine ? 2 : L.tile ? 1 : L.batched ? 3 : 0;
+    if (out_level) out_level[i] = h->hp.P.sb[find_subband(h->hp.P, L.u0)].level;
+  }
+  return PCWD_OK;
+}
+
 int pcwd_destroy(void* handle) {
   Handle* h = static_cast<Handle*>(handle);
   if (!h) return PCWD_OK;
   cudaSetDevice(h->desc.device);
   for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : h->lev)
     if (e) cudaEventDestroy(e);
   free_all(h);
   delete h;

@@ -52,7 +52,7 @@ class Info(ctypes.Structure):
 EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_max", "pcwd_get_csr",
            "pcwd_copy_csr", "pcwd_apply", "pcwd_info", "pcwd_destroy", "pcwd_error_string",
            "pcwd_last_error", "pcwd_validate", "pcwd_plan_shard", "pcwd_plan_stencil",
-           "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times"]
+           "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile"]
 
 _lib = None
 
@@ -83,6 +83,8 @@ def lib():
         L.pcwd_plan_num_subbands.argtypes = [ctypes.POINTER(Desc), i32p]
         L.pcwd_profile.argtypes = [vp, ctypes.c_int]
         L.pcwd_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+        dp = ctypes.POINTER(ctypes.c_double)
+        L.pcwd_launch_profile.argtypes = [vp, ctypes.c_int, i32p, dp, dp, i32p, i32p]
         for f in EXPORTS:
             getattr(L, f)  # every declared symbol must exist
         _lib = L
@@ -179,6 +181,19 @@ class Decomposition:
         fm = (ctypes.c_double * 3)()
         _check(lib().pcwd_phase_times(self._h, ms, fm), "pcwd_phase_times")
         return list(ms), list(fm)
+
+    def launch_profile(self):
+        """[(ms, algorithmic_fma, kind, level)] per unit-kernel launch of the last decompose."""
+        cnt = ctypes.c_int32()
+        _check(lib().pcwd_launch_profile(self._h, 0, ctypes.byref(cnt), None, None, None, None), "pcwd_launch_profile")
+        n = cnt.value
+        ms = (ctypes.c_double * n)()
+        fm = (ctypes.c_double * n)()
+        kd = (ctypes.c_int32 * n)()
+        lv = (ctypes.c_int32 * n)()
+        _check(lib().pcwd_launch_profile(self._h, n, ctypes.byref(cnt), ms, fm, kd, lv), "pcwd_launch_profile")
+        kinds = {0: "generic", 1: "tile", 2: "fine", 3: "batched"}
+        return [(ms[i], fm[i], kinds[kd[i]], lv[i]) for i in range(n)]
 
     def csr_meta(self) -> Csr:
         out = Csr()
