@@ -33,6 +33,7 @@ struct Launch {
   BatchArgs ba{};
   int64_t maxX0 = 0, maxY = 0, maxB = 0;
   int64_t workA[kMaxJ + 1] = {}, workB[kMaxJ + 1] = {};   // batched: per-step work items of pass A / B
+  int64_t appr0[kMaxJ + 1] = {}, appr1[kMaxJ + 1] = {};   // batched: per-step max approximation window
   int steps = 0;
 };
 
@@ -139,8 +140,12 @@ int build_templates(Handle* h, cudaStream_t st) {
   const HostPlan& hp = h->hp;
   CK(launch_phi0(P, h->u_d, h->phi[0], hp.phiS[0][0], hp.phiW[0][0], hp.phiS[1][0], hp.phiW[1][0], st));
   h->nlaunch++;
+  // only the levels of the sub-bands this shard owns (the à-trous chain runs up to the coarsest of them)
+  int maxlev = 1;
+  for (int s = 0; s < P.nsb; ++s)
+    if (P.sb[s].offset < hp.row1 && P.sb[s].offset + P.sb[s].count > hp.row0) maxlev = std::max(maxlev, P.sb[s].level);
   int cur = 0;
-  for (int lev = 1; lev <= P.J; ++lev) {
+  for (int lev = 1; lev <= maxlev; ++lev) {
     TmplArgs A{};
     A.phi_in = h->phi[cur];
     A.phi_out = h->phi[cur ^ 1];
@@ -206,7 +211,7 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
       B.col = h->col;
       B.val = h->val;
       int nl = 0;
-      CK(launch_band_batched(P, B, h->hp.real_bytes, L.maxX0, L.workA, L.workB, L.steps, st, &nl));
+      CK(launch_band_batched(P, B, h->hp.real_bytes, L.maxX0, L.workA, L.workB, L.appr0, L.appr1, L.steps, st, &nl));
       h->nlaunch += nl;
       continue;
     }
@@ -565,7 +570,9 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       }
     }
     Launch T{0, 0, 0, 0};
-    if (tile_ok && !getenv("PCWD_NO_TILE")) {
+    // the tile kernel only where the fine kernel does not apply and windows are small (levels ≤ 3); coarser
+    // levels run faster on the batched path (tiled k-sum + fused approximation steps)
+    if (tile_ok && lev <= 3 && !getenv("PCWD_NO_TILE")) {
       // per-unit scratch of the tile kernel: X (R window and approximations), Yt, D boxes, stage
       const SubBand& S0 = P.sb[s];
       const int VW = 16 / rb;
@@ -701,6 +708,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           mb = std::max(mb, 4 * o0 * o1);
           B.workA[st] = std::max(B.workA[st], w0 * ((o1 + 3) / 4));
           B.workB[st] = std::max(B.workB[st], ((o0 + 3) / 4) * o1);
+          B.appr0[st] = std::max(B.appr0[st], o0);
+          B.appr1[st] = std::max(B.appr1[st], o1);
           w0 = o0; w1 = o1; nl0 >>= 1; nl1 >>= 1;
         }
       }

@@ -272,6 +272,116 @@ __global__ void __launch_bounds__(kB) bk_passB(const __grid_constant__ Plan P, c
   }
 }
 
+// Fused approximation step s (axis 1 then axis 0) for windows of any size: one CTA computes a 32 × 32 (fp64: 16 × 16) tile of
+// the level-s approximation window of one unit.  The (62 + 2δ)² input tile is read from the unit's step
+// input (zero outside its window, periodic where the window covers a line) into shared memory, filtered
+// along axis 1 into a second tile, then along axis 0 into the next approximation (h taps only; the
+// stencil's detail coefficients are computed directly by bk_gather).
+template <typename Real, int L2>
+__global__ void __launch_bounds__(kB) bk_approx(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
+                                                int s, int ntx) {
+  constexpr int TO = sizeof(Real) == 4 ? 32 : 16;   // outputs per tile side (static smem < 48 KB)
+  constexpr int TI = 2 * (TO - 1) + L2;              // inputs per tile side
+  constexpr int XS = ((TI + 2 + 3) / 4) * 4 + 2;     // even row stride, ≡ 2 mod 4 (conflict-free pair loads)
+  constexpr int NI = 2 * 3 + L2;                     // inputs of 4 consecutive outputs
+  __shared__ __align__(16) Real Xs[TI][XS];
+  __shared__ Real Ys[TI][TO + 1];
+  __shared__ int lr[TI], lc[TI];
+  const int64_t unit = A.u0 + blockIdx.y;
+  const UnitPos up = unit_pos(P, unit);
+  const SubBand& S = P.sb[up.sbi];
+  if (!(s < S.steps || s == P.J)) return;
+  Range in0, in1;
+  step_in(P, S, up, s, in0, in1);
+  const Range a0 = step_out(in0, L2, 0), a1 = step_out(in1, L2, 0);
+  const int ty = blockIdx.x / ntx, tx = blockIdx.x - ty * ntx;
+  const int j0 = ty * TO, k0 = tx * TO;
+  if (j0 >= a0.len || k0 >= a1.len) return;
+  Real* base = reinterpret_cast<Real*>(A.scratch) + int64_t(blockIdx.y) * A.stride;
+  const Real* X = base + ((s & 1) ? S.offX0 : S.offX1);
+  Real* Xn = base + ((s & 1) ? S.offX1 : S.offX0);
+  // input positions of the tile: 2·(a.lo + j0) + i on the input grid, i < TI; local indices are separable
+  const int g0 = 2 * (a0.lo + j0), g1 = 2 * (a1.lo + k0);
+  for (int i = threadIdx.x; i < TI; i += kB) {
+    lr[i] = local_index(in0, g0 + i);
+    lc[i] = local_index(in1, g1 + i);
+  }
+  __syncthreads();
+  {
+    // asynchronous element copies (many in flight); elements outside the window are zero-filled
+    const bool fast = lr[0] >= 0 && lr[TI - 1] == lr[0] + TI - 1 && lc[0] >= 0 && lc[TI - 1] == lc[0] + TI - 1;
+    for (int idx = threadIdx.x; idx < TI * TI; idx += kB) {
+      const int r = idx / TI, c = idx - r * TI;
+      int li0, li1;
+      if (fast) { li0 = lr[0] + r; li1 = lc[0] + c; }
+      else { li0 = lr[r]; li1 = lc[c]; }
+      const bool ok = li0 >= 0 && li1 >= 0;
+      const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&Xs[r][c]));
+      const Real* src = X + (ok ? int64_t(li0) * in1.len + li1 : 0);
+      const unsigned nbytes = ok ? unsigned(sizeof(Real)) : 0u;
+      if constexpr (sizeof(Real) == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(src), "r"(nbytes) : "memory");
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(nbytes) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+  // axis 1: Ys[r][c] = Σ_t h[t] Xs[r][2c + t]; task = (row, 4 consecutive outputs), row fastest
+  for (int idx = threadIdx.x; idx < TI * (TO / 4); idx += kB) {
+    const int cq = idx / TI, r = idx - cq * TI;
+    Real x[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) x[i] = Xs[r][8 * cq + i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      Real acc = Real(0);
+#pragma unroll
+      for (int t = 0; t < L2; ++t) acc = fmaB(TapsOf<Real>::get(P, 0, t), x[2 * q + t], acc);
+      Ys[r][4 * cq + q] = acc;
+    }
+  }
+  __syncthreads();
+  // axis 0: out[j][c] = Σ_t h[t] Ys[2j + t][c]; task = (4 consecutive output rows, column), column fastest
+  for (int idx = threadIdx.x; idx < (TO / 4) * TO; idx += kB) {
+    const int jq = idx / TO, c = idx - jq * TO;
+    if (k0 + c >= a1.len) continue;
+    Real y[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) y[i] = Ys[8 * jq + i][c];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = 4 * jq + q;
+      if (j0 + j >= a0.len) break;
+      Real acc = Real(0);
+#pragma unroll
+      for (int t = 0; t < L2; ++t) acc = fmaB(TapsOf<Real>::get(P, 0, t), y[2 * q + t], acc);
+      Xn[int64_t(j0 + j) * a1.len + k0 + c] = acc;
+    }
+  }
+}
+
+template <typename Real>
+static void launch_approx(const Plan& P, const BatchArgs& A, int s, int64_t maxA0, int64_t maxA1, int nb,
+                          cudaStream_t st) {
+  constexpr int TO = sizeof(Real) == 4 ? 32 : 16;
+  const int ntx = int((maxA1 + TO - 1) / TO), nty = int((maxA0 + TO - 1) / TO);
+  const dim3 grid(ntx * nty, nb);
+  switch (P.L2) {
+    case 2: bk_approx<Real, 2><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 4: bk_approx<Real, 4><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 6: bk_approx<Real, 6><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 8: bk_approx<Real, 8><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 10: bk_approx<Real, 10><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 12: bk_approx<Real, 12><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    default: {
+      auto gx = [](int64_t elems) { return int(std::max<int64_t>(1, std::min<int64_t>((elems + kB - 1) / kB, 64))); };
+      bk_passA<Real><<<dim3(gx(maxA0 * 2 * maxA1 / 4 + 1), nb), kB, 0, st>>>(P, A, s);
+      bk_passB<Real><<<dim3(gx(maxA0 * maxA1 / 4 + 1), nb), kB, 0, st>>>(P, A, s);
+    }
+  }
+}
+
 // gather the stencil entries of level s: details computed directly from the step's input
 // window X (level s-1): d(l0,l1) = Σ_{t0,t1} f_{e0}[t0] f_{e1}[t1] X[2l0+o_{e0}+t0][2l1+o_{e1}+t1];
 // the coarse block (e = 0, s = J) is read from the approximation output.
@@ -395,7 +505,8 @@ static bool launch_ksum_tiled(const Plan& P, const BatchArgs& A, int nb, cudaStr
 
 template <typename Real>
 static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0, const int64_t* workA,
-                               const int64_t* workB, int steps, cudaStream_t st, int* launches) {
+                               const int64_t* workB, const int64_t* appr0, const int64_t* appr1, int steps,
+                               cudaStream_t st, int* launches) {
   const int64_t units = A0.u1 - A0.u0;
   for (int64_t b0 = 0; b0 < units; b0 += A0.batch) {
     BatchArgs A = A0;
@@ -405,11 +516,18 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
     auto gx = [](int64_t elems) { return int(std::max<int64_t>(1, std::min<int64_t>((elems + kB - 1) / kB, 64))); };
     if (!launch_ksum_tiled<Real>(P, A, nb, st)) bk_ksum<Real><<<dim3(gx(maxX0), nb), kB, 0, st>>>(P, A);
     ++*launches;
+    static const bool old_passes = getenv("PCWD_OLD_PASSES") != nullptr;
     for (int s = 1; s <= steps; ++s) {
-      bk_passA<Real><<<dim3(gx(workA[s]), nb), kB, 0, st>>>(P, A, s);
-      bk_passB<Real><<<dim3(gx(workB[s]), nb), kB, 0, st>>>(P, A, s);
+      if (old_passes) {
+        bk_passA<Real><<<dim3(gx(workA[s]), nb), kB, 0, st>>>(P, A, s);
+        bk_passB<Real><<<dim3(gx(workB[s]), nb), kB, 0, st>>>(P, A, s);
+        *launches += 2;
+      } else {
+        launch_approx<Real>(P, A, s, appr0[s], appr1[s], nb, st);
+        *launches += 1;
+      }
       bk_gather<Real><<<dim3(1, nb), kB, 0, st>>>(P, A, s);
-      *launches += 3;
+      *launches += 1;
     }
     const size_t sm = ((P.band_Lpad * 4 + 15) & ~15) + size_t(P.band_Lpad) * sizeof(Real);
     bk_write<Real><<<nb, kB, sm, st>>>(P, A);
@@ -421,9 +539,10 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
 }
 
 cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, const int64_t* workA,
-                                const int64_t* workB, int steps, cudaStream_t st, int* launches) {
-  return real_bytes == 4 ? run_batch_t<float>(P, A, maxX0, workA, workB, steps, st, launches)
-                         : run_batch_t<double>(P, A, maxX0, workA, workB, steps, st, launches);
+                                const int64_t* workB, const int64_t* appr0, const int64_t* appr1, int steps,
+                                cudaStream_t st, int* launches) {
+  return real_bytes == 4 ? run_batch_t<float>(P, A, maxX0, workA, workB, appr0, appr1, steps, st, launches)
+                         : run_batch_t<double>(P, A, maxX0, workA, workB, appr0, appr1, steps, st, launches);
 }
 
 }  // namespace pcwd

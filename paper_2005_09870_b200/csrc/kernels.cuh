@@ -95,7 +95,8 @@ struct BatchArgs {
 };
 
 cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, const int64_t* workA,
-                                const int64_t* workB, int steps, cudaStream_t st, int* launches);
+                                const int64_t* workB, const int64_t* appr0, const int64_t* appr1, int steps,
+                                cudaStream_t st, int* launches);
 
 struct TmplArgs {
   const double* phi_in;     // m × Win0 × Win1 (fp64)

@@ -264,7 +264,9 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
     hp->phi_elems = std::max<int64_t>(hp->phi_elems, int64_t(in0.W) * in1.W);
     hp->phi_elems = std::max<int64_t>(hp->phi_elems, int64_t(o0.W) * o1.W);
     hp->y_elems = std::max<int64_t>(hp->y_elems, 2 * int64_t(in0.W) * o1.W);
-    hp->fma_templates += double(P.m) * L2 * (2.0 * in0.W * o1.W + (P.d == 2 ? 4.0 * o0.W * o1.W : 0.0));
+    const double tf = double(P.m) * L2 * (2.0 * in0.W * o1.W + (P.d == 2 ? 4.0 * o0.W * o1.W : 0.0));
+    hp->fma_templates += tf;
+    hp->tmpl_fma_level[lev] = tf;
   }
   for (int s = 0; s < ns; ++s) {
     SubBand& S = P.sb[s];
@@ -410,15 +412,29 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
       }
   }
 
-  // shard: contiguous unit ranges with equal algorithmic cost (units in Λ order)
+  // shard: contiguous unit ranges (Λ order) with equal estimated time.  A unit's time is its algorithmic
+  // FMA count times a per-path weight (measured on B200: coarse-level units — batched / tile kernels — run
+  // ≈3× slower per FMA than units on the fine kernel); the template chain up to level ℓ is charged to the
+  // first unit of level ℓ (its owner builds it).  Boundaries are rounded to 16 units so every shard keeps
+  // whole rounds of the fine and tiled kernels.
+  std::vector<double> ucost(ns, 0.0), lump(ns, 0.0);
+  for (int s = 0; s < ns; ++s) {
+    const SubBand& S = P.sb[s];
+    const bool fine = P.retain == PCWD_RETAIN_BAND && S.fg_m > 0 && S.level <= 3;
+    ucost[s] = S.fma * (P.retain == PCWD_RETAIN_BAND && !fine ? 3.0 : 1.0);
+  }
+  for (int lev = 1; lev <= J; ++lev) {
+    const int s = sb_index(P.d, J, lev, 1);   // first detail sub-band of the level in Λ order
+    lump[lev == J ? 0 : s] += hp->tmpl_fma_level[lev] * 2.0;   // fp64 template passes: DFMA at half rate
+  }
   double total = 0.0;
-  for (int s = 0; s < ns; ++s) total += P.sb[s].fma * double(P.sb[s].count);
+  for (int s = 0; s < ns; ++s) total += ucost[s] * double(P.sb[s].count) + lump[s];
   auto unit_at_cost = [&](double c) -> int64_t {   // first unit whose prefix cost ≥ c
     double acc = 0.0;
     for (int s = 0; s < ns; ++s) {
-      double sc = P.sb[s].fma * double(P.sb[s].count);
+      double sc = ucost[s] * double(P.sb[s].count) + lump[s];
       if (acc + sc >= c) {
-        int64_t k = int64_t(std::ceil((c - acc) / P.sb[s].fma - 1e-9));
+        int64_t k = ucost[s] > 0 ? int64_t(std::ceil((c - acc - lump[s]) / ucost[s] - 1e-9)) : 0;
         k = std::max<int64_t>(0, std::min<int64_t>(k, P.sb[s].count));
         return P.sb[s].offset + k;
       }
@@ -426,8 +442,10 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
     }
     return P.N;
   };
-  hp->row0 = d->rank == 0 ? 0 : unit_at_cost(total * d->rank / d->world);
-  hp->row1 = d->rank == d->world - 1 ? P.N : unit_at_cost(total * (d->rank + 1) / d->world);
+  auto align16 = [&](int64_t u) { return P.N >= 256 ? std::min<int64_t>(P.N, (u + 8) / 16 * 16) : u; };
+  hp->row0 = d->rank == 0 ? 0 : align16(unit_at_cost(total * d->rank / d->world));
+  hp->row1 = d->rank == d->world - 1 ? P.N : align16(unit_at_cost(total * (d->rank + 1) / d->world));
+  if (hp->row1 < hp->row0) hp->row1 = hp->row0;
   double f = 0.0;
   for (int s = 0; s < ns; ++s) {
     int64_t a = std::max(hp->row0, P.sb[s].offset);

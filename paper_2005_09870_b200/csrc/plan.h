@@ -28,6 +28,7 @@ struct HostPlan {
   // template φ-chain windows per axis and level (ℓ = 0..J), and the ψ-window start per level
   int phiS[2][kMaxJ + 1] = {}, phiW[2][kMaxJ + 1] = {}, psiS[2][kMaxJ + 1] = {};
   double fma_templates = 0.0;
+  double tmpl_fma_level[kMaxJ + 1] = {};   // template FMAs of each level's à-trous step
   std::vector<FGeom> fgeom;       // BAND, fine levels: class geometry records (SubBand::fg_off / fg_m)
 };
 
