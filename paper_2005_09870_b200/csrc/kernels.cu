@@ -47,67 +47,98 @@ __device__ __forceinline__ double win_read(const double* buf, int y, int S, int 
   return li < W ? buf[li * stride] : 0.0;
 }
 
-template <typename Real>
+// One à-trous step of the template recursion along one axis, QT outputs per thread: the outputs at positions
+// y, y + dil, …, y + (QT-1)·dil of one line share all but one input each (the filter is dilated by dil), so
+// a thread reads QT + 2δ - 1 inputs for QT·2δ FMAs (fp64).
+constexpr int QT = 8;
+
+template <typename Real, int L2>
 __global__ void tmpl_passA(const __grid_constant__ Plan P, const __grid_constant__ TmplArgs A, int coarse_level,
                            int level) {
-  // along axis 1: Y[k][e1][i0][j1] = Σ_j f_{e1}[j] φ(i0, y1 - dil (o_{e1} + j))
-  const int mask = P.n - 1;
+  // along axis 1: Y[k][e1][i0][j1] = Σ_t f_{e1}[t] φ(i0, y1 - dil (o_{e1} + t)),  y1 = Sout[e1] + j1
+  const int mask = P.n - 1, dil = A.dil;
   const int Win0 = A.Win[0], Win1 = A.Win[1], Wout1 = A.Wout[1];
-  const int64_t total = int64_t(P.m) * 2 * Win0 * Wout1;
+  const int ngr = (Wout1 + dil * QT - 1) / (dil * QT);   // groups of QT outputs per residue
+  const int64_t total = int64_t(P.m) * 2 * Win0 * dil * ngr;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
-    int j1 = int(idx % Wout1);
-    int64_t t = idx / Wout1;
-    int i0 = int(t % Win0);
+    const int r = int(idx % dil);
+    int64_t t = idx / dil;
+    const int g = int(t % ngr);
+    t /= ngr;
+    const int i0 = int(t % Win0);
     t /= Win0;
-    int e1 = int(t & 1);
-    int64_t k = t >> 1;
-    int y1 = (A.Sout[1][e1] + j1) & mask;
+    const int e1 = int(t & 1);
+    const int64_t k = t >> 1;
+    const int o = e1 ? 2 - L2 : 0;
     const double* line = A.phi_in + (k * Win0 + i0) * Win1;
-    double acc = 0.0;
-    for (int j = 0; j < P.L2; ++j)
-      acc = fma(P.td[e1][j], win_read(line, y1 - A.dil * (P.to[e1] + j), A.Sin[1], Win1, mask, 1), acc);
-    if (P.d == 2) {
-      A.Y[idx] = acc;
-    } else {  // d = 1: this is the output
-      Real* T = reinterpret_cast<Real*>(A.T);
-      if (e1 == 0) {
-        A.phi_out[k * Wout1 + j1] = acc;
-        if (level == coarse_level && A.toff[0] >= 0) T[A.toff[0] + k * A.tstride + j1] = Real(acc);
-      } else if (A.toff[1] >= 0) {
-        T[A.toff[1] + k * A.tstride + j1] = Real(acc);
+    const int ybase = A.Sout[1][e1] + r + dil * (QT * g - o - (L2 - 1));
+    double in[QT + L2 - 1];
+#pragma unroll
+    for (int i = 0; i < QT + L2 - 1; ++i) in[i] = win_read(line, (ybase + dil * i) & mask, A.Sin[1], Win1, mask, 1);
+#pragma unroll
+    for (int q = 0; q < QT; ++q) {
+      const int j1 = r + dil * (QT * g + q);
+      if (j1 >= Wout1) break;
+      double acc = 0.0;
+#pragma unroll
+      for (int tt = 0; tt < L2; ++tt) acc = fma(P.td[e1][tt], in[q + (L2 - 1) - tt], acc);
+      if (P.d == 2) {
+        A.Y[((k * 2 + e1) * Win0 + i0) * Wout1 + j1] = acc;
+      } else {  // d = 1: this is the output
+        Real* T = reinterpret_cast<Real*>(A.T);
+        if (e1 == 0) {
+          A.phi_out[k * Wout1 + j1] = acc;
+          if (level == coarse_level && A.toff[0] >= 0) T[A.toff[0] + k * A.tstride + j1] = Real(acc);
+        } else if (A.toff[1] >= 0) {
+          T[A.toff[1] + k * A.tstride + j1] = Real(acc);
+        }
       }
     }
   }
 }
 
-template <typename Real>
+template <typename Real, int L2>
 __global__ void tmpl_passB(const __grid_constant__ Plan P, const __grid_constant__ TmplArgs A, int coarse_level,
                            int level) {
-  // along axis 0, d = 2 only: out[k][e0 e1][j0][j1] = Σ_j f_{e0}[j] Y[k][e1](y0 - dil (o_{e0} + j), j1)
-  const int mask = P.n - 1;
+  // along axis 0, d = 2 only: out[k][e0 e1][j0][j1] = Σ_t f_{e0}[t] Y[k][e1](y0 - dil (o_{e0} + t), j1)
+  const int mask = P.n - 1, dil = A.dil;
   const int Win0 = A.Win[0], Wout0 = A.Wout[0], Wout1 = A.Wout[1];
+  const int ngr = (Wout0 + dil * QT - 1) / (dil * QT);
   const int64_t per = int64_t(Wout0) * Wout1;
-  const int64_t total = int64_t(P.m) * 4 * per;
+  const int64_t total = int64_t(P.m) * 4 * dil * ngr * Wout1;
   Real* T = reinterpret_cast<Real*>(A.T);
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
-    int64_t r = idx % per;
-    int64_t t = idx / per;
-    int ec = int(t & 3);
-    int64_t k = t >> 2;
-    int e0 = ec >> 1, e1 = ec & 1;
-    int j0 = int(r / Wout1), j1 = int(r - int64_t(j0) * Wout1);
-    int y0 = (A.Sout[0][e0] + j0) & mask;
+    const int j1 = int(idx % Wout1);
+    int64_t t = idx / Wout1;
+    const int r = int(t % dil);
+    t /= dil;
+    const int g = int(t % ngr);
+    t /= ngr;
+    const int ec = int(t & 3);
+    const int64_t k = t >> 2;
+    const int e0 = ec >> 1, e1 = ec & 1;
+    const int o = e0 ? 2 - L2 : 0;
     const double* col = A.Y + ((k * 2 + e1) * Win0) * Wout1 + j1;
-    double acc = 0.0;
-    for (int j = 0; j < P.L2; ++j)
-      acc = fma(P.td[e0][j], win_read(col, y0 - A.dil * (P.to[e0] + j), A.Sin[0], Win0, mask, Wout1), acc);
-    if (ec == 0) {
-      A.phi_out[k * per + r] = acc;
-      if (level == coarse_level && A.toff[0] >= 0) T[A.toff[0] + k * A.tstride + int64_t(j0) * A.trs + j1] = Real(acc);
-    } else if (A.toff[ec] >= 0) {
-      T[A.toff[ec] + k * A.tstride + int64_t(j0) * A.trs + j1] = Real(acc);
+    const int ybase = A.Sout[0][e0] + r + dil * (QT * g - o - (L2 - 1));
+    double in[QT + L2 - 1];
+#pragma unroll
+    for (int i = 0; i < QT + L2 - 1; ++i) in[i] = win_read(col, (ybase + dil * i) & mask, A.Sin[0], Win0, mask, Wout1);
+#pragma unroll
+    for (int q = 0; q < QT; ++q) {
+      const int j0 = r + dil * (QT * g + q);
+      if (j0 >= Wout0) break;
+      double acc = 0.0;
+#pragma unroll
+      for (int tt = 0; tt < L2; ++tt) acc = fma(P.td[e0][tt], in[q + (L2 - 1) - tt], acc);
+      const int64_t rr = int64_t(j0) * Wout1 + j1;
+      if (ec == 0) {
+        A.phi_out[k * per + rr] = acc;
+        if (level == coarse_level && A.toff[0] >= 0) T[A.toff[0] + k * A.tstride + int64_t(j0) * A.trs + j1] = Real(acc);
+      } else if (A.toff[ec] >= 0) {
+        T[A.toff[ec] + k * A.tstride + int64_t(j0) * A.trs + j1] = Real(acc);
+      }
     }
   }
 }
@@ -498,17 +529,36 @@ cudaError_t launch_phi0(const Plan& P, const double* u, double* phi0, int S0, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_tmpl_level(const Plan& P, const TmplArgs& A, int real_bytes, int level, cudaStream_t st) {
-  const int64_t totA = int64_t(P.m) * 2 * A.Win[0] * A.Wout[1];
-  const int64_t totB = int64_t(P.m) * 4 * A.Wout[0] * A.Wout[1];
-  if (real_bytes == 4) {
-    tmpl_passA<float><<<grid_for(totA), kBlock, 0, st>>>(P, A, P.J, level);
-    if (P.d == 2) tmpl_passB<float><<<grid_for(totB), kBlock, 0, st>>>(P, A, P.J, level);
-  } else {
-    tmpl_passA<double><<<grid_for(totA), kBlock, 0, st>>>(P, A, P.J, level);
-    if (P.d == 2) tmpl_passB<double><<<grid_for(totB), kBlock, 0, st>>>(P, A, P.J, level);
+template <typename Real, int L2>
+static void launch_tmpl_t(const Plan& P, const TmplArgs& A, int level, cudaStream_t st) {
+  const int64_t ngA = (A.Wout[1] + int64_t(A.dil) * QT - 1) / (int64_t(A.dil) * QT);
+  const int64_t ngB = (A.Wout[0] + int64_t(A.dil) * QT - 1) / (int64_t(A.dil) * QT);
+  const int64_t totA = int64_t(P.m) * 2 * A.Win[0] * A.dil * ngA;
+  const int64_t totB = int64_t(P.m) * 4 * A.dil * ngB * A.Wout[1];
+  tmpl_passA<Real, L2><<<grid_for(totA), kBlock, 0, st>>>(P, A, P.J, level);
+  if (P.d == 2) tmpl_passB<Real, L2><<<grid_for(totB), kBlock, 0, st>>>(P, A, P.J, level);
+}
+
+template <typename Real>
+static cudaError_t launch_tmpl_r(const Plan& P, const TmplArgs& A, int level, cudaStream_t st) {
+  switch (P.L2) {
+    case 2: launch_tmpl_t<Real, 2>(P, A, level, st); break;
+    case 4: launch_tmpl_t<Real, 4>(P, A, level, st); break;
+    case 6: launch_tmpl_t<Real, 6>(P, A, level, st); break;
+    case 8: launch_tmpl_t<Real, 8>(P, A, level, st); break;
+    case 10: launch_tmpl_t<Real, 10>(P, A, level, st); break;
+    case 12: launch_tmpl_t<Real, 12>(P, A, level, st); break;
+    case 14: launch_tmpl_t<Real, 14>(P, A, level, st); break;
+    case 16: launch_tmpl_t<Real, 16>(P, A, level, st); break;
+    case 18: launch_tmpl_t<Real, 18>(P, A, level, st); break;
+    case 20: launch_tmpl_t<Real, 20>(P, A, level, st); break;
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_tmpl_level(const Plan& P, const TmplArgs& A, int real_bytes, int level, cudaStream_t st) {
+  return real_bytes == 4 ? launch_tmpl_r<float>(P, A, level, st) : launch_tmpl_r<double>(P, A, level, st);
 }
 
 cudaError_t launch_pad_v(const void* v, void* vpad, int n, int P, int m, int real_bytes, cudaStream_t st) {
