@@ -725,7 +725,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     add_generic(u0, u1, scr);
     s = e;
   }
-  if (h->bscratch_bytes) CKB(dalloc(&h->bscratch, h->bscratch_bytes));
+  if (h->bscratch_bytes) CKB(dalloc(&h->bscratch, h->bscratch_bytes + 1024));   // + vector over-read slack
   // fine path: periodically padded v (K1) and the TMA descriptors of every fine launch
   bool any_fine = false;
   for (const Launch& L : h->launches) any_fine = any_fine || L.fine;

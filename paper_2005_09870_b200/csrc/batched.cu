@@ -21,6 +21,10 @@ constexpr int kB = 256;
 __device__ __forceinline__ float fmaB(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fmaB(double a, double b, double c) { return fma(a, b, c); }
 
+// Row stride of the per-unit window buffers (R, approximations) in the batched scratch: 16-byte multiples so
+// tile loads can use aligned vector copies.
+__host__ __device__ __forceinline__ int rstride(int len) { return (len + 3) & ~3; }
+
 inline int find_subband_host(const Plan& P, int64_t unit) {
   int s = P.nsb - 1;
   while (s > 0 && unit < P.sb[s].offset) --s;
@@ -77,6 +81,7 @@ __global__ void __launch_bounds__(kB) bk_ksum(const __grid_constant__ Plan P, co
   const int n = P.n, mask = n - 1;
   const bool f0 = S.tW[0] >= n, f1 = S.tW[1] >= n;
   const int tw1 = S.tRS;
+  const int rs = rstride(r1.len);
   for (int idx = blockIdx.x * kB + threadIdx.x; idx < total; idx += gridDim.x * kB) {
     const int i0 = idx / r1.len, i1 = idx - i0 * r1.len;
     const int y0 = (r0.lo + i0) & mask, y1 = (r1.lo + i1) & mask;
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(kB) bk_ksum(const __grid_constant__ Plan P, co
     Real acc = Real(0);
 #pragma unroll 5
     for (int k = 0; k < P.m; ++k) acc = fmaB(__ldg(v + k * P.N + vy), __ldg(T + k * S.tstride + ti), acc);
-    X0[idx] = acc;
+    X0[int64_t(i0) * rs + i1] = acc;
   }
 }
 
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(kB) bk_ksum_tiled(const __grid_constant__ Plan
   if (z0 + r < R0) {
 #pragma unroll
     for (int u = 0; u < G; ++u) {
-      Real* X0 = reinterpret_cast<Real*>(A.scratch) + (ug + u - A.u0) * A.stride + S.offX0 + int64_t(z0 + r) * R1;
+      Real* X0 = reinterpret_cast<Real*>(A.scratch) + (ug + u - A.u0) * A.stride + S.offX0 + int64_t(z0 + r) * rstride(R1);
 #pragma unroll
       for (int i = 0; i < GZ; ++i) {
         const int z = zc + res + SH * i;
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(kB) bk_passA(const __grid_constant__ Plan P, c
     const int i0 = idx / ng, g = idx - i0 * ng;
     const int jj = 4 * g, nout = min(4, a1.len - jj);
     Real out[4];
-    line4<Real>(P, X + int64_t(i0) * in1.len, 1, in1, a1.lo + jj, nout, out);
+    line4<Real>(P, X + int64_t(i0) * rstride(in1.len), 1, in1, a1.lo + jj, nout, out);
     Real* yd = Y + int64_t(i0) * a1.len + jj;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(kB) bk_passB(const __grid_constant__ Plan P, c
     line4<Real>(P, Y + j1, a1.len, in0, a0.lo + j0, nout, out);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (q < nout) Xn[int64_t(j0 + q) * a1.len + j1] = out[q];
+      if (q < nout) Xn[int64_t(j0 + q) * rstride(a1.len) + j1] = out[q];
   }
 }
 
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(kB) bk_approx(const __grid_constant__ Plan P, 
                                                 int s, int ntx) {
   constexpr int TO = sizeof(Real) == 4 ? 32 : 16;   // outputs per tile side (static smem < 48 KB)
   constexpr int TI = 2 * (TO - 1) + L2;              // inputs per tile side
-  constexpr int XS = ((TI + 2 + 3) / 4) * 4 + 2;     // even row stride, ≡ 2 mod 4 (conflict-free pair loads)
+  constexpr int XS = ((TI + 1 + 1) / 2) * 2 % 4 == 2 ? ((TI + 1 + 1) / 2) * 2 : ((TI + 1 + 1) / 2) * 2 + 2;   // even, ≡ 2 mod 4
   constexpr int NI = 2 * 3 + L2;                     // inputs of 4 consecutive outputs
   __shared__ __align__(16) Real Xs[TI][XS];
   __shared__ Real Ys[TI][TO + 1];
@@ -307,32 +312,45 @@ __global__ void __launch_bounds__(kB) bk_approx(const __grid_constant__ Plan P, 
     lc[i] = local_index(in1, g1 + i);
   }
   __syncthreads();
-  {
-    // asynchronous element copies (many in flight); elements outside the window are zero-filled
-    const bool fast = lr[0] >= 0 && lr[TI - 1] == lr[0] + TI - 1 && lc[0] >= 0 && lc[TI - 1] == lc[0] + TI - 1;
+  // tile rows/columns contiguous inside the window: 16-byte copies from the aligned-down column (the row
+  // stride of the scratch is a 16-byte multiple), the misalignment `sh` is applied when reading Xs; otherwise
+  // element copies with zero fill outside the window
+  const bool fast = lr[0] >= 0 && lr[TI - 1] == lr[0] + TI - 1 && lc[0] >= 0 && lc[TI - 1] == lc[0] + TI - 1;
+  const int rsx = rstride(in1.len);
+  int sh = 0;
+  if (fast) {
+    constexpr int VWE = 8 / int(sizeof(Real));   // 8-byte copies: the even smem row stride stays bank-friendly
+    const int ca = lc[0] & ~(VWE - 1);
+    sh = lc[0] - ca;
+    constexpr int NVEC = (TI + VWE - 1 + VWE - 1) / VWE;
+    for (int idx = threadIdx.x; idx < TI * NVEC; idx += kB) {
+      const int r = idx / NVEC, c = (idx - r * NVEC) * VWE;
+      const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&Xs[r][c]));
+      const Real* src = X + int64_t(lr[0] + r) * rsx + ca + c;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
+    }
+  } else {
     for (int idx = threadIdx.x; idx < TI * TI; idx += kB) {
       const int r = idx / TI, c = idx - r * TI;
-      int li0, li1;
-      if (fast) { li0 = lr[0] + r; li1 = lc[0] + c; }
-      else { li0 = lr[r]; li1 = lc[c]; }
+      const int li0 = lr[r], li1 = lc[c];
       const bool ok = li0 >= 0 && li1 >= 0;
       const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&Xs[r][c]));
-      const Real* src = X + (ok ? int64_t(li0) * in1.len + li1 : 0);
+      const Real* src = X + (ok ? int64_t(li0) * rsx + li1 : 0);
       const unsigned nbytes = ok ? unsigned(sizeof(Real)) : 0u;
       if constexpr (sizeof(Real) == 4)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(src), "r"(nbytes) : "memory");
       else
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(nbytes) : "memory");
     }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   // axis 1: Ys[r][c] = Σ_t h[t] Xs[r][2c + t]; task = (row, 4 consecutive outputs), row fastest
   for (int idx = threadIdx.x; idx < TI * (TO / 4); idx += kB) {
     const int cq = idx / TI, r = idx - cq * TI;
     Real x[NI];
 #pragma unroll
-    for (int i = 0; i < NI; ++i) x[i] = Xs[r][8 * cq + i];
+    for (int i = 0; i < NI; ++i) x[i] = Xs[r][sh + 8 * cq + i];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       Real acc = Real(0);
@@ -356,7 +374,7 @@ __global__ void __launch_bounds__(kB) bk_approx(const __grid_constant__ Plan P, 
       Real acc = Real(0);
 #pragma unroll
       for (int t = 0; t < L2; ++t) acc = fmaB(TapsOf<Real>::get(P, 0, t), y[2 * q + t], acc);
-      Xn[int64_t(j0 + j) * a1.len + k0 + c] = acc;
+      Xn[int64_t(j0 + j) * rstride(a1.len) + k0 + c] = acc;
     }
   }
 }
@@ -417,7 +435,7 @@ __global__ void __launch_bounds__(kB) bk_gather(const __grid_constant__ Plan P, 
     Real val = Real(0);
     if (L.e == 0) {
       const int li0 = local_index(a0, l0), li1 = local_index(a1, l1);
-      if (li0 >= 0 && li1 >= 0) val = Xn[int64_t(li0) * a1.len + li1];
+      if (li0 >= 0 && li1 >= 0) val = Xn[int64_t(li0) * rstride(a1.len) + li1];
     } else {
       const int e0 = L.e0, e1 = L.e1;
       for (int t0 = 0; t0 < L2; ++t0) {
@@ -426,7 +444,7 @@ __global__ void __launch_bounds__(kB) bk_gather(const __grid_constant__ Plan P, 
         Real row = Real(0);
         for (int t1 = 0; t1 < L2; ++t1) {
           const int c = local_index(in1, 2 * l1 + P.to[e1] + t1);
-          if (c >= 0) row = fmaB(TapsOf<Real>::get(P, e1, t1), X[int64_t(r) * in1.len + c], row);
+          if (c >= 0) row = fmaB(TapsOf<Real>::get(P, e1, t1), X[int64_t(r) * rstride(in1.len) + c], row);
         }
         val = fmaB(TapsOf<Real>::get(P, e0, t0), row, val);
       }

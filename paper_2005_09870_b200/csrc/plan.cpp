@@ -326,7 +326,8 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
     int64_t w0 = P.d == 2 ? std::min(S.tW[0], n) : 1;
     int64_t w1 = std::min(S.tW[1], n);
     int64_t nl0 = P.d == 2 ? n : 1, nl1 = n;
-    int64_t X0 = w0 * w1;
+    auto rs4 = [](int64_t x) { return (x + 3) & ~int64_t(3); };   // batched path: 16-byte row strides
+    int64_t X0 = w0 * rs4(w1);
     int64_t maxA = 0, maxY = 0, maxD = 0;
     double fma = double(P.m) * X0;
     S.any_full = (S.tW[1] >= n) || (P.d == 2 && S.tW[0] >= n);
@@ -335,7 +336,7 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
       int64_t o1 = step_out_maxlen(int(w1), int(nl1), L2);
       if (P.d == 2) {
         maxY = std::max(maxY, w0 * 2 * o1);
-        maxA = std::max(maxA, o0 * o1);
+        maxA = std::max(maxA, o0 * rs4(o1));
         maxD = std::max(maxD, 3 * o0 * o1);
         fma += double(L2) * (w0 * 2.0 * o1 + 4.0 * o0 * o1);
       } else {
