@@ -126,10 +126,14 @@ PCWD_HD Range unit_window(const Plan& P, const SubBand& s, int a, int p) {
   return Range{((p << s.level) + s.tS[a]) & (P.n - 1), s.tW[a], P.n};
 }
 
-PCWD_HD int find_subband(const Plan& P, int64_t unit) {
-  int s = P.nsb - 1;
-  while (s > 0 && unit < P.sb[s].offset) --s;
-  return s;
+PCWD_HD int find_subband(const Plan& P, int64_t unit) {   // largest s with sb[s].offset <= unit
+  int lo = 0, hi = P.nsb - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.sb[mid].offset <= unit) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
 }
 
 }  // namespace pcwd
