@@ -525,11 +525,18 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         const int64_t regR = SLK + fc.GU * RSZ + SLK;
         const int al = 128 / rb;   // TMA destinations: 128-byte aligned boxes
         const int TSZ = (R0 * TS + al - 1) / al * al, VSZ = (R0 * VS + al - 1) / al * al;
-        const int64_t stg = int64_t(fc.NST) * (TSZ + VSZ) + al;
-        ok = ok && stg <= fc.GU * RSZ;          // the k-sum staging aliases the R region
+        // staging ring depth: the ring may use the whole dynamic smem (R, Yt and D regions are all idle
+        // during the k-sum); as many buffers as fit, up to the kernel's NST
         const int64_t regS = SLK + fc.CG * YSZ + SLK;
         const int64_t regD = regR + regS;
-        const size_t smem = size_t(regD + fc.CG * DS) * rb;
+        int64_t total_el = regD + fc.CG * DS;
+        int nst = int(std::min<int64_t>(fc.NST, (total_el - SLK - al) / (TSZ + VSZ)));
+        if (nst < 1) {   // enlarge the allocation to hold one staging buffer
+          total_el = SLK + al + (TSZ + VSZ);
+          nst = 1;
+        }
+        const int64_t stg = int64_t(nst) * (TSZ + VSZ) + al;
+        const size_t smem = size_t(std::max<int64_t>(total_el, regD + fc.CG * DS)) * rb;
         ok = ok && smem + 4096 <= size_t(smem_optin > 0 ? smem_optin : 48 * 1024);
         int64_t a0 = (u0 + fc.GU - 1) / fc.GU * fc.GU, a1 = u1 / fc.GU * fc.GU;
         if (getenv("PCWD_DEBUG_PLAN"))
@@ -547,6 +554,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           A.u0 = a0; A.u1 = a1;
           A.regS = regR; A.regD = regD;
           A.TSZ = TSZ; A.VSZ = VSZ;
+          A.nst = nst;
+          (void)stg;
           A.sb_first = s;
           // halo of the padded v that every round's boxes stay inside
           int tmin0 = 1 << 30, tmax0 = -(1 << 30), tmin1 = 1 << 30, tmax1 = -(1 << 30);

@@ -258,11 +258,11 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
 #pragma unroll
           for (int i = 0; i < GZ; ++i) acc[a][j][i] = Real(0);
       stage(0, 0);
-#pragma unroll
-      for (int q = 1; q < NST; ++q)
+      const int nst = A.nst;           // staging buffers in use (≤ NST, as many as fit in the R region)
+      for (int q = 1; q < nst; ++q)
         if (q < P.m) stage(q, q);
+      int b = 0;
       for (int k = 0; k < P.m; ++k) {
-        const int b = k % NST;
         mbar_wait(&fullbar[b], (phase >> b) & 1u);
         phase ^= 1u << b;
         const Real* Ts = Sbase + b * (A.TSZ + A.VSZ);
@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
           }
         }
         __syncthreads();
-        if (k + NST < P.m) stage(k + NST, b);
+        if (k + nst < P.m) stage(k + nst, b);
+        b = (b + 1 == nst) ? 0 : b + 1;
       }
       // R_j[r][z] (row stride RS), z < R1
 #pragma unroll

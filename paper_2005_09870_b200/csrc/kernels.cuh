@@ -69,6 +69,7 @@ struct FineArgs {
   int TS, VS;               // staged T row stride, staged v row stride
   int YS, YSZ;              // Yt row stride, per-unit Yt size
   int DS;                   // per-unit D size
+  int nst;                  // staging buffers used (1 ≤ nst ≤ the kernel's NST)
   unsigned long long* dbg;  // optional phase clock counters (PCWD_DEBUG_PHASES): k-sum, cascade
 };
 

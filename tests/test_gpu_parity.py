@@ -219,3 +219,92 @@ def test_apply_matches_csr(dtype):
     assert np.max(np.abs(y - dense @ x)) <= tol * np.max(np.abs(dense @ x))
     yt = g["dec"].apply(torch.tensor(x, dtype=tdt, device="cuda"), transpose=True).cpu().numpy()
     assert np.max(np.abs(yt - dense.T @ x)) <= tol * np.max(np.abs(dense.T @ x))
+
+
+# ----------------------------------------------------------------------------- kernel-path coverage
+
+def _kinds(p, dtype):
+    u = torch.from_numpy(np.ascontiguousarray(p.u)).cuda()
+    v = torch.from_numpy(np.ascontiguousarray(p.v)).cuda()
+    dec = Decomposition(Spec(p.d, p.n, p.J, p.h, u, v, dtype=dtype, retain=p.retain, tau_rel=p.tau_rel,
+                             band_L=p.band_L))
+    dec.profile(True)
+    dec.decompose()
+    torch.cuda.synchronize()
+    lp = dec.launch_profile()
+    dec.close()
+    return {(k, lv) for (_, _, k, lv) in lp}
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_band_configs_run_on_fine_and_batched_kernels(name):
+    """The parity-tested c3/c5 results come from the fine kernel (levels 1-3, TMA + register-blocked
+    k-sum) and the batched coarse kernels (levels ≥ 4) — no fallback path is silently taken."""
+    p = C.get(name)
+    kinds = _kinds(p, "f32")
+    assert {("fine", 1), ("fine", 2), ("fine", 3)} <= kinds
+    assert all(k == "batched" for (k, lv) in kinds if lv >= 4)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_fine_kernel_parity_128(dtype):
+    """A 128² band problem whose levels 1-2 run on the fine kernel in both precisions (windows never cover
+    a line there); parity on sampled units against the oracle rows."""
+    p = C.micro(128, 2, 4, 5, 3, 4, 45, retain="band", band_L=64)
+    kinds = _kinds(p, dtype)
+    assert ("fine", 1) in kinds and ("fine", 2) in kinds
+    g = run(p, dtype)
+    units = _sample_units(p, 24, 4, 2, seed=3)
+    compare(p, g, units, R.rows(p, units), dtype)
+
+
+def test_c3_shard_concatenation_bit_identical():
+    """Cost-balanced shards (aligned to 16 units) concatenate to the single-handle CSR bit for bit."""
+    p = C.get("c3")
+    full = run(p, "f32")
+    cols, vals, nxt = [], [], 0
+    for r in range(4):
+        g = run(p, "f32", world=4, rank=r)
+        assert g["row0"] == nxt and (g["row0"] % 16 == 0)
+        nxt = g["row1"]
+        cols.append(g["col"])
+        vals.append(g["val"])
+    assert nxt == p.N
+    assert np.array_equal(np.concatenate(cols), full["col"])
+    assert np.array_equal(np.concatenate(vals), full["val"])
+
+
+# ----------------------------------------------------------------------------- degenerate cases
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_band_L1_single_partner(dtype):
+    """L = 1: each unit keeps one partner, the first of the key order (Δ = ρ = 0; at level J the coarse
+    scaling block ranks before the unit's own detail sub-band, R16)."""
+    p = C.micro(16, 2, 4, 3, 2, 2, 41, retain="band", band_L=1)
+    T = op.theta_dense(p)
+    g = run(p, dtype)
+    assert np.array_equal(g["rp"], np.arange(p.N + 1))
+    compare(p, g, list(range(p.N)), T, dtype)     # the single partner is the oracle's first-ranked one
+
+
+def test_band_L_equals_N_is_full():
+    p = C.micro(8, 2, 2, 2, 2, 1, 42, retain="band", band_L=64)
+    T = op.theta_dense(p)
+    g = run(p, "f64")
+    assert np.array_equal(g["col"], np.tile(np.arange(64), 64))
+    assert np.max(np.abs(g["val"].reshape(64, 64) - T)) < 1e-13
+
+
+def test_zero_multiplier_gives_exact_zeros():
+    p = C.micro(16, 2, 4, 3, 2, 2, 43, retain="band", band_L=20)
+    p.v = np.zeros_like(p.v)
+    g = run(p, "f32")
+    assert g["nnz"] == p.N * 20 and np.all(g["val"] == 0.0)
+
+
+def test_smallest_torus_haar():
+    """n = 2, J = 1 (one analysis step, Haar): the 4×4 Θ matches the dense definition."""
+    p = C.micro(2, 2, 1, 1, 1, 0, 44)
+    T = op.theta_dense(p)
+    g = run(p, "f64")
+    assert np.max(np.abs(g["val"].reshape(4, 4) - T)) < 1e-14

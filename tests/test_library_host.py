@@ -124,3 +124,17 @@ def test_shard_partition(world):
     assert ranges[0][0] == 0 and ranges[-1][1] == p.N
     for a, b in zip(ranges, ranges[1:]):
         assert a[1] == b[0] and a[0] <= a[1]
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_c5_shard_plan_aligned_and_time_balanced(world):
+    """Shards of c5 cover Λ, are contiguous, start on multiples of 16 units (whole fine-kernel rounds)
+    and put the costly coarse units on the first ranks."""
+    p = C.get("c5")
+    rs = [P.plan_shard(P.Spec(2, p.n, p.J, p.h, p.u, p.v, retain="band", band_L=128, rank=r, world=world))
+          for r in range(world)]
+    assert rs[0][0] == 0 and rs[-1][1] == p.N
+    for a, b in zip(rs, rs[1:]):
+        assert a[1] == b[0] and b[0] % 16 == 0
+    sizes = [b - a for a, b in rs]
+    assert sizes[0] < sizes[-1]          # rank 0 holds the coarse (expensive) units
