@@ -228,17 +228,20 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
       static const bool dbg_on = getenv("PCWD_DEBUG_PHASES") != nullptr;
       unsigned long long* dbg = nullptr;
       if (dbg_on) {
-        CK(cudaMalloc(&dbg, 2 * sizeof(unsigned long long)));
-        CK(cudaMemset(dbg, 0, 2 * sizeof(unsigned long long)));
+        CK(cudaMalloc(&dbg, 8 * sizeof(unsigned long long)));
+        CK(cudaMemset(dbg, 0, 8 * sizeof(unsigned long long)));
       }
       F.dbg = dbg;
+      F.dbg_flags = getenv("PCWD_FINE_DBG") ? atoi(getenv("PCWD_FINE_DBG")) : 0;
       CK(launch_fine(P, F, h->hp.real_bytes, L.level, L.grid, L.smem, st));
       h->nlaunch++;
       if (dbg_on) {
-        unsigned long long c[2];
+        unsigned long long c[8];
         CK(cudaMemcpy(c, dbg, sizeof(c), cudaMemcpyDeviceToHost));
-        fprintf(stderr, "[pcwd fine] level %d grid %d: ksum %.1f%% cascade+gather %.1f%%\n", L.level, L.grid,
-                100.0 * c[0] / double(c[0] + c[1]), 100.0 * c[1] / double(c[0] + c[1]));
+        const double tot = double(c[0] + c[1] + c[2] + c[3] + c[4]);
+        fprintf(stderr, "[pcwd fine] level %d grid %d: ksum %.1f%% desc %.1f%% step1 %.1f%% steps2+ %.1f%% gather %.1f%%\n",
+                L.level, L.grid, 100.0 * c[0] / tot, 100.0 * c[1] / tot, 100.0 * c[2] / tot, 100.0 * c[3] / tot,
+                100.0 * c[4] / tot);
         cudaFree(dbg);
       }
       continue;
@@ -494,15 +497,21 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         ok = ok && int64_t(R0) * SH * NZB <= int64_t(fc.NT) * 256;
         // strides: multiples of VW with an odd vector count (8 consecutive rows -> distinct bank groups)
         auto odd_stride = [&](int w) { int x = (w + VW - 1) / VW * VW; if ((x / VW) % 2 == 0) x += VW; return x; };
-        int arl = 0, ycols = 0, dsz = 0;
+        int arl = 0, ycols = 0, dsz = 0, arl2 = 0, ycols2 = 0;
         for (int q = s; q < e && ok; ++q) {
           const SubBand& Sq = P.sb[q];
+          ok = ok && Sq.steps <= lev + 2;     // sdesc capacity of the kernel
           for (int c = 0; c < Sq.fg_m * Sq.fg_m; ++c) {
             const FGeom& g = h->hp.fgeom[Sq.fg_off + c];
             dsz = std::max(dsz, g.dsize);
             for (int st = 0; st < g.steps; ++st) {
-              arl = std::max(arl, g.st[st].arl);
-              ycols = std::max(ycols, g.st[st].hlen + g.st[st].glen);
+              if (st == 0) {
+                arl = std::max(arl, g.st[st].arl);
+                ycols = std::max(ycols, g.st[st].hlen + g.st[st].glen);
+              } else {
+                arl2 = std::max(arl2, g.st[st].arl);
+                ycols2 = std::max(ycols2, g.st[st].hlen + g.st[st].glen);
+              }
               // the approximations of steps ≥ 1 are stored in the unit's R region (row stride RS)
               if (st > 0) ok = ok && g.st[st].xcl + VW - 1 <= ((R1 + VW - 1) / VW * VW) && g.st[st].xrl <= R0;
             }
@@ -518,7 +527,9 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         const int VS = odd_stride(VW - 1 + std::max(R1 + SH * (fc.GU - 1), zmaxV + 1));
         const int YS = pair_stride(arl + VW - 1);
         const int64_t lpad = P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb;
-        const int64_t YSZ = (std::max<int64_t>(int64_t(ycols) * YS, lpad) + VW - 1) / VW * VW;
+        const int64_t YSZ = (int64_t(ycols) * YS + VW - 1) / VW * VW;
+        const int YS2 = pair_stride(arl2 + VW - 1);
+        const int64_t YSZ2 = (std::max<int64_t>(int64_t(ycols2) * YS2, lpad) + VW - 1) / VW * VW;
         const int64_t RSZ = int64_t(R0) * RS;
         const int64_t DS = (dsz + VW - 1) / VW * VW;
         const int SLK = 32;
@@ -527,22 +538,22 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         const int TSZ = (R0 * TS + al - 1) / al * al, VSZ = (R0 * VS + al - 1) / al * al;
         // staging ring depth: the ring may use the whole dynamic smem (R, Yt and D regions are all idle
         // during the k-sum); as many buffers as fit, up to the kernel's NST
-        const int64_t regS = SLK + fc.CG * YSZ + SLK;
+        const int64_t regS = SLK + std::max<int64_t>(fc.CG * YSZ, fc.GU * YSZ2) + SLK;
         const int64_t regD = regR + regS;
-        int64_t total_el = regD + fc.CG * DS;
+        int64_t total_el = regD + fc.GU * DS;
         int nst = int(std::min<int64_t>(fc.NST, (total_el - SLK - al) / (TSZ + VSZ)));
         if (nst < 1) {   // enlarge the allocation to hold one staging buffer
           total_el = SLK + al + (TSZ + VSZ);
           nst = 1;
         }
         const int64_t stg = int64_t(nst) * (TSZ + VSZ) + al;
-        const size_t smem = size_t(std::max<int64_t>(total_el, regD + fc.CG * DS)) * rb;
+        const size_t smem = size_t(std::max<int64_t>(total_el, regD + fc.GU * DS)) * rb;
         ok = ok && smem + 4096 <= size_t(smem_optin > 0 ? smem_optin : 48 * 1024);
         int64_t a0 = (u0 + fc.GU - 1) / fc.GU * fc.GU, a1 = u1 / fc.GU * fc.GU;
         if (getenv("PCWD_DEBUG_PLAN"))
           fprintf(stderr, "[pcwd fine] level %d ok %d GU %d R %dx%d RS %d TS %d VS %d YS %d ycols %d arl %d dsz %d "
                   "regR %lld stg %lld yt %lld smem %zu\n", lev, int(ok), fc.GU, R0, R1, RS, TS, VS, YS, ycols, arl, dsz,
-                  (long long)regR, (long long)stg, (long long)(fc.CG * YSZ), smem);
+                  (long long)regR, (long long)stg, (long long)std::max<int64_t>(fc.CG * YSZ, fc.GU * YSZ2), smem);
         if (ok && a1 > a0) {
           Launch F{a0, a1, 0, 0};
           F.fine = 1;
@@ -570,6 +581,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           h->vpad = std::max(h->vpad, (need + 3) / 4 * 4);
           F.box[0] = R0; F.box[1] = TS; F.box[2] = VS;
           A.RS = RS; A.RSZ = int(RSZ); A.TS = TS; A.VS = VS; A.YS = YS; A.YSZ = int(YSZ); A.DS = int(DS);
+          A.YS2 = YS2; A.YSZ2 = int(YSZ2);
           add_generic(u0, a0, scr);
           h->launches.push_back(F);
           add_generic(a1, u1, scr);

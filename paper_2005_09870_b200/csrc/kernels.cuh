@@ -67,10 +67,12 @@ struct FineArgs {
   int64_t regS, regD;       // region offsets (elements): staging / Yt, D
   int RS, RSZ;              // R / approximation row stride, per-unit R region size
   int TS, VS;               // staged T row stride, staged v row stride
-  int YS, YSZ;              // Yt row stride, per-unit Yt size
+  int YS, YSZ;              // Yt row stride, per-slot Yt size (step 1, CG slots)
+  int YS2, YSZ2;            // Yt row stride and per-unit size for steps ≥ 2 and the gather stage (GU units)
   int DS;                   // per-unit D size
   int nst;                  // staging buffers used (1 ≤ nst ≤ the kernel's NST)
   unsigned long long* dbg;  // optional phase clock counters (PCWD_DEBUG_PHASES): k-sum, cascade
+  int dbg_flags;            // debug experiments (PCWD_FINE_DBG, results invalid): 2 = no cascade, 4 = step 1 only
 };
 
 // Template configuration of the fine kernel for (real_bytes, level): units per round GU, template
