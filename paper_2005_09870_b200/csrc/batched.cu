@@ -330,17 +330,55 @@ __global__ void __launch_bounds__(kB) bk_approx(const __grid_constant__ Plan P, 
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
     }
   } else {
-    for (int idx = threadIdx.x; idx < TI * TI; idx += kB) {
-      const int r = idx / TI, c = idx - r * TI;
-      const int li0 = lr[r], li1 = lc[c];
-      const bool ok = li0 >= 0 && li1 >= 0;
-      const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&Xs[r][c]));
-      const Real* src = X + (ok ? int64_t(li0) * rsx + li1 : 0);
-      const unsigned nbytes = ok ? unsigned(sizeof(Real)) : 0u;
-      if constexpr (sizeof(Real) == 4)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(src), "r"(nbytes) : "memory");
-      else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(nbytes) : "memory");
+    // edge tiles: the valid columns form one run [cf, cl] when the window does not wrap inside the tile (the
+    // usual case); zero the tile, then copy each valid row's run with one warp (no per-element index math)
+    __shared__ int crun[3];
+    if (threadIdx.x < 32) {
+      int first = TI, last = -1;
+      for (int c = threadIdx.x; c < TI; c += 32)
+        if (lc[c] >= 0) { first = min(first, c); last = max(last, c); }
+      for (int o = 16; o > 0; o >>= 1) {
+        first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+        last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+      }
+      if (threadIdx.x == 0) {
+        crun[0] = first;
+        crun[1] = last;
+        crun[2] = last >= first && lc[last] - lc[first] == last - first;
+      }
+    }
+    for (int i = threadIdx.x; i < TI * XS; i += kB) (&Xs[0][0])[i] = Real(0);
+    __syncthreads();
+    const int cf = crun[0], cl = crun[1];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (crun[2]) {
+      for (int r = w; r < TI; r += kB / 32) {
+        const int li0 = lr[r];
+        if (li0 < 0) continue;
+        const Real* xrow = X + int64_t(li0) * rsx + lc[cf] - cf;
+        for (int c = cf + lane; c <= cl; c += 32) {
+          const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&Xs[r][c]));
+          if constexpr (sizeof(Real) == 4)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(xrow + c) : "memory");
+          else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(xrow + c) : "memory");
+        }
+      }
+    } else {
+      for (int r = w; r < TI; r += kB / 32) {
+        const int li0 = lr[r];
+        if (li0 < 0) continue;
+        const Real* xrow = X + int64_t(li0) * rsx;
+        for (int c = lane; c < TI; c += 32) {
+          const int li1 = lc[c];
+          if (li1 < 0) continue;
+          const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&Xs[r][c]));
+          if constexpr (sizeof(Real) == 4)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(xrow + li1) : "memory");
+          else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(xrow + li1) : "memory");
+        }
+      }
     }
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
