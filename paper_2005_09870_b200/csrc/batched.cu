@@ -190,6 +190,87 @@ __global__ void __launch_bounds__(kB) bk_ksum_tiled(const __grid_constant__ Plan
   }
 }
 
+// Tiled k-sum for windows covering the whole torus on both axes (coarsest levels): the window is the torus,
+// R(y) = Σ_k v_k(y) T_k((y - 2^ℓ p) mod n); G units adjacent along axis 1 read the same v tile and
+// template columns shifted by 2^ℓ u.  A thread owns tile row r and the NL columns res + 2^ℓ i of one residue
+// (a tile row spans the torus: 2^ℓ · NL = n); the template strip it reads is periodic.
+template <typename Real, int LEV, int NL>
+__global__ void __launch_bounds__(kB) bk_ksum_full(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A) {
+  constexpr int SH = 1 << LEV;
+  constexpr int TR = kB / SH > 0 ? kB / SH : 1;   // tile rows
+  constexpr int G = NL;                            // units per group (a whole sub-band row)
+  constexpr int TW = SH * NL;                      // = n
+  constexpr int TSW = SH * (NL + G - 1);           // template strip width
+  __shared__ Real Vt[2][TR][TW];
+  __shared__ Real Tt[2][TR][TSW];
+  const int tid = threadIdx.x;
+  const int n = P.n, mask = n - 1;
+  const int64_t ug = A.u0 + int64_t(blockIdx.y) * G;
+  const UnitPos up = unit_pos(P, ug);
+  const SubBand& S = P.sb[up.sbi];
+  const int z0 = blockIdx.x * TR;                  // tile rows y0 = z0 .. z0 + TR - 1
+  const int sy = up.p0 << LEV;                      // template row shift
+  const int sx0 = (up.p1 << LEV) + SH * (G - 1);    // strip column 0 = template column (-sx0) mod n
+  const Real* __restrict__ v = reinterpret_cast<const Real*>(A.v);
+  const Real* __restrict__ T = reinterpret_cast<const Real*>(A.T) + S.toff;
+  auto stage = [&](int k, int b) {
+    const Real* vk = v + int64_t(k) * P.N;
+    const Real* Tk = T + int64_t(k) * S.tstride;
+    for (int i = tid; i < TR * TW; i += kB) {
+      const int r = i / TW, c = i - r * TW;
+      cp_async_el(&Vt[b][r][c], vk + int64_t(z0 + r) * n + c);
+    }
+    for (int i = tid; i < TR * TSW; i += kB) {
+      const int r = i / TSW, c = i - r * TSW;
+      cp_async_el(&Tt[b][r][c], Tk + int64_t((z0 + r - sy) & mask) * S.tRS + ((c - sx0) & mask));
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int r = tid / SH, res = tid - r * SH;
+  const bool active = tid < TR * SH;
+  Real acc[G][NL];
+#pragma unroll
+  for (int u = 0; u < G; ++u)
+#pragma unroll
+    for (int i = 0; i < NL; ++i) acc[u][i] = Real(0);
+  stage(0, 0);
+  for (int k = 0; k < P.m; ++k) {
+    if (k + 1 < P.m) {
+      stage(k + 1, (k + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const int b = k & 1;
+    if (active) {
+      Real vv[NL];
+#pragma unroll
+      for (int i = 0; i < NL; ++i) vv[i] = Vt[b][r][res + SH * i];
+      // unit u, column res + SH i: template column res + SH (i - u) - 2^ℓ p1  ->  strip index res + SH (i - u + G - 1)
+#pragma unroll
+      for (int mm = 0; mm < NL + G - 1; ++mm) {
+        const Real tm = Tt[b][r][res + SH * mm];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const int i = mm + u - (G - 1);
+          if (i >= 0 && i < NL) acc[u][i] = fmaB(vv[i], tm, acc[u][i]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (active) {
+    const int rs = rstride(n);
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      Real* X0 = reinterpret_cast<Real*>(A.scratch) + (ug + u - A.u0) * A.stride + S.offX0 + int64_t(z0 + r) * rs;
+#pragma unroll
+      for (int i = 0; i < NL; ++i) X0[res + SH * i] = acc[u][i];
+    }
+  }
+}
+
 // Only the approximation chain is carried through the whole window (the stencil's coarse
 // partners need all of it); the stencil's detail coefficients are computed directly in
 // bk_gather from the step's input window (2δ × 2δ taps each).
@@ -559,6 +640,30 @@ static bool launch_ksum_tiled(const Plan& P, const BatchArgs& A, int nb, cudaStr
   return true;
 }
 
+// Full-torus windows: bk_ksum_full when 2^ℓ ≤ 256, a row of the sub-band is one group (nl ∈ {2, 4, 8}).
+template <typename Real>
+static bool launch_ksum_full(const Plan& P, const BatchArgs& A, int nb, cudaStream_t st) {
+  if (getenv("PCWD_NO_TILED_KSUM")) return false;
+  const int s0 = find_subband_host(P, A.u0), s1 = find_subband_host(P, A.u1 - 1);
+  const SubBand& S = P.sb[s0];
+  const int lev = S.level, nl = S.nl;
+  if (P.d != 2 || (1 << lev) > kB || (nl != 2 && nl != 4 && nl != 8) || (nl << lev) != P.n) return false;
+  if (sizeof(Real) == 8 && nl == 8) return false;   // static smem
+  for (int q = s0; q <= s1; ++q)
+    if (P.sb[q].level != lev || P.sb[q].tW[0] < P.n || P.sb[q].tW[1] < P.n) return false;
+  if (nb % nl || (A.u0 - S.offset) % nl) return false;
+  const int TR = std::max(1, kB >> lev);
+  const dim3 grid((P.n + TR - 1) / TR, nb / nl);
+#define PCWD_KF(L, NLV)                                                                      \
+  if constexpr (!(sizeof(Real) == 8 && NLV == 8)) {                                          \
+    if (lev == L && nl == NLV) { bk_ksum_full<Real, L, NLV><<<grid, kB, 0, st>>>(P, A); return true; } \
+  }
+  PCWD_KF(8, 4) PCWD_KF(8, 2) PCWD_KF(7, 4) PCWD_KF(7, 2) PCWD_KF(6, 4) PCWD_KF(6, 2) PCWD_KF(5, 4) PCWD_KF(5, 2)
+  PCWD_KF(7, 8) PCWD_KF(6, 8) PCWD_KF(5, 8) PCWD_KF(4, 8) PCWD_KF(4, 4) PCWD_KF(4, 2)
+#undef PCWD_KF
+  return false;
+}
+
 template <typename Real>
 static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0, const int64_t* workA,
                                const int64_t* workB, const int64_t* appr0, const int64_t* appr1, int steps,
@@ -570,7 +675,8 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
     const int nb = int(std::min<int64_t>(A0.batch, units - b0));
     A.u1 = A.u0 + nb;
     auto gx = [](int64_t elems) { return int(std::max<int64_t>(1, std::min<int64_t>((elems + kB - 1) / kB, 64))); };
-    if (!launch_ksum_tiled<Real>(P, A, nb, st)) bk_ksum<Real><<<dim3(gx(maxX0), nb), kB, 0, st>>>(P, A);
+    if (!launch_ksum_tiled<Real>(P, A, nb, st) && !launch_ksum_full<Real>(P, A, nb, st))
+      bk_ksum<Real><<<dim3(gx(maxX0), nb), kB, 0, st>>>(P, A);
     ++*launches;
     static const bool old_passes = getenv("PCWD_OLD_PASSES") != nullptr;
     for (int s = 1; s <= steps; ++s) {
