@@ -179,108 +179,6 @@ __device__ __forceinline__ void filt8hg(const Plan& P, const Real* __restrict__ 
   }
 }
 
-// Pass A task t of one unit-step (descriptor d, fields as in FStep): 8 output columns of one input row,
-// both filters where the block meets the h and the g ranges; outputs to Yt[col][row - yb].
-template <typename Real, int L2, bool MASK>
-__device__ __forceinline__ void passA_task(const Plan& P, const int* d, const Real* X, int RS, int xb, int xr0,
-                                           Real* Yt, int YS, int t) {
-  constexpr int VW = FVec<Real>::W;
-  const int ar = d[4], rows = d[5];
-  const int hlo = d[6], hlen = d[7], glo = d[8], glen = d[9];
-  const int gend = glo + glen, hend = hlo + hlen;
-  const int ulo = glen ? (hlen ? min(hlo, glo) : glo) : hlo;
-  const int yb = ar & ~(VW - 1);
-  const int vlo = d[2] - xb, vhi = vlo + d[3];
-  const int q = __float2int_rz((float(t) + 0.5f) * __frcp_rn(float(rows)));   // t / rows
-  const int rr = t - q * rows;
-  const int j0 = ulo + 8 * q;
-  const bool doh = j0 < hend && j0 + 8 > hlo, dog = j0 < gend && j0 + 8 > glo;
-  const int r = ar + rr;
-  const Real* xrow = X + (r - xr0) * RS;
-  Real oh[8], og[8];
-  filt8hg<Real, L2, MASK>(P, xrow, xb, j0, doh, dog, 8, 8, vlo, vhi, oh, og);
-  Real* yh = Yt + (j0 - hlo) * YS + (r - yb);
-  Real* yg = Yt + (hlen + j0 - glo) * YS + (r - yb);
-  if (doh) {
-    if (j0 >= hlo && j0 + 8 <= hend) {   // whole block inside the h range: plain stores
-#pragma unroll
-      for (int i = 0; i < 8; ++i) yh[i * YS] = oh[i];
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (j0 + i >= hlo && j0 + i < hend) yh[i * YS] = oh[i];
-    }
-  }
-  if (dog) {
-    if (j0 >= glo && j0 + 8 <= gend) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) yg[i * YS] = og[i];
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (j0 + i >= glo && j0 + i < gend) yg[i * YS] = og[i];
-    }
-  }
-}
-
-__device__ __forceinline__ int passA_count(const int* d) {
-  const int hlo = d[6], hlen = d[7], glo = d[8], glen = d[9];
-  if (!(hlen + glen)) return 0;
-  const int ulo = glen ? (hlen ? min(hlo, glo) : glo) : hlo;
-  const int uhi = glen ? (hlen ? max(hlo + hlen, glo + glen) : glo + glen) : hlo + hlen;
-  return ((uhi - ulo + 7) >> 3) * d[5];
-}
-
-// pass B task counts per orientation box (prefix sums n0 ≤ n1 ≤ n2 ≤ n3 = total)
-__device__ __forceinline__ void passB_counts(const int* d, bool want0, int& n0, int& n1, int& n2, int& n3) {
-  n0 = want0 ? ((d[14] + 7) >> 3) * d[22] : 0;
-  n1 = n0 + ((d[15] + 7) >> 3) * d[23];
-  n2 = n1 + ((d[16] + 7) >> 3) * d[24];
-  n3 = n2 + ((d[17] + 7) >> 3) * d[25];
-}
-
-// Pass B task t: 8 outputs (rows) of one column of one box; the approximation box goes to the next step's
-// input X (when `tox`), detail boxes (and the coarse block at the last step) to D.
-template <typename Real, int L2>
-__device__ __forceinline__ void passB_task(const Plan& P, const int* d, Real* X, int RS, int nxb, int nxr, bool tox,
-                                           const Real* Yt, int YS, Real* Dd, int n0, int n1, int n2, int t) {
-  constexpr int VW = FVec<Real>::W;
-  const int ar = d[4], arl = d[5];
-  const int yb = ar & ~(VW - 1);
-  const int vlo = ar - yb, vhi = vlo + arl;
-  const int hlo = d[6], hlen = d[7], glo = d[8];
-  const int ec = (t >= n0) + (t >= n1) + (t >= n2);
-  const int idx = t - (ec == 0 ? 0 : ec == 1 ? n0 : ec == 2 ? n1 : n2);
-  const int bl0 = d[14 + ec], bl1 = d[22 + ec];
-  const int q = __float2int_rz((float(idx) + 0.5f) * __frcp_rn(float(bl1)));   // idx / bl1
-  const int cc = idx - q * bl1;
-  const int l0 = d[10 + ec] + 8 * q;
-  const int nrow = min(8, bl0 - 8 * q);
-  const int j = d[18 + ec] + cc;
-  const int e0 = ec >> 1, e1 = ec & 1;
-  const int ycol = e1 ? hlen + (j - glo) : (j - hlo);
-  Real out[8];
-  if (e0) filt8<Real, L2, 1, true>(P, Yt + ycol * YS, yb, l0, nrow, vlo, vhi, out);
-  else filt8<Real, L2, 0, true>(P, Yt + ycol * YS, yb, l0, nrow, vlo, vhi, out);
-  Real* dst;
-  int dstr;
-  if (ec == 0 && tox) {
-    dst = X + (l0 - nxr) * RS + (j - nxb);
-    dstr = RS;
-  } else {
-    dst = Dd + d[26 + ec] + (8 * q) * bl1 + cc;
-    dstr = bl1;
-  }
-  if (nrow == 8) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) dst[i * dstr] = out[i];
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i < nrow) dst[i * dstr] = out[i];
-  }
-}
-
 }  // namespace
 
 // Shared-memory layout (elements of Real), all offsets from the dynamic smem base:
@@ -290,9 +188,8 @@ __device__ __forceinline__ void passB_task(const Plan& P, const int* d, Real* X,
 template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG>
 __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Plan P, const __grid_constant__ FineArgs A) {
   extern __shared__ __align__(16) unsigned char fsm[];
-  __shared__ int wflag[GU];
-  __shared__ int pcnt[5][GU];             // pooled steps: pass A count, pass B prefix counts n0 n1 n2 n3 per unit
-  __shared__ int sdesc[GU][LEV + 2][32];   // per unit: translated step geometry (FStep fields), steps ≤ ℓ + 2
+  __shared__ int wflag[CG];
+  __shared__ int sdesc[CG][kFMS][32];   // per slot: translated step geometry (FStep fields)
   Real* sm = reinterpret_cast<Real*>(fsm);
   constexpr int SH = 1 << LEV;           // window shift between adjacent units (2^ℓ)
   constexpr int VW = FVec<Real>::W;
@@ -319,10 +216,7 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
   unsigned phase = 0u;   // bit b: parity of the next completion of fullbar[b]
   static_assert(NST >= 1 && NST <= 8, "staging depth");
 
-  long long t_ph[6] = {0, 0, 0, 0, 0, 0}, t_last = 0;
-  auto tick = [&](int i) {   // debug phase clocks (thread 0): 0 k-sum 1 descriptors 2 step 1 3 steps ≥ 2 4 gather
-    if (A.dbg && tid == 0) { const long long t = clock64(); t_ph[i] += t - t_last; t_last = t; }
-  };
+  long long t_ksum = 0, t_casc = 0, t_last = 0;
   for (int64_t rd = blockIdx.x; rd < rounds; rd += gridDim.x) {
     if (A.dbg && tid == 0) t_last = clock64();
     const int64_t ufirst = A.u0 + rd * GU;
@@ -336,28 +230,6 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
     const int roff = c1f & 1;                     // R row offset: makes every row base even (pair loads)
     const Real* __restrict__ T = reinterpret_cast<const Real*>(A.T) + S.toff;
 
-    // step descriptors of all GU units: each unit's class record (FStep fields) translated to its position.
-    // field layout (FStep): 0 xr 1 xrl 2 xc 3 xcl 4 ar 5 arl 6 hlo 7 hlen 8 glo 9 glen
-    //                       10+ec blo0  14+ec blen0  18+ec blo1  22+ec blen1  26+ec doff
-    const int steps = S.steps;
-    for (int i = tid; i < GU * steps * 32; i += kFT) {
-      const int uu = i / (steps * 32), rem = i - uu * steps * 32;
-      const int si = rem >> 5, fi = rem & 31;
-      const int pp1 = p1f + uu;
-      const int q0 = p0 & (S.fg_m - 1), q1 = pp1 & (S.fg_m - 1);
-      const FGeom& G = A.geom[S.fg_off + q0 * S.fg_m + q1];
-      const int d0 = p0 - q0, d1 = pp1 - q1;
-      int val = 0;
-      if (fi < 30) {
-        val = reinterpret_cast<const int*>(&G.st[si])[fi];
-        if (fi == 0 || fi == 4) val += g_shift(d0, LEV, si);
-        else if (fi == 2) val += g_shift(d1, LEV, si);
-        else if (fi == 6 || fi == 8 || (fi >= 18 && fi < 22)) val += g_shift(d1, LEV, si + 1);
-        else if (fi >= 10 && fi < 14) val += g_shift(d0, LEV, si + 1);
-      }
-      sdesc[uu][si][fi] = val;
-    }
-    if (tid < GU) wflag[tid] = 0;
     // ------------------------------------------------------------------ a2: k-sum
     {
       const int c1a = c1f & ~(VW - 1);                      // aligned strip start (may be < 0: padded v)
@@ -450,116 +322,195 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
       __syncthreads();
     }
 
-    tick(0);
-    tick(1);
-    // ------------------------------------------------------------------ a3: cascade (descriptors were
-    // written before the k-sum, whose loads hide their latency; the k-sum's final barrier publishes them)
-    const int steps_run = (A.dbg_flags & 2) ? 0 : (A.dbg_flags & 4) ? 1 : steps;   // debug: skip cascade steps
-    // step 1 (the large one): CG units at a time, one thread group each (Yt slot per group)
-    if (steps_run >= 1) {
-      for (int w0 = 0; w0 < GU; w0 += CG) {
-        const int u = w0 + slot;
-        const int* d = &sdesc[u][0][0];
-        Real* X = Rbase + u * A.RSZ;
-        Real* Yt = Ybase + slot * A.YSZ;
-        const int xb = ((p1f + u) << LEV) + S.tSu[1] - roff;   // column of R's local index 0 (even)
-        const int na = passA_count(d);
-        for (int t = gt; t < na; t += GT) passA_task<Real, L2, false>(P, d, X, A.RS, xb, c0, Yt, A.YS, t);
-        bar_group(1 + slot, GT);
-        int n0, n1, n2, n3;
-        passB_counts(d, steps > 1 || P.J == 1, n0, n1, n2, n3);
-        const int nxb = steps > 1 ? (d[32 + 2] & ~(VW - 1)) : 0, nxr = steps > 1 ? d[32 + 0] : 0;
-        for (int t = gt; t < n3; t += GT)
-          passB_task<Real, L2>(P, d, X, A.RS, nxb, nxr, steps > 1, Yt, A.YS, Dbase + u * A.DS, n0, n1, n2, t);
-        bar_group(1 + slot, GT);
+    if (A.dbg && tid == 0) { const long long t = clock64(); t_ksum += t - t_last; t_last = t; }
+    // ------------------------------------------------------------------ a3: cascade of unit u
+    // (CG units at a time, one thread group each; Yt, D and the step descriptors are per group slot)
+    for (int w0 = 0; w0 < GU; w0 += CG) {
+    const int u = w0 + slot;
+    const int p1 = p1f + u;
+    const int cls0 = p0 & (S.fg_m - 1), cls1 = p1 & (S.fg_m - 1);
+    const FGeom& G = A.geom[S.fg_off + cls0 * S.fg_m + cls1];
+    const int d0 = p0 - cls0, d1 = p1 - cls1;
+    const int steps = S.steps;
+    Real* X = Rbase + u * A.RSZ;                 // step input (R, then each step's approximation)
+    Real* Yt = Ybase + slot * A.YSZ;
+    Real* Dd = Dbase + slot * A.DS;
+    int* sd = &sdesc[slot][0][0];
+    // step descriptors: the class record's FStep fields translated to this unit (lane-parallel).
+    // field layout (FStep): 0 xr 1 xrl 2 xc 3 xcl 4 ar 5 arl 6 hlo 7 hlen 8 glo 9 glen
+    //                       10+ec blo0  14+ec blen0  18+ec blo1  22+ec blen1  26+ec doff
+    for (int i = gt; i < steps * 32; i += GT) {
+      const int si = i >> 5, fi = i & 31;
+      int val = 0;
+      if (fi < 30) {
+        val = reinterpret_cast<const int*>(&G.st[si])[fi];
+        if (fi == 0 || fi == 4) val += g_shift(d0, LEV, si);
+        else if (fi == 2) val += g_shift(d1, LEV, si);
+        else if (fi == 6 || fi == 8 || (fi >= 18 && fi < 22)) val += g_shift(d1, LEV, si + 1);
+        else if (fi >= 10 && fi < 14) val += g_shift(d0, LEV, si + 1);
       }
-      __syncthreads();
+      sd[i] = val;
     }
-    tick(2);
-    // steps ≥ 2 (small): all GU units pooled over the CTA, one flat task list per pass; per-unit task counts
-    // (prefix sums) in shared memory
-    for (int s = 2; s <= steps_run; ++s) {
-      if (tid < GU) {
-        const int* d = &sdesc[tid][s - 1][0];
-        pcnt[0][tid] = passA_count(d);
-        passB_counts(d, s < steps || s == P.J, pcnt[1][tid], pcnt[2][tid], pcnt[3][tid], pcnt[4][tid]);
+    if (gt == 0) wflag[slot] = 0;
+    bar_group(1 + slot, GT);
+    int xb = (p1 << LEV) + S.tSu[1] - roff;      // column of X's local index 0 (even)
+    int xr0 = c0;                                // row of X's local index 0
+    const int steps_run = (A.dbg_flags & 2) ? 0 : (A.dbg_flags & 4) ? 1 : steps;   // debug: skip cascade steps
+    for (int s = 1; s <= steps_run; ++s) {
+      const int* d = sd + (s - 1) * 32;
+      const int ar = d[4], arl = d[5];
+      const int hlo = d[6], hlen = d[7], glo = d[8], glen = d[9];
+      // pass A: rows of X (axis 1) -> Yt[col][row - yb]; task = (8-column block of the union of the h and
+      // g output ranges, row), row fastest; a block inside both ranges computes both filters from one load
+      const int yb = ar & ~(VW - 1);
+      {
+        const int gend = glo + glen, hend = hlo + hlen;
+        const int ulo = glen ? (hlen ? min(hlo, glo) : glo) : hlo;
+        const int uhi = glen ? (hlen ? max(hend, gend) : gend) : hend;
+        const int nb = (uhi - ulo + 7) >> 3;
+        const int rows = arl;
+        const int ntask = (hlen + glen) ? nb * rows : 0;
+        const int vlo = d[2] - xb, vhi = vlo + d[3];
+        const float inv = 1.0f / float(max(rows, 1));
+        for (int t = gt; t < ntask; t += GT) {
+          const int q = __float2int_rz((float(t) + 0.5f) * inv);   // t / rows (exact for t < 2^20)
+          const int rr = t - q * rows;
+          const int j0 = ulo + 8 * q;
+          const bool doh = j0 < hend && j0 + 8 > hlo, dog = j0 < gend && j0 + 8 > glo;
+          const int r = ar + rr;
+          const Real* xrow = X + (r - xr0) * A.RS;
+          Real oh[8], og[8];
+          if (s == 1) filt8hg<Real, L2, false>(P, xrow, xb, j0, doh, dog, 8, 8, vlo, vhi, oh, og);
+          else filt8hg<Real, L2, true>(P, xrow, xb, j0, doh, dog, 8, 8, vlo, vhi, oh, og);
+          Real* yh = Yt + (j0 - hlo) * A.YS + (r - yb);
+          Real* yg = Yt + (hlen + j0 - glo) * A.YS + (r - yb);
+          if (doh) {
+            if (j0 >= hlo && j0 + 8 <= hend) {   // whole block inside the h range: plain stores
+#pragma unroll
+              for (int i = 0; i < 8; ++i) yh[i * A.YS] = oh[i];
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (j0 + i >= hlo && j0 + i < hend) yh[i * A.YS] = oh[i];
+            }
+          }
+          if (dog) {
+            if (j0 >= glo && j0 + 8 <= gend) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) yg[i * A.YS] = og[i];
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (j0 + i >= glo && j0 + i < gend) yg[i * A.YS] = og[i];
+            }
+          }
+        }
       }
-      __syncthreads();
-      int tot = 0;
-      for (int u = 0; u < GU; ++u) tot += pcnt[0][u];
-      for (int t = tid; t < tot; t += kFT) {
-        int u = 0, tt = t;
-        while (tt >= pcnt[0][u]) { tt -= pcnt[0][u]; ++u; }
-        const int* d = &sdesc[u][s - 1][0];
-        passA_task<Real, L2, true>(P, d, Rbase + u * A.RSZ, A.RS, d[2] & ~(VW - 1), d[0], Ybase + u * A.YSZ2, A.YS2,
-                                   tt);
+      bar_group(1 + slot, GT);
+      // pass B: Yt rows (axis 0) -> approximation box (next X) and detail boxes (D); one flat task index
+      // over the four boxes (box, row block, column), column fastest
+      int nxb = 0, nxr = 0;
+      if (s < steps) {
+        nxb = d[32 + 2] & ~(VW - 1);
+        nxr = d[32 + 0];
       }
-      __syncthreads();
-      tot = 0;
-      for (int u = 0; u < GU; ++u) tot += pcnt[4][u];
-      for (int t = tid; t < tot; t += kFT) {
-        int u = 0, tt = t;
-        while (tt >= pcnt[4][u]) { tt -= pcnt[4][u]; ++u; }
-        const int* d = &sdesc[u][s - 1][0];
-        const int nxb = s < steps ? (d[32 + 2] & ~(VW - 1)) : 0, nxr = s < steps ? d[32 + 0] : 0;
-        passB_task<Real, L2>(P, d, Rbase + u * A.RSZ, A.RS, nxb, nxr, s < steps, Ybase + u * A.YSZ2, A.YS2,
-                             Dbase + u * A.DS, pcnt[1][u], pcnt[2][u], pcnt[3][u], tt);
+      {
+        const bool want0 = s < steps || s == P.J;
+        const int vlo = ar - yb, vhi = vlo + arl;
+        const int n0 = want0 ? ((d[14] + 7) >> 3) * d[22] : 0;
+        const int n1 = n0 + ((d[15] + 7) >> 3) * d[23];
+        const int n2 = n1 + ((d[16] + 7) >> 3) * d[24];
+        const int n3 = n2 + ((d[17] + 7) >> 3) * d[25];
+        for (int t = gt; t < n3; t += GT) {
+          const int ec = (t >= n0) + (t >= n1) + (t >= n2);
+          const int idx = t - (ec == 0 ? 0 : ec == 1 ? n0 : ec == 2 ? n1 : n2);
+          const int bl0 = d[14 + ec], bl1 = d[22 + ec];
+          const int q = __float2int_rz((float(idx) + 0.5f) * __frcp_rn(float(bl1)));   // idx / bl1
+          const int cc = idx - q * bl1;
+          const int l0 = d[10 + ec] + 8 * q;
+          const int nrow = min(8, bl0 - 8 * q);
+          const int j = d[18 + ec] + cc;
+          const int e0 = ec >> 1, e1 = ec & 1;
+          const int ycol = e1 ? hlen + (j - glo) : (j - hlo);
+          Real out[8];
+          if (e0) filt8<Real, L2, 1, true>(P, Yt + ycol * A.YS, yb, l0, nrow, vlo, vhi, out);
+          else filt8<Real, L2, 0, true>(P, Yt + ycol * A.YS, yb, l0, nrow, vlo, vhi, out);
+          Real* dst;
+          int dstr;
+          if (ec == 0 && s < steps) {
+            dst = X + (l0 - nxr) * A.RS + (j - nxb);
+            dstr = A.RS;
+          } else {
+            dst = Dd + d[26 + ec] + (8 * q) * bl1 + cc;
+            dstr = bl1;
+          }
+          if (nrow == 8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i * dstr] = out[i];
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i < nrow) dst[i * dstr] = out[i];
+          }
+        }
       }
-      __syncthreads();
+      bar_group(1 + slot, GT);
+      xb = nxb;
+      xr0 = nxr;
     }
 
-    tick(3);
-    // ------------------------------------------------------------------ a4: gather + write rows (pooled)
+    // ------------------------------------------------------------------ a4: gather + write row
     {
+      const int lev = LEV;
       const int4* st = A.stencil + S.stencil_off;
       const int L = P.band_L;
+      const int64_t base = (ufirst + u - A.row0) * L;
       Real* outv = reinterpret_cast<Real*>(A.val);
-      const float invL = __frcp_rn(float(L));
-      for (int i = tid; i < GU * L; i += kFT) {
-        const int u = __float2int_rz((float(i) + 0.5f) * invL), jj = i - u * L;
-        const int p1 = p1f + u;
+      Real* sv = Yt;                              // wrap-case stage (Yt is dead now)
+      int* sc = reinterpret_cast<int*>(sv + P.band_Lpad);
+      int wrap = 0;
+      for (int jj = gt; jj < L; jj += GT) {
         const int4 e = st[jj];
         const int s = e.w;                        // level of the partner sub-band
         const SubBand& Lb = P.sb[e.x];
-        const int D = s - LEV;
+        const int D = s - lev;
         const int b0 = D == 0 ? p0 : (D < 0 ? (p0 << -D) : (p0 >> D));
         const int b1 = D == 0 ? p1 : (D < 0 ? (p1 << -D) : (p1 >> D));
         const int l0 = b0 + e.y, l1 = b1 + e.z;
         const int ec = Lb.e;
-        const int* dl = &sdesc[u][s - 1][0];
+        const int* dl = sd + (s - 1) * 32;
         const int i0 = l0 - dl[10 + ec], i1 = l1 - dl[18 + ec];
         const int bl1 = dl[22 + ec];
         Real x = Real(0);
-        if (i0 >= 0 && i0 < dl[14 + ec] && i1 >= 0 && i1 < bl1) x = Dbase[u * A.DS + dl[26 + ec] + i0 * bl1 + i1];
-        const bool wr = (l0 < 0) | (l0 >= Lb.nl) | (l1 < 0) | (l1 >= Lb.nl);
+        if (i0 >= 0 && i0 < dl[14 + ec] && i1 >= 0 && i1 < bl1) x = Dd[dl[26 + ec] + i0 * bl1 + i1];
+        wrap |= (l0 < 0) | (l0 >= Lb.nl) | (l1 < 0) | (l1 >= Lb.nl);
         const int c = int(Lb.offset + int64_t(l0 & (Lb.nl - 1)) * Lb.nl + (l1 & (Lb.nl - 1)));
-        Real* sv = Ybase + u * A.YSZ2;             // per-unit stage (Yt is dead now)
-        int* sc = reinterpret_cast<int*>(sv + P.band_Lpad);
         sv[jj] = x;
         sc[jj] = c;
-        if (wr) wflag[u] = 1;
       }
-      __syncthreads();
-      for (int i = tid; i < GU * L; i += kFT) {
-        const int u = __float2int_rz((float(i) + 0.5f) * invL), jj = i - u * L;
-        const Real* sv = Ybase + u * A.YSZ2;
-        const int* sc = reinterpret_cast<const int*>(sv + P.band_Lpad);
+      // any partner wraps around the torus -> place by rank of the column
+      if (wrap) wflag[slot] = 1;
+      bar_group(1 + slot, GT);
+      wrap = wflag[slot];
+      for (int jj = gt; jj < L; jj += GT) {
         const int c = sc[jj];
         int rank = jj;
-        if (wflag[u]) {                          // a partner wraps around the torus: place by rank of the column
+        if (wrap) {
           rank = 0;
-          for (int k2 = 0; k2 < L; ++k2) rank += sc[k2] < c;
+          for (int i = 0; i < L; ++i) rank += sc[i] < c;
         }
-        const int64_t base = (ufirst + u - A.row0) * L;
         A.col[base + rank] = c;
         outv[base + rank] = sv[jj];
       }
     }
     __syncthreads();
-    tick(4);
+    }
+    if (A.dbg && tid == 0) { const long long t = clock64(); t_casc += t - t_last; t_last = t; }
   }
-  if (A.dbg && tid == 0)
-    for (int i = 0; i < 5; ++i) atomicAdd(A.dbg + i, (unsigned long long)t_ph[i]);
+  if (A.dbg && tid == 0) {
+    atomicAdd(A.dbg, (unsigned long long)t_ksum);
+    atomicAdd(A.dbg + 1, (unsigned long long)t_casc);
+  }
 }
 
 // ---------------------------------------------------------------------------------- launcher
