@@ -111,8 +111,9 @@ __global__ void __launch_bounds__(kB) bk_ksum_tiled(const __grid_constant__ Plan
   constexpr int VW = 16 / int(sizeof(Real));  // elements per 16-byte vector
   constexpr int VWID = SH * (GZ + G - 1);     // v columns the G windows read
   constexpr int VS = VWID + VW;               // staged v row (aligned start + misalignment)
-  __shared__ __align__(16) Real Ts[2][TR][TW];
-  __shared__ __align__(16) Real Vs[2][TR][VS];
+  extern __shared__ __align__(16) unsigned char ksm[];   // dynamic: Ts[2][TR][TW], Vs[2][TR][VS]
+  auto Ts = reinterpret_cast<Real(*)[TR][TW]>(ksm);
+  auto Vs = reinterpret_cast<Real(*)[TR][VS]>(ksm + sizeof(Real) * 2 * TR * TW);
   const int tid = threadIdx.x;
   const int n = P.n, mask = n - 1;
   const int64_t ug = A.u0 + int64_t(blockIdx.y) * G;            // first unit of the group
@@ -615,9 +616,23 @@ __global__ void __launch_bounds__(kB) bk_write(const __grid_constant__ Plan P, c
 
 // Tiled k-sum when every window of the launch's level stays inside one period per axis, the shift 2^ℓ is
 // in [8, 128], and groups of G units stay in one sub-band row.  Returns false to use bk_ksum instead.
+template <typename Real, int LEV, int G, int GZ>
+static void launch_tiled_t(const Plan& P, const BatchArgs& A, dim3 grid, int ntile1, cudaStream_t st) {
+  constexpr int SH = 1 << LEV, TR = kB / SH, TW = SH * GZ, VW = 16 / int(sizeof(Real));
+  constexpr int VS = SH * (GZ + G - 1) + VW;
+  constexpr size_t smem = sizeof(Real) * 2 * (size_t(TR) * TW + size_t(TR) * VS);
+  auto k = bk_ksum_tiled<Real, LEV, G, GZ>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  k<<<grid, kB, smem, st>>>(P, A, ntile1);
+}
+
 template <typename Real>
 static bool launch_ksum_tiled(const Plan& P, const BatchArgs& A, int nb, cudaStream_t st) {
-  constexpr int G = sizeof(Real) == 4 ? 8 : 4, GZ = sizeof(Real) == 4 ? 8 : 4;   // static smem < 48 KB
+  constexpr int G = sizeof(Real) == 4 ? 8 : 4;
   if (getenv("PCWD_NO_TILED_KSUM")) return false;
   const int s0 = find_subband_host(P, A.u0), s1 = find_subband_host(P, A.u1 - 1);
   const SubBand& S = P.sb[s0];
@@ -627,17 +642,33 @@ static bool launch_ksum_tiled(const Plan& P, const BatchArgs& A, int nb, cudaStr
     if (P.sb[q].level != lev || P.sb[q].tW[0] >= P.n || P.sb[q].tW[1] >= P.n || P.sb[q].tW[0] != S.tW[0] ||
         P.sb[q].tW[1] != S.tW[1] || P.sb[q].e == 0)
       return false;
-  const int SH = 1 << lev, TR = kB / SH, TW = SH * GZ;
-  const int ntile0 = (S.tW[0] + TR - 1) / TR, ntile1 = (S.tW[1] + TW - 1) / TW;
-  const dim3 grid(ntile0 * ntile1, nb / G);
-  switch (lev) {
-    case 3: bk_ksum_tiled<Real, 3, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
-    case 4: bk_ksum_tiled<Real, 4, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
-    case 5: bk_ksum_tiled<Real, 5, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
-    case 6: bk_ksum_tiled<Real, 6, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
-    case 7: bk_ksum_tiled<Real, 7, G, GZ><<<grid, kB, 0, st>>>(P, A, ntile1); break;
+  // template columns per thread: the GZ ∈ {4, ..., 10} (fp64: {2, 4}) whose tiles waste the fewest columns
+  const int SH = 1 << lev, TR = kB / SH;
+  const int cand_f[] = {8, 9, 10, 6, 5, 4}, cand_d[] = {4, 2};
+  const int* cand = sizeof(Real) == 4 ? cand_f : cand_d;
+  const int ncand = sizeof(Real) == 4 ? 6 : 2;
+  int GZ = cand[0];
+  int64_t best = -1;
+  for (int c = 0; c < ncand; ++c) {
+    const int tw = SH * cand[c], nt = (S.tW[1] + tw - 1) / tw;
+    const int64_t cost = int64_t(nt) * (tw + SH * (G - 1));   // staged v columns per tile row ≈ traffic + work
+    if (best < 0 || cost < best) { best = cost; GZ = cand[c]; }
   }
-  return true;
+  const int ntile0 = (S.tW[0] + TR - 1) / TR, ntile1 = (S.tW[1] + SH * GZ - 1) / (SH * GZ);
+  const dim3 grid(ntile0 * ntile1, nb / G);
+#define PCWD_KT(L, Z) if (lev == L && GZ == Z) { launch_tiled_t<Real, L, G, Z>(P, A, grid, ntile1, st); return true; }
+  if constexpr (sizeof(Real) == 4) {
+    PCWD_KT(3, 8) PCWD_KT(3, 9) PCWD_KT(3, 10) PCWD_KT(3, 6) PCWD_KT(3, 5) PCWD_KT(3, 4)
+    PCWD_KT(4, 8) PCWD_KT(4, 9) PCWD_KT(4, 10) PCWD_KT(4, 6) PCWD_KT(4, 5) PCWD_KT(4, 4)
+    PCWD_KT(5, 8) PCWD_KT(5, 9) PCWD_KT(5, 10) PCWD_KT(5, 6) PCWD_KT(5, 5) PCWD_KT(5, 4)
+    PCWD_KT(6, 8) PCWD_KT(6, 9) PCWD_KT(6, 10) PCWD_KT(6, 6) PCWD_KT(6, 5) PCWD_KT(6, 4)
+    PCWD_KT(7, 8) PCWD_KT(7, 9) PCWD_KT(7, 10) PCWD_KT(7, 6) PCWD_KT(7, 5) PCWD_KT(7, 4)
+  } else {
+    PCWD_KT(3, 4) PCWD_KT(3, 2) PCWD_KT(4, 4) PCWD_KT(4, 2) PCWD_KT(5, 4) PCWD_KT(5, 2)
+    PCWD_KT(6, 4) PCWD_KT(6, 2) PCWD_KT(7, 4) PCWD_KT(7, 2)
+  }
+#undef PCWD_KT
+  return false;
 }
 
 // Full-torus windows: bk_ksum_full when 2^ℓ ≤ 256, a row of the sub-band is one group (nl ∈ {2, 4, 8}).
