@@ -364,10 +364,10 @@ __global__ void __launch_bounds__(kB) bk_passB(const __grid_constant__ Plan P, c
 // input (zero outside its window, periodic where the window covers a line) into shared memory, filtered
 // along axis 1 into a second tile, then along axis 0 into the next approximation (h taps only; the
 // stencil's detail coefficients are computed directly by bk_gather).
-template <typename Real, int L2>
+template <typename Real, int L2, int TO>
 __global__ void __launch_bounds__(kB) bk_approx(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
                                                 int s, int ntx) {
-  constexpr int TO = sizeof(Real) == 4 ? 32 : 16;   // outputs per tile side (static smem < 48 KB)
+  // TO: outputs per tile side (chosen per step by the launcher; static smem < 48 KB)
   constexpr int TI = 2 * (TO - 1) + L2;              // inputs per tile side
   constexpr int XS = ((TI + 1 + 1) / 2) * 2 % 4 == 2 ? ((TI + 1 + 1) / 2) * 2 : ((TI + 1 + 1) / 2) * 2 + 2;   // even, ≡ 2 mod 4
   constexpr int NI = 2 * 3 + L2;                     // inputs of 4 consecutive outputs
@@ -499,24 +499,46 @@ __global__ void __launch_bounds__(kB) bk_approx(const __grid_constant__ Plan P, 
   }
 }
 
+template <typename Real, int TO>
+static void launch_approx_to(const Plan& P, const BatchArgs& A, int s, dim3 grid, int ntx, cudaStream_t st) {
+  switch (P.L2) {
+    case 2: bk_approx<Real, 2, TO><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 4: bk_approx<Real, 4, TO><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 6: bk_approx<Real, 6, TO><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 8: bk_approx<Real, 8, TO><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 10: bk_approx<Real, 10, TO><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+    case 12: bk_approx<Real, 12, TO><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
+  }
+}
+
+// Tile side per step: the TO ∈ {16, 24, 32} (fp64: {16}) with the least staged input Σ_tiles (2·TO + 2δ)²
+// (edge tiles that run past the output window waste their share).
 template <typename Real>
 static void launch_approx(const Plan& P, const BatchArgs& A, int s, int64_t maxA0, int64_t maxA1, int nb,
                           cudaStream_t st) {
-  constexpr int TO = sizeof(Real) == 4 ? 32 : 16;
-  const int ntx = int((maxA1 + TO - 1) / TO), nty = int((maxA0 + TO - 1) / TO);
+  if (P.L2 > 12 || (P.L2 & 1)) {
+    auto gx = [](int64_t elems) { return int(std::max<int64_t>(1, std::min<int64_t>((elems + kB - 1) / kB, 64))); };
+    bk_passA<Real><<<dim3(gx(maxA0 * 2 * maxA1 / 4 + 1), nb), kB, 0, st>>>(P, A, s);
+    bk_passB<Real><<<dim3(gx(maxA0 * maxA1 / 4 + 1), nb), kB, 0, st>>>(P, A, s);
+    return;
+  }
+  int best_to = 16;
+  int64_t best = -1;
+  const int cands[3] = {32, 24, 16};
+  for (int c = 0; c < (sizeof(Real) == 4 ? 3 : 1); ++c) {
+    const int to = sizeof(Real) == 4 ? cands[c] : 16;
+    const int64_t ti = 2 * (to - 1) + P.L2;
+    const int64_t cost = ((maxA0 + to - 1) / to) * ((maxA1 + to - 1) / to) * (ti * ti + 2048);   // + per-CTA overhead
+    if (best < 0 || cost < best) { best = cost; best_to = to; }
+  }
+  const int ntx = int((maxA1 + best_to - 1) / best_to), nty = int((maxA0 + best_to - 1) / best_to);
   const dim3 grid(ntx * nty, nb);
-  switch (P.L2) {
-    case 2: bk_approx<Real, 2><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
-    case 4: bk_approx<Real, 4><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
-    case 6: bk_approx<Real, 6><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
-    case 8: bk_approx<Real, 8><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
-    case 10: bk_approx<Real, 10><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
-    case 12: bk_approx<Real, 12><<<grid, kB, 0, st>>>(P, A, s, ntx); break;
-    default: {
-      auto gx = [](int64_t elems) { return int(std::max<int64_t>(1, std::min<int64_t>((elems + kB - 1) / kB, 64))); };
-      bk_passA<Real><<<dim3(gx(maxA0 * 2 * maxA1 / 4 + 1), nb), kB, 0, st>>>(P, A, s);
-      bk_passB<Real><<<dim3(gx(maxA0 * maxA1 / 4 + 1), nb), kB, 0, st>>>(P, A, s);
-    }
+  if constexpr (sizeof(Real) == 4) {
+    if (best_to == 32) launch_approx_to<Real, 32>(P, A, s, grid, ntx, st);
+    else if (best_to == 24) launch_approx_to<Real, 24>(P, A, s, grid, ntx, st);
+    else launch_approx_to<Real, 16>(P, A, s, grid, ntx, st);
+  } else {
+    launch_approx_to<Real, 16>(P, A, s, grid, ntx, st);
   }
 }
 
