@@ -520,13 +520,15 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         // R rows: [roff, roff + R1) valid, zero pad of ≥ 2δ + 2 after (serves as the next row's left pad);
         // even stride with an odd number of pairs (16 lanes of 8-byte loads hit distinct banks)
         auto pair_stride = [&](int w) { int x = (w + 1) / 2 * 2; if ((x / 2) % 2 == 0) x += 2; return x; };
-        const int RS = pair_stride(R1 + 1 + P.L2 + 2);
+        int roffmax = 0;   // R rows are shifted by one column when a window starts at an odd column
+        for (int q = s; q < e; ++q) roffmax |= P.sb[q].tSu[1] & 1;
+        const int RS = pair_stride(R1 + roffmax + P.L2 + 2);
         const int zmaxT = (SH - 1) + SH * fc.GZ * (NZB - 1) + SH * (fc.GZ - 1);
         const int zmaxV = zmaxT + SH * (fc.GU - 1);
         const int TS = odd_stride(std::max(S0.tRS, zmaxT + 1));
         const int VS = odd_stride(VW - 1 + std::max(R1 + SH * (fc.GU - 1), zmaxV + 1));
         const int YS = pair_stride(arl + VW - 1);
-        const int64_t lpad = P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb;
+        const int64_t lpad = P.band_Lpad + (int64_t(P.band_Lpad) * 8 + rb - 1) / rb;   // gather: values, columns, heavy list
         const int64_t YSZ = (int64_t(ycols) * YS + VW - 1) / VW * VW;
         const int YS2 = pair_stride(arl2 + VW - 1);
         const int64_t YSZ2 = (std::max<int64_t>(int64_t(ycols2) * YS2, lpad) + VW - 1) / VW * VW;
@@ -566,6 +568,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           A.regS = regR; A.regD = regD;
           A.TSZ = TSZ; A.VSZ = VSZ;
           A.nst = nst;
+          A.direct = getenv("PCWD_NO_DIRECT") ? 0 : 1;
           (void)stg;
           A.sb_first = s;
           // halo of the padded v that every round's boxes stay inside

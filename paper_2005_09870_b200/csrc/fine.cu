@@ -189,6 +189,19 @@ template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int C
 __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Plan P, const __grid_constant__ FineArgs A) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int wflag[CG];
+  __shared__ int nheavy[CG];
+  __shared__ Real onef[2][kMaxTaps];              // f_0 = h, f_1 = g taps (gather's direct partners)
+  __shared__ Real comp[2][3 * kMaxTaps - 2];      // two-step composites: c_e[x] = Σ_{2t+u=x} f_e[t] h[u]
+  if (threadIdx.x < 2 * (3 * kMaxTaps - 2)) {
+    const int e = threadIdx.x / (3 * kMaxTaps - 2), x = threadIdx.x % (3 * kMaxTaps - 2);
+    double c = 0.0;
+    for (int t = 0; t < L2; ++t) {
+      const int uu = x - 2 * t;
+      if (uu >= 0 && uu < L2) c += P.td[e][t] * P.td[0][uu];
+    }
+    comp[e][x] = Real(c);
+    if (x < L2) onef[e][x] = Real(P.td[e][x]);
+  }
   __shared__ int sdesc[CG][kFMS][32];   // per slot: translated step geometry (FStep fields)
   Real* sm = reinterpret_cast<Real*>(fsm);
   constexpr int SH = 1 << LEV;           // window shift between adjacent units (2^ℓ)
@@ -351,11 +364,16 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
       }
       sd[i] = val;
     }
-    if (gt == 0) wflag[slot] = 0;
+    if (gt == 0) { wflag[slot] = 0; nheavy[slot] = 0; }
     bar_group(1 + slot, GT);
     int xb = (p1 << LEV) + S.tSu[1] - roff;      // column of X's local index 0 (even)
     int xr0 = c0;                                // row of X's local index 0
-    const int steps_run = (A.dbg_flags & 2) ? 0 : (A.dbg_flags & 4) ? 1 : steps;   // debug: skip cascade steps
+    // cascade steps 1..S1; the partners of the last two levels are computed in the gather directly from the
+    // step-S1 approximation (2δ × 2δ taps for level S1 + 1, composite (3·2δ − 2)² taps for S1 + 2), which
+    // replaces the two smallest, latency-bound cascade steps
+    const int S1 = A.direct ? (steps <= 2 ? 1 : steps - 2) : steps;
+    int steps_run = (A.dbg_flags & 2) ? 0 : (A.dbg_flags & 4) ? 1 : steps;   // debug: skip cascade steps
+    steps_run = min(steps_run, S1);
     for (int s = 1; s <= steps_run; ++s) {
       const int* d = sd + (s - 1) * 32;
       const int ar = d[4], arl = d[5];
@@ -469,6 +487,11 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
       Real* sv = Yt;                              // wrap-case stage (Yt is dead now)
       int* sc = reinterpret_cast<int*>(sv + P.band_Lpad);
       int wrap = 0;
+      int* hl = sc + P.band_Lpad;                  // heavy (two-step) partners of this unit
+      // X_{S1} (the step-S1 approximation) in the R region: box rows [bxr, bxr + bxrl), columns [bxc, bxc + bxcl),
+      // local origin (xr0, xb)
+      const int* dn = sd + min(S1, steps - 1) * 32;
+      const int bxr = dn[0], bxrl = dn[1], bxc = dn[2], bxcl = dn[3];
       for (int jj = gt; jj < L; jj += GT) {
         const int4 e = st[jj];
         const int s = e.w;                        // level of the partner sub-band
@@ -478,11 +501,38 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
         const int b1 = D == 0 ? p1 : (D < 0 ? (p1 << -D) : (p1 >> D));
         const int l0 = b0 + e.y, l1 = b1 + e.z;
         const int ec = Lb.e;
-        const int* dl = sd + (s - 1) * 32;
-        const int i0 = l0 - dl[10 + ec], i1 = l1 - dl[18 + ec];
-        const int bl1 = dl[22 + ec];
+        const int e0 = ec >> 1, e1 = ec & 1;
         Real x = Real(0);
-        if (i0 >= 0 && i0 < dl[14 + ec] && i1 >= 0 && i1 < bl1) x = Dd[dl[26 + ec] + i0 * bl1 + i1];
+        if (s <= S1) {
+          const int* dl = sd + (s - 1) * 32;
+          const int i0 = l0 - dl[10 + ec], i1 = l1 - dl[18 + ec];
+          const int bl1 = dl[22 + ec];
+          if (i0 >= 0 && i0 < dl[14 + ec] && i1 >= 0 && i1 < bl1) x = Dd[dl[26 + ec] + i0 * bl1 + i1];
+        } else if (s == S1 + 1) {
+          // one analysis step applied to X_{S1} at this coefficient only (2δ × 2δ taps)
+          const int r0 = 2 * l0 + (e0 ? 2 - L2 : 0), q0 = 2 * l1 + (e1 ? 2 - L2 : 0);
+          const int ta = max(0, bxr - r0), tb = min(L2, bxr + bxrl - r0);
+          const int ua = max(0, bxc - q0), ub = min(L2, bxc + bxcl - q0);
+          const Real* row0 = X + (r0 - xr0) * A.RS + (q0 - xb);
+          if (ta == 0 && tb == L2 && ua == 0 && ub == L2) {
+#pragma unroll
+            for (int t = 0; t < L2; ++t) {
+              Real acc = Real(0);
+#pragma unroll
+              for (int u2 = 0; u2 < L2; ++u2) acc = ffma_(onef[e1][u2], row0[t * A.RS + u2], acc);
+              x = ffma_(onef[e0][t], acc, x);
+            }
+          } else {
+            for (int t = ta; t < tb; ++t) {
+              Real acc = Real(0);
+              for (int u2 = ua; u2 < ub; ++u2) acc = ffma_(onef[e1][u2], row0[t * A.RS + u2], acc);
+              x = ffma_(onef[e0][t], acc, x);
+            }
+          }
+        } else {
+          // two steps (composite taps): deferred to the warp-cooperative pass below
+          hl[atomicAdd(&nheavy[slot], 1)] = jj;
+        }
         wrap |= (l0 < 0) | (l0 >= Lb.nl) | (l1 < 0) | (l1 >= Lb.nl);
         const int c = int(Lb.offset + int64_t(l0 & (Lb.nl - 1)) * Lb.nl + (l1 & (Lb.nl - 1)));
         sv[jj] = x;
@@ -490,6 +540,36 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
       }
       // any partner wraps around the torus -> place by rank of the column
       if (wrap) wflag[slot] = 1;
+      bar_group(1 + slot, GT);
+      // partners two levels past S1: one warp per coefficient, lanes over the (3·2δ − 2) rows of its
+      // composite footprint, warp reduction
+      {
+        const int nh = nheavy[slot];
+        const int wg = gt >> 5, lane = gt & 31, nw = GT >> 5;
+        constexpr int NT2 = 3 * L2 - 2;
+        for (int h = wg; h < nh; h += nw) {
+          const int jj = hl[h];
+          const int4 e = st[jj];
+          const SubBand& Lb = P.sb[e.x];
+          const int D = e.w - lev;
+          const int b0 = D == 0 ? p0 : (D < 0 ? (p0 << -D) : (p0 >> D));
+          const int b1 = D == 0 ? p1 : (D < 0 ? (p1 << -D) : (p1 >> D));
+          const int l0 = b0 + e.y, l1 = b1 + e.z;
+          const int e0 = Lb.e >> 1, e1 = Lb.e & 1;
+          const int r0 = 4 * l0 + 2 * (e0 ? 2 - L2 : 0), q0 = 4 * l1 + 2 * (e1 ? 2 - L2 : 0);
+          const int ua = max(0, bxc - q0), ub = min(NT2, bxc + bxcl - q0);
+          Real part = Real(0);
+          for (int t = lane; t < NT2; t += 32) {
+            if (r0 + t < bxr || r0 + t >= bxr + bxrl) continue;
+            const Real* row = X + (r0 + t - xr0) * A.RS + (q0 - xb);
+            Real acc = Real(0);
+            for (int u2 = ua; u2 < ub; ++u2) acc = ffma_(comp[e1][u2], row[u2], acc);
+            part = ffma_(comp[e0][t], acc, part);
+          }
+          for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+          if (lane == 0) sv[jj] = part;
+        }
+      }
       bar_group(1 + slot, GT);
       wrap = wflag[slot];
       for (int jj = gt; jj < L; jj += GT) {
