@@ -274,22 +274,30 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
       const int nst = A.nst;           // staging buffers in use (≤ NST, as many as fit in the R region)
       for (int q = 1; q < nst; ++q)
         if (q < P.m) stage(q, q);
+      // per-task offsets into the staged T / v tiles (loop-invariant over k)
+      int tofs[NT], vofs[NT];
+      bool tact[NT];
+#pragma unroll
+      for (int a = 0; a < NT; ++a) {
+        const int t = tid + a * kFT;
+        const int r = t / Q;
+        const int q = t - r * Q;
+        const int res = q % SH, zb = q / SH;
+        const int z0 = res + SH * zb * GZ;
+        tact[a] = r < R0;
+        tofs[a] = r * A.TS + z0;
+        vofs[a] = A.TSZ + r * A.VS + sh + z0;
+      }
       int b = 0;
       for (int k = 0; k < P.m; ++k) {
         mbar_wait(&fullbar[b], (phase >> b) & 1u);
         phase ^= 1u << b;
         const Real* Ts = Sbase + b * (A.TSZ + A.VSZ);
-        const Real* Vs = Ts + A.TSZ;
 #pragma unroll
         for (int a = 0; a < NT; ++a) {
-          const int t = tid + a * kFT;
-          const int r = t / Q;
-          if (r < R0) {
-            const int q = t - r * Q;
-            const int res = q % SH, zb = q / SH;
-            const int z0 = res + SH * zb * GZ;
-            const Real* tr = Ts + r * A.TS + z0;
-            const Real* vr = Vs + r * A.VS + sh + z0;
+          if (tact[a]) {
+            const Real* tr = Ts + tofs[a];
+            const Real* vr = Ts + vofs[a];
             Real tv[GZ];
 #pragma unroll
             for (int i = 0; i < GZ; ++i) tv[i] = tr[SH * i];
