@@ -97,10 +97,11 @@ def dist_env():
 def cpu_oracle_rate(p, budget_s: float = 20.0, seed: int = 0):
     """Oracle (oracle/rows.c + brute-force band ranking) timed on a bounded stratified sample of units.
 
-    Per level, a few units are computed (one batch, OpenMP over units) and timed; the per-unit wall time
-    with all threads busy is extrapolated to every unit of the level: entries/s = nnz / Σ_level count·t̄.
-    Fine levels take one unit per thread; levels whose units cost more (window ≥ n/4) take one unit
-    each, computed together in a single batch so the threads stay busy."""
+    Levels are measured finest first (one unit per host thread, one batch per level) while the running time
+    stays within `budget_s`; a level whose single unit would exceed what is left is not run.  The oracle's
+    per-unit cost is dominated by the adjoint sum over the nonzeros of ψ_μ (rows.c), so unmeasured levels are
+    extrapolated with t(ℓ) = a + b·|supp ψ_ℓ| fitted (least squares) on the measured levels.  entries/s =
+    nnz / Σ_ℓ count(ℓ)·t(ℓ)."""
     from oracle import basis
     from oracle import retention as ret
     from oracle import rows as R
@@ -110,11 +111,10 @@ def cpu_oracle_rate(p, budget_s: float = 20.0, seed: int = 0):
     for (lev, e, off, nl) in basis.subbands(p.d, p.n, p.J):
         levels.setdefault(lev, []).append((off, nl ** p.d))
     lev_order = sorted(levels)
-    R_ = int(p.meta.get("R", 0)) if hasattr(p, "meta") else 0
-    fine = [l for l in lev_order if ((2 ** l - 1) * (len(p.h) - 1) + 1 + 2 * R_) < p.n // 4]
-    coarse = [l for l in lev_order if l not in fine]
-    t_total_est, sampled, spent = 0.0, 0, 0.0
-    per_level = {}
+
+    def supp(lev):   # nonzeros of ψ_μ at level ℓ (P:103-104 length, periodic)
+        w = min(p.n, (2 ** lev - 1) * (len(p.h) - 1) + 1)
+        return w ** p.d
 
     def pick(lev, k):
         offs = levels[lev]
@@ -124,37 +124,38 @@ def cpu_oracle_rate(p, budget_s: float = 20.0, seed: int = 0):
             out.append(off + int(rng.integers(c)))
         return out
 
-    for lev in fine:
-        units = pick(lev, nthreads if spent < budget_s else 1)
-        t0 = time.perf_counter()
-        rows = R.rows(p, units, nthreads=nthreads)
-        for i, mu in enumerate(units):
-            ret.retained_row(p, mu, rows[i])
-        dt = time.perf_counter() - t0
-        spent += dt
-        sampled += len(units)
-        per_level[lev] = dt / len(units) * min(1.0, len(units) / nthreads) if len(units) < nthreads else dt / len(units)
-    if coarse:
-        units = [u for lev in coarse for u in pick(lev, 1)]
-        t0 = time.perf_counter()
-        rows = R.rows(p, units, nthreads=nthreads)
-        for i, mu in enumerate(units):
-            ret.retained_row(p, mu, rows[i])
-        dt = time.perf_counter() - t0
-        spent += dt
-        sampled += len(units)
-        # units ran concurrently (≤ 1 thread each): a unit's cost with every thread busy is dt / nthreads
-        # when there are at least as many units as threads, else dt·(units/threads) / units = dt / threads
-        for lev in coarse:
-            per_level[lev] = dt / max(nthreads, len(units))
+    per_unit, spent, sampled = {}, 0.0, 0
     for lev in lev_order:
-        count = sum(c for _, c in levels[lev])
-        t_total_est += per_level[lev] * count
+        if len(per_unit) >= 2:                      # predict this level's single-unit time
+            xs = np.array([supp(l) for l in per_unit], dtype=float)
+            ys = np.array([per_unit[l] * nthreads for l in per_unit])   # single-thread seconds per unit
+            b, a = np.polyfit(xs, ys, 1)
+            if a + b * supp(lev) > budget_s - spent:
+                break
+        k = nthreads if lev == lev_order[0] or per_unit.get(lev - 1, 0) * nthreads < budget_s / 8 else 1
+        units = pick(lev, k)
+        t0 = time.perf_counter()
+        rows = R.rows(p, units, nthreads=nthreads)
+        for i, mu in enumerate(units):
+            ret.retained_row(p, mu, rows[i])
+        dt = time.perf_counter() - t0
+        spent += dt
+        sampled += len(units)
+        per_unit[lev] = dt / max(len(units), nthreads)   # wall seconds per unit with every thread busy
+    measured = sorted(per_unit)
+    xs = np.array([supp(l) for l in measured], dtype=float)
+    ys = np.array([per_unit[l] for l in measured])
+    b, a = np.polyfit(xs, ys, 1) if len(measured) >= 2 else (0.0, ys[0])
+    t_total_est = 0.0
+    for lev in lev_order:
+        t_unit = per_unit[lev] if lev in per_unit else a + b * supp(lev)
+        t_total_est += t_unit * sum(c for _, c in levels[lev])
+    extrap = [l for l in lev_order if l not in per_unit]
     nnz = p.N * p.band_L if p.retain == "band" else p.N * p.N
     return {"value": nnz / t_total_est, "unit": "entries/s", "cores": nthreads, "kind": "oracle",
-            "sample": (f"{sampled} units stratified over {len(levels)} levels ({spent:.1f} s wall on "
-                       f"{nthreads} threads), extrapolated per level to all {p.N} units: "
-                       f"est. {t_total_est:.0f} s for the full decomposition")}, t_total_est
+            "sample": (f"{sampled} units over levels {measured} ({spent:.1f} s wall on {nthreads} threads); "
+                       f"levels {extrap} extrapolated by t = a + b·|supp ψ| fitted on the measured levels; "
+                       f"est. {t_total_est:.0f} s for all {p.N} units")}, t_total_est
 
 
 def run_reference(args):
