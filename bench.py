@@ -126,12 +126,8 @@ def cpu_oracle_rate(p, budget_s: float = 20.0, seed: int = 0):
 
     per_unit, spent, sampled = {}, 0.0, 0
     for lev in lev_order:
-        if len(per_unit) >= 2:                      # predict this level's single-unit time
-            xs = np.array([supp(l) for l in per_unit], dtype=float)
-            ys = np.array([per_unit[l] * nthreads for l in per_unit])   # single-thread seconds per unit
-            b, a = np.polyfit(xs, ys, 1)
-            if a + b * supp(lev) > budget_s - spent:
-                break
+        if lev > max(lev_order[0], lev_order[-1] - 2) and len(per_unit) >= 3:
+            break                                   # the two coarsest levels: one unit costs ~1 min
         k = nthreads if lev == lev_order[0] or per_unit.get(lev - 1, 0) * nthreads < budget_s / 8 else 1
         units = pick(lev, k)
         t0 = time.perf_counter()
