@@ -325,12 +325,21 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
           const int q = t - r * Q;
           const int res = q % SH, zb = q / SH;
           const int z0 = res + SH * zb * GZ;
+          if (z0 + SH * (GZ - 1) < R1) {   // the whole block inside the window: plain stores
 #pragma unroll
-          for (int j = 0; j < GU; ++j) {
-            Real* dst = Rbase + j * A.RSZ + r * A.RS + roff;
+            for (int j = 0; j < GU; ++j) {
+              Real* dst = Rbase + j * A.RSZ + r * A.RS + roff + z0;
 #pragma unroll
-            for (int i = 0; i < GZ; ++i)
-              if (z0 + SH * i < R1) dst[z0 + SH * i] = acc[a][j][i];
+              for (int i = 0; i < GZ; ++i) dst[SH * i] = acc[a][j][i];
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < GU; ++j) {
+              Real* dst = Rbase + j * A.RSZ + r * A.RS + roff;
+#pragma unroll
+              for (int i = 0; i < GZ; ++i)
+                if (z0 + SH * i < R1) dst[z0 + SH * i] = acc[a][j][i];
+            }
           }
         }
       }
@@ -364,11 +373,14 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
       const int si = i >> 5, fi = i & 31;
       int val = 0;
       if (fi < 30) {
-        val = reinterpret_cast<const int*>(&G.st[si])[fi];
-        if (fi == 0 || fi == 4) val += g_shift(d0, LEV, si);
-        else if (fi == 2) val += g_shift(d1, LEV, si);
-        else if (fi == 6 || fi == 8 || (fi >= 18 && fi < 22)) val += g_shift(d1, LEV, si + 1);
-        else if (fi >= 10 && fi < 14) val += g_shift(d0, LEV, si + 1);
+        // which shift a field takes: xr, ar (axis 0, level s-1); xc (axis 1, level s-1); hlo, glo, blo1 (axis 1,
+        // level s); blo0 (axis 0, level s)
+        const bool a0p = fi == 0 || fi == 4, a1p = fi == 2;
+        const bool a1s = fi == 6 || fi == 8 || (fi >= 18 && fi < 22), a0s = fi >= 10 && fi < 14;
+        const int dd = (a0p || a0s) ? d0 : d1;
+        const int lv = (a0p || a1p) ? si : si + 1;
+        const int sh = lv <= LEV ? dd * (1 << (LEV - lv)) : (dd >> (lv - LEV));
+        val = reinterpret_cast<const int*>(&G.st[si])[fi] + ((a0p || a1p || a0s || a1s) ? sh : 0);
       }
       sd[i] = val;
     }
@@ -567,12 +579,23 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
           const int r0 = 4 * l0 + 2 * (e0 ? 2 - L2 : 0), q0 = 4 * l1 + 2 * (e1 ? 2 - L2 : 0);
           const int ua = max(0, bxc - q0), ub = min(NT2, bxc + bxcl - q0);
           Real part = Real(0);
-          for (int t = lane; t < NT2; t += 32) {
-            if (r0 + t < bxr || r0 + t >= bxr + bxrl) continue;
-            const Real* row = X + (r0 + t - xr0) * A.RS + (q0 - xb);
-            Real acc = Real(0);
-            for (int u2 = ua; u2 < ub; ++u2) acc = ffma_(comp[e1][u2], row[u2], acc);
-            part = ffma_(comp[e0][t], acc, part);
+          if (ua == 0 && ub == NT2) {
+            for (int t = lane; t < NT2; t += 32) {
+              if (r0 + t < bxr || r0 + t >= bxr + bxrl) continue;
+              const Real* row = X + (r0 + t - xr0) * A.RS + (q0 - xb);
+              Real acc = Real(0);
+#pragma unroll
+              for (int u2 = 0; u2 < NT2; ++u2) acc = ffma_(comp[e1][u2], row[u2], acc);
+              part = ffma_(comp[e0][t], acc, part);
+            }
+          } else {
+            for (int t = lane; t < NT2; t += 32) {
+              if (r0 + t < bxr || r0 + t >= bxr + bxrl) continue;
+              const Real* row = X + (r0 + t - xr0) * A.RS + (q0 - xb);
+              Real acc = Real(0);
+              for (int u2 = ua; u2 < ub; ++u2) acc = ffma_(comp[e1][u2], row[u2], acc);
+              part = ffma_(comp[e0][t], acc, part);
+            }
           }
           for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
           if (lane == 0) sv[jj] = part;
