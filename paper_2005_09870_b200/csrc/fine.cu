@@ -535,11 +535,18 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
           const int ua = max(0, bxc - q0), ub = min(L2, bxc + bxcl - q0);
           const Real* row0 = X + (r0 - xr0) * A.RS + (q0 - xb);
           if (ta == 0 && tb == L2 && ua == 0 && ub == L2) {
+            // rows of 2δ taps start at an even column (q0 - xb even, even row stride): pair loads
+            using V2 = typename std::conditional<sizeof(Real) == 4, float2, double2>::type;
 #pragma unroll
             for (int t = 0; t < L2; ++t) {
+              const V2* rp = reinterpret_cast<const V2*>(row0 + t * A.RS);
               Real acc = Real(0);
 #pragma unroll
-              for (int u2 = 0; u2 < L2; ++u2) acc = ffma_(onef[e1][u2], row0[t * A.RS + u2], acc);
+              for (int u2 = 0; u2 < L2 / 2; ++u2) {
+                const V2 pr = rp[u2];
+                acc = ffma_(onef[e1][2 * u2], pr.x, acc);
+                acc = ffma_(onef[e1][2 * u2 + 1], pr.y, acc);
+              }
               x = ffma_(onef[e0][t], acc, x);
             }
           } else {
@@ -580,12 +587,17 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
           const int ua = max(0, bxc - q0), ub = min(NT2, bxc + bxcl - q0);
           Real part = Real(0);
           if (ua == 0 && ub == NT2) {
+            using V2 = typename std::conditional<sizeof(Real) == 4, float2, double2>::type;
             for (int t = lane; t < NT2; t += 32) {
               if (r0 + t < bxr || r0 + t >= bxr + bxrl) continue;
-              const Real* row = X + (r0 + t - xr0) * A.RS + (q0 - xb);
+              const V2* rp = reinterpret_cast<const V2*>(X + (r0 + t - xr0) * A.RS + (q0 - xb));
               Real acc = Real(0);
 #pragma unroll
-              for (int u2 = 0; u2 < NT2; ++u2) acc = ffma_(comp[e1][u2], row[u2], acc);
+              for (int u2 = 0; u2 < NT2 / 2; ++u2) {   // q0 - xb even: pair loads
+                const V2 pr = rp[u2];
+                acc = ffma_(comp[e1][2 * u2], pr.x, acc);
+                acc = ffma_(comp[e1][2 * u2 + 1], pr.y, acc);
+              }
               part = ffma_(comp[e0][t], acc, part);
             }
           } else {
