@@ -486,7 +486,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     // fine kernel (fine.cu): levels 1..3 whose every sub-band has a class geometry table
     {
       FineCfg fc{};
-      bool ok = P.retain == PCWD_RETAIN_BAND && P.d == 2 && fine_config(rb, lev, P.L2, &fc) && !getenv("PCWD_NO_FINE");
+      bool ok = P.retain == PCWD_RETAIN_BAND && P.d == 2 && fine_config(rb, lev, P.L2, &fc) && !getenv("PCWD_NO_FINE") &&
+                lev <= (getenv("PCWD_FINE_MAXLEV") ? atoi(getenv("PCWD_FINE_MAXLEV")) : 3);
       for (int q = s; q < e && ok; ++q) ok = P.sb[q].fg_m > 0 && P.sb[q].e != 0 && P.sb[q].nl % fc.GU == 0;
       if (ok) {
         const int VW = 16 / rb, SH = 1 << lev;
@@ -562,6 +563,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           F.level = lev;
           F.smem = smem;
           const int per_sm = int(std::max<size_t>(1, std::min<size_t>(2, (228 * 1024) / (smem + 4096))));
+          // (MINB = 1 instances use up to 255 registers: one CTA per SM regardless of smem)
           F.grid = int(std::min<int64_t>((a1 - a0) / fc.GU, int64_t(nsm) * per_sm));
           FineArgs& A = F.fa;
           A.u0 = a0; A.u1 = a1;

@@ -18,6 +18,7 @@
 // Geometry comes from the host plan (one record per sub-band and class p mod 2^{steps-ℓ}, geom.h),
 // translated to the unit's position.
 #include <climits>
+#include <cstdlib>
 #include <type_traits>
 
 #include "geom.h"
@@ -185,8 +186,8 @@ __device__ __forceinline__ void filt8hg(const Plan& P, const Real* __restrict__ 
 //   [slack] R_0 .. R_{GU-1} (RS × R0 each; later the approximation of each step, row stride RS) [slack]
 //   [slack] staging: NST × (T_k tile R0 × TS, v_k strip R0 × VS)  ∪  Yt_0 .. Yt_{GU-1} (YC × YS)  [slack]
 //   D_0 .. D_{GU-1} (DS each)
-template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG>
-__global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Plan P, const __grid_constant__ FineArgs A) {
+template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG, int MINB>
+__global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__ Plan P, const __grid_constant__ FineArgs A) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int wflag[CG];
   __shared__ int nheavy[CG];
@@ -638,12 +639,20 @@ __global__ void __launch_bounds__(kFT, 2) fine_kernel(const __grid_constant__ Pl
 
 // ---------------------------------------------------------------------------------- launcher
 
+// "wide" fp32 variants: twice the units per round at one CTA per SM (up to 255 registers, ~200 KB smem):
+// more template reuse per staged tile.  PCWD_FINE_WIDE = bit mask over levels 1..3 (default: level 3).
+static int fine_wide(int level) {
+  static const int mask = getenv("PCWD_FINE_WIDE") ? atoi(getenv("PCWD_FINE_WIDE")) : 4;
+  return (mask >> (level - 1)) & 1;
+}
+
 bool fine_config(int real_bytes, int level, int L2, FineCfg* c) {
   if (L2 != 2 && L2 != 4 && L2 != 8 && L2 != 12) return false;
   if (real_bytes == 4) {
-    if (level == 1) { *c = FineCfg{8, 11, 1, 4, 4}; return true; }
-    if (level == 2) { *c = FineCfg{4, 15, 1, 2, 4}; return true; }
-    if (level == 3) { *c = FineCfg{2, 11, 3, 1, 2}; return true; }
+    const int wide = fine_wide(level);
+    if (level == 1) { *c = wide ? FineCfg{16, 11, 1, 4, 8} : FineCfg{8, 11, 1, 4, 4}; return true; }
+    if (level == 2) { *c = wide ? FineCfg{8, 15, 1, 2, 4} : FineCfg{4, 15, 1, 2, 4}; return true; }
+    if (level == 3) { *c = wide ? FineCfg{4, 11, 3, 2, 4} : FineCfg{2, 11, 3, 1, 2}; return true; }
   } else {
     if (level == 1) { *c = FineCfg{4, 11, 1, 1, 4}; return true; }
     if (level == 2) { *c = FineCfg{2, 15, 1, 1, 2}; return true; }
@@ -652,9 +661,9 @@ bool fine_config(int real_bytes, int level, int L2, FineCfg* c) {
   return false;
 }
 
-template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG>
+template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG, int MINB>
 static cudaError_t launch_fine_t(const Plan& P, const FineArgs& A, int grid, size_t smem, cudaStream_t st) {
-  auto k = fine_kernel<Real, L2, LEV, GU, GZ, NT, NST, CG>;
+  auto k = fine_kernel<Real, L2, LEV, GU, GZ, NT, NST, CG, MINB>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
@@ -667,13 +676,23 @@ template <int L2>
 static cudaError_t launch_fine_l2(const Plan& P, const FineArgs& A, int real_bytes, int level, int grid, size_t smem,
                                   cudaStream_t st) {
   if (real_bytes == 4) {
-    if (level == 1) return launch_fine_t<float, L2, 1, 8, 11, 1, 4, 4>(P, A, grid, smem, st);
-    if (level == 2) return launch_fine_t<float, L2, 2, 4, 15, 1, 2, 4>(P, A, grid, smem, st);
-    if (level == 3) return launch_fine_t<float, L2, 3, 2, 11, 3, 1, 2>(P, A, grid, smem, st);
+    const int wide = fine_wide(level);
+    if (level == 1) {
+      if (wide) return launch_fine_t<float, L2, 1, 16, 11, 1, 4, 8, 1>(P, A, grid, smem, st);
+      return launch_fine_t<float, L2, 1, 8, 11, 1, 4, 4, 2>(P, A, grid, smem, st);
+    }
+    if (level == 2) {
+      if (wide) return launch_fine_t<float, L2, 2, 8, 15, 1, 2, 4, 1>(P, A, grid, smem, st);
+      return launch_fine_t<float, L2, 2, 4, 15, 1, 2, 4, 2>(P, A, grid, smem, st);
+    }
+    if (level == 3) {
+      if (wide) return launch_fine_t<float, L2, 3, 4, 11, 3, 2, 4, 1>(P, A, grid, smem, st);
+      return launch_fine_t<float, L2, 3, 2, 11, 3, 1, 2, 2>(P, A, grid, smem, st);
+    }
   } else {
-    if (level == 1) return launch_fine_t<double, L2, 1, 4, 11, 1, 1, 4>(P, A, grid, smem, st);
-    if (level == 2) return launch_fine_t<double, L2, 2, 2, 15, 1, 1, 2>(P, A, grid, smem, st);
-    if (level == 3) return launch_fine_t<double, L2, 3, 1, 11, 3, 1, 1>(P, A, grid, smem, st);
+    if (level == 1) return launch_fine_t<double, L2, 1, 4, 11, 1, 1, 4, 2>(P, A, grid, smem, st);
+    if (level == 2) return launch_fine_t<double, L2, 2, 2, 15, 1, 1, 2, 2>(P, A, grid, smem, st);
+    if (level == 3) return launch_fine_t<double, L2, 3, 1, 11, 3, 1, 1, 2>(P, A, grid, smem, st);
   }
   return cudaErrorInvalidValue;
 }
