@@ -109,6 +109,24 @@ int pcwd_get_csr(void* handle, pcwd_csr* out);
  * may be NULL to skip that array.  Enqueued on stream. */
 int pcwd_copy_csr(void* handle, int64_t* row_ptr, int32_t* col, void* val, void* stream);
 
+/* Replace the operator's kernels (u_k, v_k of H f = Σ_k u_k ⋆ (v_k ⊙ f)) on an existing
+ * handle, keeping its plan (sub-band table, windows, stencil, shard, launch plan, buffers): the
+ * "plan once, decompose many operators" use.  u, v: m·N fp64 each, layout as in pcwd_desc, host
+ * (pinned for asynchronous copies) or device pointers; the caller keeps ownership.  The union of
+ * supp u_k must lie inside the periodic bounding box of the u given to pcwd_create (the windows
+ * of the plan are derived from it): checked on the GPU, PCWD_E_PARAM otherwise (the
+ * handle then keeps its previous kernels).  Invalidates the last decompose.  Enqueued on stream,
+ * then synchronises it once for the support check. */
+int pcwd_set_kernels(void* handle, const double* u, const double* v, void* stream);
+
+/* pcwd_decompose followed by the copy of the CSR into caller buffers (as pcwd_copy_csr; NULL
+ * skips an array), with the copies overlapped with the computation: BAND and FULL rows have a
+ * fixed width, so each launch's rows are copied (on a second stream, event-ordered) as soon as
+ * that launch has finished, the largest level first.  THRESHOLD: decompose, then copy.  Enqueued
+ * on `stream`: the host buffers are complete once `stream` has been synchronised.  Host buffers
+ * should be pinned (pageable memory serialises the copies). */
+int pcwd_decompose_to_host(void* handle, int64_t* row_ptr, int32_t* col, void* val, void* stream);
+
 /* y = Θ_ret x (transpose = 0: x has N entries, y has n_rows) or y = Θ_retᵀ x (transpose = 1:
  * x has n_rows entries, y has N, overwritten).  x, y: DEVICE arrays of type dtype.
  * This is the Θ_L z product of Eq. (7).  Enqueued on stream. */

@@ -35,6 +35,7 @@ struct Launch {
   int64_t workA[kMaxJ + 1] = {}, workB[kMaxJ + 1] = {};   // batched: per-step work items of pass A / B
   int64_t appr0[kMaxJ + 1] = {}, appr1[kMaxJ + 1] = {};   // batched: per-step max approximation window
   int steps = 0;
+  int gu = 1;       // fine: units per round (chunks of a launch are multiples of it)
 };
 
 struct Handle {
@@ -72,6 +73,14 @@ struct Handle {
   bool profile = false;
   cudaEvent_t ev[8] = {};
   std::vector<cudaEvent_t> lev;     // profile: one event pair per unit launch (run_units)
+  cudaStream_t cs = nullptr;        // decompose_to_host: copy stream
+  std::vector<cudaEvent_t> cev;     // decompose_to_host: chunk-done events
+  cudaEvent_t cjoin = nullptr;      // decompose_to_host: copies done
+  double* ustage = nullptr;         // set_kernels: staging of u (swapped with u_d once checked)
+  void* vstage = nullptr;           // set_kernels: staging of v (fp64; swapped with v_d in fp64 compute)
+  struct Sink { int64_t width; int32_t* col; char* val; int ob; };
+  const Sink* sink = nullptr;       // decompose_to_host: caller buffers the finished rows go to
+  int* flag_d = nullptr;            // set_kernels: support check flag
   int64_t rows() const { return hp.row1 - hp.row0; }
 };
 
@@ -100,9 +109,15 @@ bool is_device_ptr(const void* p) {
 
 void free_all(Handle* h) {
   void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->gscratch, h->bscratch,
-                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax};
+                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->ustage, h->vstage, h->flag_d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& e : h->cev) cudaEventDestroy(e);
+  h->cev.clear();
+  if (h->cjoin) cudaEventDestroy(h->cjoin);
+  h->cjoin = nullptr;
+  if (h->cs) cudaStreamDestroy(h->cs);
+  h->cs = nullptr;
 }
 
 template <typename T>
@@ -192,9 +207,31 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     h->lev.assign(2 * h->launches.size(), nullptr);
     for (auto& e : h->lev) CK(cudaEventCreate(&e));
   }
-  int li = -1;
-  for (const Launch& L : h->launches) {
-    ++li;
+  // decompose_to_host: after each launch, its rows (fixed width in BAND / FULL) are copied on the
+  // copy stream, ordered by an event; the largest level runs first so that the copies start early
+  const Handle::Sink* sk = h->sink;
+  int ci = 0;
+  auto emit = [&](int64_t a, int64_t b) -> int {
+    if (!sk || b <= a) return PCWD_OK;
+    if (ci >= int(h->cev.size())) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->cev.push_back(e);
+    }
+    cudaEvent_t e = h->cev[ci++];
+    CK(cudaEventRecord(e, st));
+    CK(cudaStreamWaitEvent(h->cs, e, 0));
+    const int64_t off = (a - h->hp.row0) * sk->width, cnt = (b - a) * sk->width;
+    if (sk->col) CK(cudaMemcpyAsync(sk->col + off, h->col + off, cnt * sizeof(int32_t), cudaMemcpyDefault, h->cs));
+    if (sk->val)
+      CK(cudaMemcpyAsync(sk->val + off * sk->ob, static_cast<char*>(h->val) + off * sk->ob, cnt * sk->ob,
+                         cudaMemcpyDefault, h->cs));
+    return PCWD_OK;
+  };
+  const int nL = int(h->launches.size());
+  for (int it = 0; it < nL; ++it) {
+    const int li = sk ? nL - 1 - it : it;
+    const Launch& L = h->launches[li];
     if (h->profile) cudaEventRecord(h->lev[2 * li], st);
     struct Rec {   // record the launch's end event on every path out of this iteration
       Handle* h; int i; cudaStream_t st;
@@ -213,6 +250,7 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
       int nl = 0;
       CK(launch_band_batched(P, B, h->hp.real_bytes, L.maxX0, L.workA, L.workB, L.appr0, L.appr1, L.steps, st, &nl));
       h->nlaunch += nl;
+      if (int rc = emit(L.u0, L.u1)) return rc;
       continue;
     }
     if (L.fine) {
@@ -233,8 +271,23 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
       }
       F.dbg = dbg;
       F.dbg_flags = getenv("PCWD_FINE_DBG") ? atoi(getenv("PCWD_FINE_DBG")) : 0;
-      CK(launch_fine(P, F, h->hp.real_bytes, L.level, L.grid, L.smem, st));
-      h->nlaunch++;
+      {
+        // chunks of about 64K units when the rows stream to the host (each chunk's copy overlaps the next)
+        const int64_t GU = L.gu, units = L.u1 - L.u0;
+        int64_t chunk = units;
+        if (sk) {
+          const int64_t nch = std::max<int64_t>(1, (units + 65535) / 65536);
+          chunk = ((units + nch - 1) / nch + GU - 1) / GU * GU;
+        }
+        for (int64_t a = L.u0; a < L.u1; a += chunk) {
+          const int64_t b = std::min(L.u1, a + chunk);
+          F.u0 = a;
+          F.u1 = b;
+          CK(launch_fine(P, F, h->hp.real_bytes, L.level, int(std::min<int64_t>(L.grid, (b - a) / GU)), L.smem, st));
+          h->nlaunch++;
+          if (int rc = emit(a, b)) return rc;
+        }
+      }
       if (dbg_on) {
         unsigned long long c[8];
         CK(cudaMemcpy(c, dbg, sizeof(c), cudaMemcpyDeviceToHost));
@@ -266,6 +319,7 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
       }
       CK(launch_band_tile(P, T, h->hp.real_bytes, L.grid, L.smem, st));
       h->nlaunch++;
+      if (int rc = emit(L.u0, L.u1)) return rc;
       if (dbg_on) {
         unsigned long long c[8];
         CK(cudaMemcpy(c, dbg, sizeof(c), cudaMemcpyDeviceToHost));
@@ -296,6 +350,8 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     A.use_smem = L.smem > 0;
     CK(launch_units(P, A, mode, h->hp.real_bytes, h->hp.out_bytes, L.grid, L.smem, st));
     h->nlaunch++;
+    if (mode == MODE_BAND || mode == MODE_FULL)
+      if (int rc = emit(L.u0, L.u1)) return rc;
   }
   return PCWD_OK;
 }
@@ -560,6 +616,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         if (ok && a1 > a0) {
           Launch F{a0, a1, 0, 0};
           F.fine = 1;
+          F.gu = fc.GU;
           F.level = lev;
           F.smem = smem;
           const int per_sm = int(std::max<size_t>(1, std::min<size_t>(2, (228 * 1024) / (smem + 4096))));
@@ -757,9 +814,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
   for (const Launch& L : h->launches) any_fine = any_fine || L.fine;
   if (any_fine) {
     const int W = P.n + 2 * h->vpad;
-    CKB(dalloc(&h->vpad_d, size_t(P.m) * W * W * rb));
-    CKB(launch_pad_v(h->v_d, h->vpad_d, P.n, h->vpad, P.m, rb, 0));
-    CKB(cudaDeviceSynchronize());
+    CKB(dalloc(&h->vpad_d, size_t(P.m) * W * W * rb));   // filled by every decompose (pad_v_kernel)
     for (Launch& L : h->launches) {
       if (!L.fine) continue;
       int rc2 = encode_map3(&L.fa.tmV, h->vpad_d, rb, W, W, P.m, int64_t(W), int64_t(W) * W, L.box[2], L.box[0]);
@@ -836,6 +891,10 @@ int pcwd_decompose(void* handle, void* stream) {
   auto rec = [&](int i) { if (h->profile) cudaEventRecord(h->ev[i], st); };
   if (P.retain == PCWD_RETAIN_BAND) {
     rec(0);
+    if (h->vpad_d) {   // periodically padded copy of v, the TMA source of the fine kernels
+      CK(launch_pad_v(h->v_d, h->vpad_d, P.n, h->vpad, P.m, h->hp.real_bytes, st));
+      h->nlaunch++;
+    }
     if ((rc = build_templates(h, st))) return rc;
     rec(1);
     if ((rc = run_units(h, MODE_BAND, st, 0.0))) return rc;
@@ -914,6 +973,60 @@ int pcwd_copy_csr(void* handle, int64_t* row_ptr, int32_t* col, void* val, void*
   if (row_ptr) CK(cudaMemcpyAsync(row_ptr, h->row_ptr, (h->rows() + 1) * sizeof(int64_t), cudaMemcpyDefault, st));
   if (col && h->nnz) CK(cudaMemcpyAsync(col, h->col, h->nnz * sizeof(int32_t), cudaMemcpyDefault, st));
   if (val && h->nnz) CK(cudaMemcpyAsync(val, h->val, h->nnz * h->hp.out_bytes, cudaMemcpyDefault, st));
+  return PCWD_OK;
+}
+
+int pcwd_set_kernels(void* handle, const double* u, const double* v, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !u || !v) return fail(PCWD_E_PARAM, "NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(h->desc.device));
+  const Plan& P = h->hp.P;
+  const int64_t mN = int64_t(P.m) * P.N;
+  const int rb = h->hp.real_bytes;
+  if (!h->ustage) CK(dalloc(&h->ustage, mN * sizeof(double)));
+  if (!h->vstage) CK(dalloc(&h->vstage, mN * sizeof(double)));
+  if (!h->flag_d) CK(dalloc(&h->flag_d, sizeof(int)));
+  CK(cudaMemsetAsync(h->flag_d, 0, sizeof(int), st));
+  CK(cudaMemcpyAsync(h->ustage, u, mN * sizeof(double), cudaMemcpyDefault, st));
+  CK(launch_support_check(h->ustage, mN, P.n, P.d, P.zlo, P.zhi, h->flag_d, st));
+  CK(cudaMemcpyAsync(h->vstage, v, mN * sizeof(double), cudaMemcpyDefault, st));
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, h->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (flag)
+    return fail(PCWD_E_PARAM, "supp u_k leaves the periodic bounding box the plan was built for (create a new handle)");
+  std::swap(h->u_d, h->ustage);
+  if (rb == 8) std::swap(h->v_d, h->vstage);
+  else CK(launch_cast(static_cast<const double*>(h->vstage), h->v_d, mN, 4, st));
+  h->M_set = false;
+  h->tmpl_fresh = false;
+  h->decomposed = false;
+  return PCWD_OK;
+}
+
+int pcwd_decompose_to_host(void* handle, int64_t* row_ptr, int32_t* col, void* val, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(PCWD_E_PARAM, "NULL handle");
+  CK(cudaSetDevice(h->desc.device));
+  const Plan& P = h->hp.P;
+  if (P.retain == PCWD_RETAIN_THRESHOLD) {
+    int rc = pcwd_decompose(handle, stream);
+    return rc ? rc : pcwd_copy_csr(handle, row_ptr, col, val, stream);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!h->cs) CK(cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking));
+  const Handle::Sink sk{P.retain == PCWD_RETAIN_BAND ? int64_t(P.band_L) : P.N, col, static_cast<char*>(val),
+                        h->hp.out_bytes};
+  h->sink = &sk;
+  int rc = pcwd_decompose(handle, stream);
+  h->sink = nullptr;
+  if (rc) return rc;
+  if (row_ptr) CK(cudaMemcpyAsync(row_ptr, h->row_ptr, (h->rows() + 1) * sizeof(int64_t), cudaMemcpyDefault, st));
+  // join: `stream` waits for the last copy
+  if (!h->cjoin) CK(cudaEventCreateWithFlags(&h->cjoin, cudaEventDisableTiming));
+  CK(cudaEventRecord(h->cjoin, h->cs));
+  CK(cudaStreamWaitEvent(st, h->cjoin, 0));
   return PCWD_OK;
 }
 

@@ -14,6 +14,7 @@
 // first); its windows live in shared memory when they fit, else in a per-CTA global slice.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <climits>
 
 #include "kernels.cuh"
@@ -565,6 +566,28 @@ cudaError_t launch_pad_v(const void* v, void* vpad, int n, int P, int m, int rea
   const int64_t total = int64_t(m) * (n + 2 * P) * (n + 2 * P);
   if (real_bytes == 4) pad_v_kernel<float><<<grid_for(total), kBlock, 0, st>>>((const float*)v, (float*)vpad, n, P, m);
   else pad_v_kernel<double><<<grid_for(total), kBlock, 0, st>>>((const double*)v, (double*)vpad, n, P, m);
+  return cudaGetLastError();
+}
+
+// Support check of pcwd_set_kernels: flag = 1 if some u_k(z) != 0 lies outside the planned periodic
+// box [zlo_a, zhi_a] of an axis (the plan's windows are derived from that box).
+__global__ void support_check_kernel(const double* __restrict__ u, int64_t total, int n, int d, int zlo0, int w0,
+                                     int zlo1, int w1, int* flag) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    if (u[i] == 0.0) continue;
+    const int64_t z = d == 2 ? i % (int64_t(n) * n) : i % n;
+    const int z1 = int(z % n), z0 = int(z / n);
+    const bool in1 = ((z1 - zlo1) % n + n) % n < w1;
+    const bool in0 = d == 1 || ((z0 - zlo0) % n + n) % n < w0;
+    if (!(in0 && in1)) *flag = 1;
+  }
+}
+
+cudaError_t launch_support_check(const double* u, int64_t total, int n, int d, const int zlo[2], const int zhi[2],
+                                 int* flag, cudaStream_t st) {
+  const int w0 = zhi[0] - zlo[0] + 1, w1 = zhi[1] - zlo[1] + 1;
+  support_check_kernel<<<std::min(grid_for(total), 148 * 8), kBlock, 0, st>>>(u, total, n, d, zlo[0], w0, zlo[1], w1,
+                                                                              flag);
   return cudaGetLastError();
 }
 

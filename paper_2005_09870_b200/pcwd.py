@@ -52,7 +52,8 @@ class Info(ctypes.Structure):
 EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_max", "pcwd_get_csr",
            "pcwd_copy_csr", "pcwd_apply", "pcwd_info", "pcwd_destroy", "pcwd_error_string",
            "pcwd_last_error", "pcwd_validate", "pcwd_plan_shard", "pcwd_plan_stencil",
-           "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile"]
+           "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile",
+           "pcwd_set_kernels", "pcwd_decompose_to_host"]
 
 _lib = None
 
@@ -85,6 +86,8 @@ def lib():
         L.pcwd_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         dp = ctypes.POINTER(ctypes.c_double)
         L.pcwd_launch_profile.argtypes = [vp, ctypes.c_int, i32p, dp, dp, i32p, i32p]
+        L.pcwd_set_kernels.argtypes = [vp, vp, vp, vp]
+        L.pcwd_decompose_to_host.argtypes = [vp, vp, vp, vp, vp]
         for f in EXPORTS:
             getattr(L, f)  # every declared symbol must exist
         _lib = L
@@ -150,6 +153,20 @@ class Decomposition:
     # -- compute ------------------------------------------------------------------------
     def decompose(self, stream: int = 0):
         _check(lib().pcwd_decompose(self._h, ctypes.c_void_p(stream)), "pcwd_decompose")
+
+    def set_kernels(self, u, v, stream: int = 0):
+        """New operator kernels (u_k, v_k) on this handle's plan (pcwd_set_kernels): (m, N) fp64,
+        host (pinned for overlap) or CUDA; supp u_k must stay inside the box the plan was built for."""
+        self._keep = (u, v)
+        _check(lib().pcwd_set_kernels(self._h, ctypes.c_void_p(_ptr(u)), ctypes.c_void_p(_ptr(v)),
+                                      ctypes.c_void_p(stream)), "pcwd_set_kernels")
+
+    def decompose_to_host(self, row_ptr, col, val, stream: int = 0):
+        """Decompose with the CSR streamed into the given (pinned host) buffers as launches finish
+        (pcwd_decompose_to_host); complete once `stream` is synchronised."""
+        _check(lib().pcwd_decompose_to_host(self._h, ctypes.c_void_p(_ptr(row_ptr)), ctypes.c_void_p(_ptr(col)),
+                                            ctypes.c_void_p(_ptr(val)), ctypes.c_void_p(stream)),
+               "pcwd_decompose_to_host")
 
     def local_max(self, stream: int = 0) -> float:
         out = ctypes.c_double()
