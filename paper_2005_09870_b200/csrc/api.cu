@@ -50,6 +50,8 @@ struct Handle {
   int4* box_d = nullptr;
   FGeom* fgeom_d = nullptr;
   void* vpad_d = nullptr;   // periodically padded v (fine path TMA source)
+  void* vwrap_d = nullptr;  // v extended periodically by kt_pr rows / kt_pc columns (tiled k-sum TMA source)
+  int kt_pr = 0, kt_pc = 0;
   int vpad = 0;
   void* gscratch = nullptr;
   int64_t gstride = 0;
@@ -108,7 +110,7 @@ bool is_device_ptr(const void* p) {
 }
 
 void free_all(Handle* h) {
-  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->gscratch, h->bscratch,
+  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->vwrap_d, h->gscratch, h->bscratch,
                   h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->ustage, h->vstage, h->flag_d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -800,6 +802,25 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       B.maxY = my;
       B.maxB = mb;
       B.steps = steps;
+      // tiled k-sum with TMA staging (levels ≤ 5): maps of the level's templates here, of the periodically
+      // extended v once its extent (max strip over the levels) is known
+      B.level = lev;
+      static const int tma_maxlev = getenv("PCWD_TMA_KSUM_MAXLEV") ? atoi(getenv("PCWD_TMA_KSUM_MAXLEV")) : 7;
+      const int gz = lev <= tma_maxlev && !getenv("PCWD_NO_TMA_KSUM") ? ksum_tiled_gz(P, u0, u1, rb) : 0;
+      if (gz) {
+        const int SH = 1 << lev, TR = 256 / SH, G = kt_units(rb);
+        const int qT = kt_box_q(SH, gz, kt_box_n(SH, gz));
+        const int qV = kt_vbox_q(SH, gz + G - 1, kt_vbox_n(SH, gz + G - 1, rb), rb);
+        h->kt_pr = std::max(h->kt_pr, TR);
+        h->kt_pc = std::max(h->kt_pc, SH * qV + kt_vpadx(SH, rb));   // one v box past the seam
+        int rc2 = 0;
+        for (int q = s, i = 0; q < e && i < 3 && !rc2; ++q, ++i)
+          rc2 = encode_map3(&B.ba.tmT[i], static_cast<char*>(h->T_d) + P.sb[q].toff * rb, rb, P.sb[q].tRS, P.sb[q].tW[0],
+                            P.m, P.sb[q].tRS, P.sb[q].tstride, SH * qT, TR);
+        if (rc2) return bail(PCWD_E_CUDA, "cuTensorMapEncodeTiled (k-sum) failed: " + std::to_string(rc2));
+        B.ba.kt_gz = gz;
+        B.ba.kt_sb_first = s;
+      }
       h->bscratch_bytes = std::max(h->bscratch_bytes, size_t(batch) * stride * rb);
       h->launches.push_back(B);
       s = e;
@@ -809,6 +830,20 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     s = e;
   }
   if (h->bscratch_bytes) CKB(dalloc(&h->bscratch, h->bscratch_bytes + 1024));   // + vector over-read slack
+  if (h->kt_pc > 0) {   // v extended periodically by kt_pr rows and kt_pc columns: every k-sum v box is one TMA copy
+    h->kt_pc = (h->kt_pc + 31) / 32 * 32;
+    const int H = P.n + h->kt_pr, W = P.n + h->kt_pc;
+    CKB(dalloc(&h->vwrap_d, size_t(P.m) * H * W * rb));
+    for (Launch& L : h->launches) {
+      if (!L.batched || !L.ba.kt_gz) continue;
+      const int SH = 1 << L.level, TR = 256 / SH, G = kt_units(rb), q0 = L.ba.kt_gz + G - 1;
+      const int qV = kt_vbox_q(SH, q0, kt_vbox_n(SH, q0, rb), rb);
+      const int rc2 = encode_map3(&L.ba.tmV, h->vwrap_d, rb, W, H, P.m, W, int64_t(W) * H, SH * qV + kt_vpadx(SH, rb), TR);
+      if (rc2) return bail(PCWD_E_CUDA, "cuTensorMapEncodeTiled (k-sum v) failed: " + std::to_string(rc2));
+      L.ba.kt_vh = H;
+      L.ba.kt_vw = W;
+    }
+  }
   // fine path: periodically padded v (K1) and the TMA descriptors of every fine launch
   bool any_fine = false;
   for (const Launch& L : h->launches) any_fine = any_fine || L.fine;
@@ -893,6 +928,10 @@ int pcwd_decompose(void* handle, void* stream) {
     rec(0);
     if (h->vpad_d) {   // periodically padded copy of v, the TMA source of the fine kernels
       CK(launch_pad_v(h->v_d, h->vpad_d, P.n, h->vpad, P.m, h->hp.real_bytes, st));
+      h->nlaunch++;
+    }
+    if (h->vwrap_d) {  // periodic extension of v, the TMA source of the tiled coarse k-sums
+      CK(launch_wrap_v(h->v_d, h->vwrap_d, P.n, 0, P.n + h->kt_pr, P.n + h->kt_pc, P.m, h->hp.real_bytes, st));
       h->nlaunch++;
     }
     if ((rc = build_templates(h, st))) return rc;
@@ -997,7 +1036,8 @@ int pcwd_set_kernels(void* handle, const double* u, const double* v, void* strea
   if (flag)
     return fail(PCWD_E_PARAM, "supp u_k leaves the periodic bounding box the plan was built for (create a new handle)");
   std::swap(h->u_d, h->ustage);
-  if (rb == 8) std::swap(h->v_d, h->vstage);
+  // v_d stays in place: the k-sum TMA maps hold its address
+  if (rb == 8) CK(cudaMemcpyAsync(h->v_d, h->vstage, mN * sizeof(double), cudaMemcpyDeviceToDevice, st));
   else CK(launch_cast(static_cast<const double*>(h->vstage), h->v_d, mN, 4, st));
   h->M_set = false;
   h->tmpl_fresh = false;

@@ -9,9 +9,11 @@
 //   bk_write   sort the stage by column (CSR order), write the row
 // Windows use the periodic Range arithmetic of common.h (a window may cover a whole line).
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "tma.h"
 
 namespace pcwd {
 
@@ -189,6 +191,128 @@ __global__ void __launch_bounds__(kB) bk_ksum_tiled(const __grid_constant__ Plan
       }
     }
   }
+}
+
+// Tiled k-sum with TMA staging (same tiling and register blocking as bk_ksum_tiled): per k, the T_k tile
+// (TR rows × SH·GZ template columns) and the v_k strip of the G windows (TR rows × SH·(GZ+G-1) columns) are
+// 3-D TMA boxes (kt_box_n / kt_box_q) issued by one thread into a ring of NST stage buffers, completion on
+// an mbarrier per buffer — no per-thread copy or address arithmetic in the k loop.  v is read from its
+// periodic extension (launch_wrap_v), so a strip that crosses the torus seam is still a run of TMA boxes.
+template <typename Real, int LEV, int G, int GZ>
+__global__ void __launch_bounds__(kB) bk_ksum_tma(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
+                                                  int ntile1) {
+  constexpr int SH = 1 << LEV;
+  constexpr int TR = kB / SH;
+  constexpr int RB = int(sizeof(Real)), VW = 16 / RB;
+  constexpr int QT0 = GZ, QV0 = GZ + G - 1;
+  constexpr int NTB = kt_box_n(SH, QT0), QT = kt_box_q(SH, QT0, NTB);
+  constexpr int NVB = kt_vbox_n(SH, QV0, RB), QV = kt_vbox_q(SH, QV0, NVB, RB);
+  constexpr int VBW = SH * QV + kt_vpadx(SH, RB);            // v box width (row pitch in shared memory)
+  constexpr int TBOX = TR * SH * QT;                          // elements per box (TMA destinations: 128-byte aligned)
+  constexpr int VBOX = (TR * VBW + 128 / RB - 1) / (128 / RB) * (128 / RB);
+  constexpr int STAGE = NTB * TBOX + NVB * VBOX;
+  constexpr int NST = 3;
+  extern __shared__ __align__(16) unsigned char ktm[];
+  __shared__ unsigned long long full[NST];
+  Real* stg = reinterpret_cast<Real*>(ktm + ((128 - (smem_u32(ktm) & 127)) & 127));
+  const int tid = threadIdx.x;
+  const int n = P.n, mask = n - 1;
+  const int64_t ug = A.u0 + int64_t(blockIdx.y) * G;
+  const UnitPos up = unit_pos(P, ug);
+  const SubBand& S = P.sb[up.sbi];
+  const int R0 = S.tW[0], R1 = S.tW[1];
+  const int t0 = blockIdx.x / ntile1, t1 = blockIdx.x - t0 * ntile1;
+  const int z0 = t0 * TR, zc = t1 * SH * GZ;
+  const int yr = ((up.p0 << LEV) + S.tSu[0] + z0) & mask;              // first v row of the tile
+  const int xc = ((up.p1 << LEV) + S.tSu[1] + zc) & mask;              // first v column of the strip
+  const int sh = xc & (VW - 1), xa = xc - sh;                          // 16-byte aligned box start
+  // each v box starts at its own wrapped column; the periodic extension (kt_vh × kt_vw ≥ (n + TR) × (n + VBW))
+  // makes every box one TMA copy, wherever the strip crosses the torus seam
+  const bool tma_v = yr + TR <= A.kt_vh && VBW <= A.kt_vw - n && !(A.kt_flags & 1);
+  const CUtensorMap* tmT = &A.tmT[up.sbi - A.kt_sb_first];
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const Real* __restrict__ v = reinterpret_cast<const Real*>(A.v);
+  auto issue = [&](int k) {
+    if (k < P.m) {
+      Real* b = stg + (k % NST) * STAGE;
+      if (tid == 0) {
+        mbar_expect_tx(&full[k % NST], unsigned(RB) * (NTB * TBOX + (tma_v ? NVB * TR * VBW : 0)));   // bytes of the boxes
+#pragma unroll
+        for (int j = 0; j < NTB; ++j) tma_load_3d(b + j * TBOX, tmT, zc + j * SH * QT, z0, k, &full[k % NST]);
+        if (tma_v) {
+#pragma unroll
+          for (int j = 0; j < NVB; ++j)
+            tma_load_3d(b + NTB * TBOX + j * VBOX, &A.tmV, (xa + j * SH * QV) & mask, yr, k, &full[k % NST]);
+        }
+      }
+      if (!tma_v) {   // strip across the torus seam: element copies into the same layout
+        const Real* vk = v + int64_t(k) * P.N;
+        Real* vb = b + NTB * TBOX;
+        for (int i = tid; i < TR * SH * QV0; i += kB) {
+          const int r = i / (SH * QV0), c = i - r * (SH * QV0);
+          cp_async_el(vb + (c / (SH * QV)) * VBOX + r * VBW + sh + c % (SH * QV),
+                      vk + int64_t((yr + r) & mask) * n + ((xc + c) & mask));
+        }
+      }
+    }
+    if (!tma_v) asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int q = 0; q < NST - 1; ++q) issue(q);
+  const int r = tid / SH, res = tid - r * SH;
+  const int offT = r * SH * QT + res, offV = r * VBW + sh + res;
+  Real acc[G][GZ];
+#pragma unroll
+  for (int u = 0; u < G; ++u)
+#pragma unroll
+    for (int i = 0; i < GZ; ++i) acc[u][i] = Real(0);
+  for (int k = 0; k < P.m; ++k) {
+    issue(k + NST - 1);
+    mbar_wait(&full[k % NST], unsigned(k / NST) & 1u);
+    if (!tma_v) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(NST - 1) : "memory");
+      __syncthreads();
+    }
+    const Real* Tb = stg + (k % NST) * STAGE;
+    const Real* Vb = Tb + NTB * TBOX;
+    Real tv[GZ];
+#pragma unroll
+    for (int i = 0; i < GZ; ++i) tv[i] = Tb[(i / QT) * TBOX + SH * (i % QT) + offT];
+#pragma unroll
+    for (int mm = 0; mm < QV0; ++mm) {
+      const Real vm = Vb[(mm / QV) * VBOX + SH * (mm % QV) + offV];
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int i = mm - u;
+        if (i >= 0 && i < GZ) acc[u][i] = fmaB(vm, tv[i], acc[u][i]);
+      }
+    }
+    __syncthreads();   // the buffer of k is refilled by issue(k + NST) at the next iteration
+  }
+  if (z0 + r < R0) {
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      Real* X0 = reinterpret_cast<Real*>(A.scratch) + (ug + u - A.u0) * A.stride + S.offX0 + int64_t(z0 + r) * rstride(R1);
+#pragma unroll
+      for (int i = 0; i < GZ; ++i) {
+        const int z = zc + res + SH * i;
+        if (z < R1) X0[z] = acc[u][i];
+      }
+    }
+  }
+}
+
+template <typename Real, int LEV, int G, int GZ>
+constexpr size_t ksum_tma_smem() {
+  constexpr int SH = 1 << LEV, TR = kB / SH, RB = int(sizeof(Real));
+  constexpr int NTB = kt_box_n(SH, GZ), QT = kt_box_q(SH, GZ, NTB);
+  constexpr int NVB = kt_vbox_n(SH, GZ + G - 1, RB), QV = kt_vbox_q(SH, GZ + G - 1, NVB, RB);
+  constexpr int VBOX = (TR * (SH * QV + kt_vpadx(SH, RB)) + 128 / RB - 1) / (128 / RB) * (128 / RB);
+  return sizeof(Real) * 3 * size_t(NTB * TR * SH * QT + NVB * VBOX) + 128;
 }
 
 // Tiled k-sum for windows covering the whole torus on both axes (coarsest levels): the window is the torus,
@@ -652,23 +776,37 @@ static void launch_tiled_t(const Plan& P, const BatchArgs& A, dim3 grid, int nti
   k<<<grid, kB, smem, st>>>(P, A, ntile1);
 }
 
-template <typename Real>
-static bool launch_ksum_tiled(const Plan& P, const BatchArgs& A, int nb, cudaStream_t st) {
-  constexpr int G = sizeof(Real) == 4 ? 8 : 4;
-  if (getenv("PCWD_NO_TILED_KSUM")) return false;
-  const int s0 = find_subband_host(P, A.u0), s1 = find_subband_host(P, A.u1 - 1);
+template <typename Real, int LEV, int G, int GZ>
+static void launch_tma_t(const Plan& P, const BatchArgs& A, dim3 grid, int ntile1, cudaStream_t st) {
+  constexpr size_t smem = ksum_tma_smem<Real, LEV, G, GZ>();
+  auto k = bk_ksum_tma<Real, LEV, G, GZ>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  BatchArgs B = A;
+  B.kt_flags = getenv("PCWD_KT_FLAGS") ? atoi(getenv("PCWD_KT_FLAGS")) : 0;
+  if (getenv("PCWD_KT_LEVMASK") && !((atoi(getenv("PCWD_KT_LEVMASK")) >> LEV) & 1)) B.kt_flags |= 1;
+  k<<<grid, kB, smem, st>>>(P, B, ntile1);
+}
+
+int ksum_tiled_gz(const Plan& P, int64_t u0, int64_t u1, int real_bytes) {
+  const int G = kt_units(real_bytes);
+  if (getenv("PCWD_NO_TILED_KSUM") || u1 <= u0) return 0;
+  const int s0 = find_subband_host(P, u0), s1 = find_subband_host(P, u1 - 1);
   const SubBand& S = P.sb[s0];
   const int lev = S.level;
-  if (lev < 3 || lev > 7 || S.nl % G || nb % G || (A.u0 - S.offset) % G) return false;
+  if (lev < 3 || lev > 7 || S.nl % G || (u0 - S.offset) % G || (u1 - u0) % G) return 0;
   for (int q = s0; q <= s1; ++q)
     if (P.sb[q].level != lev || P.sb[q].tW[0] >= P.n || P.sb[q].tW[1] >= P.n || P.sb[q].tW[0] != S.tW[0] ||
         P.sb[q].tW[1] != S.tW[1] || P.sb[q].e == 0)
-      return false;
-  // template columns per thread: the GZ ∈ {4, ..., 10} (fp64: {2, 4}) whose tiles waste the fewest columns
-  const int SH = 1 << lev, TR = kB / SH;
+      return 0;
+  // template column groups per thread: the GZ ∈ {4, ..., 10} (fp64: {2, 4}) whose tiles waste the fewest columns
+  const int SH = 1 << lev;
   const int cand_f[] = {8, 9, 10, 6, 5, 4}, cand_d[] = {4, 2};
-  const int* cand = sizeof(Real) == 4 ? cand_f : cand_d;
-  const int ncand = sizeof(Real) == 4 ? 6 : 2;
+  const int* cand = real_bytes == 4 ? cand_f : cand_d;
+  const int ncand = real_bytes == 4 ? 6 : 2;
   int GZ = cand[0];
   int64_t best = -1;
   for (int c = 0; c < ncand; ++c) {
@@ -676,9 +814,27 @@ static bool launch_ksum_tiled(const Plan& P, const BatchArgs& A, int nb, cudaStr
     const int64_t cost = int64_t(nt) * (tw + SH * (G - 1));   // staged v columns per tile row ≈ traffic + work
     if (best < 0 || cost < best) { best = cost; GZ = cand[c]; }
   }
+  return GZ;
+}
+
+template <typename Real>
+static bool launch_ksum_tiled(const Plan& P, const BatchArgs& A, int nb, cudaStream_t st) {
+  constexpr int G = sizeof(Real) == 4 ? 8 : 4;
+  static_assert(G == kt_units(int(sizeof(Real))), "G");
+  const int GZ = ksum_tiled_gz(P, A.u0, A.u1, int(sizeof(Real)));
+  if (!GZ || nb % G) return false;
+  const SubBand& S = P.sb[find_subband_host(P, A.u0)];
+  const int lev = S.level, SH = 1 << lev, TR = kB / SH;
   const int ntile0 = (S.tW[0] + TR - 1) / TR, ntile1 = (S.tW[1] + SH * GZ - 1) / (SH * GZ);
   const dim3 grid(ntile0 * ntile1, nb / G);
-#define PCWD_KT(L, Z) if (lev == L && GZ == Z) { launch_tiled_t<Real, L, G, Z>(P, A, grid, ntile1, st); return true; }
+  static const bool no_tma = getenv("PCWD_NO_TMA_KSUM") != nullptr;
+  const bool tma = A.kt_gz == GZ && !no_tma;
+#define PCWD_KT(L, Z)                                                                   \
+  if (lev == L && GZ == Z) {                                                            \
+    if (tma) launch_tma_t<Real, L, G, Z>(P, A, grid, ntile1, st);                       \
+    else launch_tiled_t<Real, L, G, Z>(P, A, grid, ntile1, st);                         \
+    return true;                                                                        \
+  }
   if constexpr (sizeof(Real) == 4) {
     PCWD_KT(3, 8) PCWD_KT(3, 9) PCWD_KT(3, 10) PCWD_KT(3, 6) PCWD_KT(3, 5) PCWD_KT(3, 4)
     PCWD_KT(4, 8) PCWD_KT(4, 9) PCWD_KT(4, 10) PCWD_KT(4, 6) PCWD_KT(4, 5) PCWD_KT(4, 4)

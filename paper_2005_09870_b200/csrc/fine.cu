@@ -5,7 +5,7 @@
 //
 //   a2 k-sum    R_j(y) = Σ_k v_k(c_j + y) T_k(y) for the GU windows at once (k-sum fused
 //               before the cascade).  T_k and the v_k strip the GU windows read are staged in shared
-//               memory by cp.async, double-buffered over k.  A thread owns one template row r and GZ
+//               memory by 3-D TMA boxes (one per k) in a ring of NST buffers (mbarrier completion).  A thread owns one template row r and GZ
 //               template columns z_i = res + 2^ℓ(zb·GZ + i) of one residue class mod 2^ℓ; unit j reads
 //               v at column z_i + 2^ℓ j = res + 2^ℓ(zb·GZ + i + j), so the GU·GZ products of one k need
 //               only GZ template values and GU+GZ-1 v values (register blocking along the shift).
@@ -23,6 +23,7 @@
 
 #include "geom.h"
 #include "kernels.cuh"
+#include "tma.h"
 
 namespace pcwd {
 
@@ -46,52 +47,6 @@ struct FVec<double> {
 
 __device__ __forceinline__ float ffma_(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double ffma_(double a, double b, double c) { return fma(a, b, c); }
-
-__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cpa4(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 1-D bulk copy global -> shared (async proxy, TMA engine); completion counted on `bar` in bytes.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-// 3-D tiled TMA load of one box of `map` at coordinates (x, y, z) into shared memory.
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void bar_group(int id, int nthreads) {
   if (nthreads == 32) __syncwarp();
@@ -208,7 +163,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
   constexpr int SH = 1 << LEV;           // window shift between adjacent units (2^ℓ)
   constexpr int VW = FVec<Real>::W;
   const int tid = threadIdx.x;
-  const int n = P.n, mask = n - 1;
   constexpr int GT = kFT / CG;           // threads per unit group in the cascade (CG units at a time)
   const int slot = tid / GT, gt = tid - slot * GT;
   Real* Rbase = sm + kSlack;

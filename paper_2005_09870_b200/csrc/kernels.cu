@@ -144,17 +144,14 @@ __global__ void tmpl_passB(const __grid_constant__ Plan P, const __grid_constant
   }
 }
 
+// Periodic extension of v: out[k][y][x] = v[k][(y - off) mod n][(x - off) mod n], y < H, x < W (row pitch W).
+// Grid (ceil(W / 256), H, m): one thread per output element, coalesced along x.
 template <typename Real>
-__global__ void pad_v_kernel(const Real* __restrict__ v, Real* __restrict__ vp, int n, int P, int m) {
-  const int w = n + 2 * P;
-  const int64_t total = int64_t(m) * w * w;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t k = i / (int64_t(w) * w);
-    const int64_t r = i - k * w * w;
-    const int y = int(r / w), x = int(r - int64_t(y) * w);
-    const int sy = ((y - P) % n + n) % n, sx = ((x - P) % n + n) % n;
-    vp[i] = v[k * int64_t(n) * n + int64_t(sy) * n + sx];
-  }
+__global__ void wrap_v_kernel(const Real* __restrict__ v, Real* __restrict__ out, int n, int off, int H, int W) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, k = blockIdx.z;
+  if (x >= W) return;
+  const int sy = (y - off + n * 4) & (n - 1), sx = (x - off + n * 4) & (n - 1);
+  out[(int64_t(k) * H + y) * W + x] = v[(int64_t(k) * n + sy) * n + sx];
 }
 
 template <typename Real>
@@ -563,9 +560,13 @@ cudaError_t launch_tmpl_level(const Plan& P, const TmplArgs& A, int real_bytes, 
 }
 
 cudaError_t launch_pad_v(const void* v, void* vpad, int n, int P, int m, int real_bytes, cudaStream_t st) {
-  const int64_t total = int64_t(m) * (n + 2 * P) * (n + 2 * P);
-  if (real_bytes == 4) pad_v_kernel<float><<<grid_for(total), kBlock, 0, st>>>((const float*)v, (float*)vpad, n, P, m);
-  else pad_v_kernel<double><<<grid_for(total), kBlock, 0, st>>>((const double*)v, (double*)vpad, n, P, m);
+  return launch_wrap_v(v, vpad, n, P, n + 2 * P, n + 2 * P, m, real_bytes, st);
+}
+
+cudaError_t launch_wrap_v(const void* v, void* out, int n, int off, int H, int W, int m, int real_bytes, cudaStream_t st) {
+  const dim3 grid((W + 255) / 256, H, m);
+  if (real_bytes == 4) wrap_v_kernel<float><<<grid, 256, 0, st>>>((const float*)v, (float*)out, n, off, H, W);
+  else wrap_v_kernel<double><<<grid, 256, 0, st>>>((const double*)v, (double*)out, n, off, H, W);
   return cudaGetLastError();
 }
 

@@ -85,7 +85,43 @@ bool fine_config(int real_bytes, int level, int L2, FineCfg* cfg);
 cudaError_t launch_fine(const Plan& P, const FineArgs& A, int real_bytes, int level, int grid, size_t smem,
                         cudaStream_t st);
 
+// Tiled k-sum (bk_ksum_tma): a tile row of Q0 column groups of width SH = 2^ℓ is staged as NB TMA boxes of
+// SH·q columns (≤ 256 elements per box dimension); q is odd for SH ≤ 16 so that the rows a warp reads fall
+// in distinct bank groups.
+constexpr int kt_box_q(int SH, int Q0, int nb) {
+  int q = (Q0 + nb - 1) / nb;
+  if (SH <= 16 && q % 2 == 0) ++q;
+  return q;
+}
+constexpr int kt_box_n(int SH, int Q0) {
+  int nb = 1;
+  while (SH * kt_box_q(SH, Q0, nb) > 256) ++nb;
+  return nb;
+}
+constexpr int kt_units(int real_bytes) { return real_bytes == 4 ? 8 : 4; }   // G: units per tiled k-sum group
+// The v strip starts at an arbitrary column but a TMA box must start on a 16-byte boundary: each v box covers
+// SH·q columns from an aligned-down start plus kt_vpadx extra columns (the shift and bank padding): SH
+// for SH ≤ 16 with q even (fp32: a warp reads 32/SH rows, a row pitch ≡ SH mod 2SH keeps them in distinct
+// banks), else one 16-byte vector.
+constexpr int kt_vpadx(int SH, int rb) { return rb == 8 ? 2 : (SH <= 16 ? SH : 4); }
+constexpr int kt_vbox_q(int SH, int Q0, int nb, int rb) {
+  int q = (Q0 + nb - 1) / nb;
+  if (rb == 4 && SH <= 16 && q % 2 == 1) ++q;
+  return q;
+}
+constexpr int kt_vbox_n(int SH, int Q0, int rb) {
+  int nb = 1;
+  while (SH * kt_vbox_q(SH, Q0, nb, rb) + kt_vpadx(SH, rb) > 256) ++nb;
+  return nb;
+}
+
 struct BatchArgs {
+  CUtensorMap tmV;          // tiled k-sum: TMA map of v (3-D: x, y, k), box (SH·qV + kt_vpadx) × TR × 1
+  CUtensorMap tmT[3];       // tiled k-sum: TMA maps of the level's templates, box SH·qT × TR × 1
+  int kt_gz;                // tiled k-sum: template column groups per thread (0 ⇒ not planned)
+  int kt_sb_first;          // tiled k-sum: sub-band of tmT[0]
+  int kt_flags;             // tiled k-sum debug: 1 = v strips by cp.async only
+  int kt_vh, kt_vw;         // tiled k-sum: rows / columns of the periodically extended v that tmV maps
   const void* v;
   const void* T;
   const int4* stencil;      // .w = level of the partner sub-band
@@ -97,6 +133,10 @@ struct BatchArgs {
   int32_t* col;
   void* val;
 };
+
+// Template column groups per thread (GZ) of the tiled k-sum for the batched launch over [u0, u1), 0 when the
+// tiled k-sum does not apply (host; api.cu encodes the TMA maps from it).
+int ksum_tiled_gz(const Plan& P, int64_t u0, int64_t u1, int real_bytes);
 
 cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, const int64_t* workA,
                                 const int64_t* workB, const int64_t* appr0, const int64_t* appr1, int steps,
@@ -125,6 +165,8 @@ cudaError_t launch_support_check(const double* u, int64_t total, int n, int d, c
                                  int* flag, cudaStream_t st);
 // K1: v_pad[k][y][x] = v[k][(y - P) mod n][(x - P) mod n], side n + 2P (compute type)
 cudaError_t launch_pad_v(const void* v, void* vpad, int n, int P, int m, int real_bytes, cudaStream_t st);
+// out[k][y][x] = v[k][(y - off) mod n][(x - off) mod n] for y < H, x < W (off ≤ 4n; n a power of two).
+cudaError_t launch_wrap_v(const void* v, void* out, int n, int off, int H, int W, int m, int real_bytes, cudaStream_t st);
 cudaError_t launch_units(const Plan& P, const UnitArgs& A, int mode, int real_bytes, int out_bytes,
                          int grid, size_t smem, cudaStream_t st);
 size_t unit_smem_limit();
