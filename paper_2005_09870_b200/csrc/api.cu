@@ -51,6 +51,7 @@ struct Handle {
   FGeom* fgeom_d = nullptr;
   void* vpad_d = nullptr;   // periodically padded v (fine path TMA source)
   void* vwrap_d = nullptr;  // v extended periodically by kt_pr rows / kt_pc columns (tiled k-sum TMA source)
+  CUtensorMap* amaps_d = nullptr;   // TMA maps of the batched approximation steps
   int kt_pr = 0, kt_pc = 0;
   int vpad = 0;
   void* gscratch = nullptr;
@@ -110,7 +111,7 @@ bool is_device_ptr(const void* p) {
 }
 
 void free_all(Handle* h) {
-  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->vwrap_d, h->gscratch, h->bscratch,
+  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->vwrap_d, h->amaps_d, h->gscratch, h->bscratch,
                   h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->ustage, h->vstage, h->flag_d};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -821,6 +822,26 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         B.ba.kt_gz = gz;
         B.ba.kt_sb_first = s;
       }
+      B.ba.kt_sb_first = s;
+      // approximation steps on the TMA path: every participating sub-band's step-s input window has one size
+      // over its units and stays clear of wrapping (maps encoded once the scratch exists)
+      for (int st = 1; st <= steps && st < 32; ++st) {
+        bool ok = e - s <= 4 && !getenv("PCWD_NO_TMA_APPROX");
+        for (int q = s; q < e && ok; ++q) {
+          const SubBand& Sq = P.sb[q];
+          if (!(st < Sq.steps || st == P.J)) continue;
+          for (int a = 0; a < 2 && ok; ++a) {
+            int len = -1;
+            for (int p = 0; p < Sq.nl && ok; ++p) {
+              Range w = unit_window(P, Sq, a, p);
+              for (int t = 1; t < st; ++t) w = step_out(w, P.L2, 0);
+              ok = (len < 0 || w.len == len) && w.len + 2 * P.L2 <= w.nl;
+              len = w.len;
+            }
+          }
+        }
+        if (ok) B.ba.am_steps |= 1u << st;
+      }
       h->bscratch_bytes = std::max(h->bscratch_bytes, size_t(batch) * stride * rb);
       h->launches.push_back(B);
       s = e;
@@ -830,6 +851,36 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     s = e;
   }
   if (h->bscratch_bytes) CKB(dalloc(&h->bscratch, h->bscratch_bytes + 1024));   // + vector over-read slack
+  {  // TMA maps of the approximation steps: [launch][step - 1][sub-band - first] over the scratch input buffer
+    std::vector<CUtensorMap> maps;
+    std::vector<size_t> first;
+    for (Launch& L : h->launches) {
+      first.push_back(maps.size());
+      if (!L.batched || !L.ba.am_steps) continue;
+      maps.resize(maps.size() + 32 * 4);
+      CUtensorMap* M = maps.data() + first.back();
+      const int TI = ap_ti(rb, P.L2), BW = ap_bw(rb, P.L2);
+      for (int st = 1; st < 32; ++st) {
+        if (!((L.ba.am_steps >> st) & 1u)) continue;
+        for (int q = L.ba.kt_sb_first, i = 0; q < P.nsb && i < 4 && P.sb[q].offset < L.u1; ++q, ++i) {
+          const SubBand& Sq = P.sb[q];
+          if (!(st < Sq.steps || st == P.J)) continue;
+          Range w0 = unit_window(P, Sq, 0, 0), w1 = unit_window(P, Sq, 1, 0);
+          for (int t = 1; t < st; ++t) { w0 = step_out(w0, P.L2, 0); w1 = step_out(w1, P.L2, 0); }
+          char* base = static_cast<char*>(h->bscratch) + ((st & 1) ? Sq.offX0 : Sq.offX1) * rb;
+          const int rc2 = encode_map3(&M[(st - 1) * 4 + i], base, rb, w1.len, w0.len, L.ba.batch, (w1.len + 3) & ~3,
+                                      L.ba.stride, BW, TI);
+          if (rc2) return bail(PCWD_E_CUDA, "cuTensorMapEncodeTiled (approximation) failed: " + std::to_string(rc2));
+        }
+      }
+    }
+    if (!maps.empty()) {
+      CKB(dalloc(&h->amaps_d, maps.size() * sizeof(CUtensorMap)));
+      CKB(cudaMemcpy(h->amaps_d, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+      for (size_t i = 0; i < h->launches.size(); ++i)
+        if (h->launches[i].batched && h->launches[i].ba.am_steps) h->launches[i].ba.amaps = h->amaps_d + first[i];
+    }
+  }
   if (h->kt_pc > 0) {   // v extended periodically by kt_pr rows and kt_pc columns: every k-sum v box is one TMA copy
     h->kt_pc = (h->kt_pc + 31) / 32 * 32;
     const int H = P.n + h->kt_pr, W = P.n + h->kt_pc;

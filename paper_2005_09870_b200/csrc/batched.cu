@@ -623,6 +623,139 @@ __global__ void __launch_bounds__(kB) bk_approx(const __grid_constant__ Plan P, 
   }
 }
 
+// Approximation step s with TMA tile loads, for steps whose input windows have one size across the launch's
+// units and do not wrap (api.cu plans a 3-D tensor map per step and sub-band over the scratch buffer:
+// columns × rows × unit slot).  A CTA computes `tpc` output tiles (TO × TO) of one unit; each input tile
+// (TI rows × BW columns from a 16-byte aligned column, window outside read as zero by the TMA unit) lands in a
+// double-buffered stage.  Axis 0 first (column-fastest tasks: conflict-free on the TMA row pitch), into Zs
+// (odd pitch), then axis 1 (row-fastest tasks), 4 outputs per task, 16-byte stores (h taps only).
+template <typename Real, int L2, int TO>
+__global__ void __launch_bounds__(kB) bk_approx_tma(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
+                                                    int s, int ntx, int ntiles, int tpc) {
+  constexpr int RB = int(sizeof(Real)), VW = 16 / RB;
+  constexpr int TI = 2 * (TO - 1) + L2;                     // input rows / columns per tile
+  constexpr int BW = (TI + VW - 1 + VW - 1) / VW * VW;      // box width: aligned start + shift
+  constexpr int XSZ = (TI * BW + 128 / RB - 1) / (128 / RB) * (128 / RB);
+  constexpr int ZP = TI | 1;                                 // odd pitch of the axis-0 output
+  constexpr int NI = 2 * 3 + L2;                             // inputs of 4 consecutive outputs
+  extern __shared__ __align__(16) unsigned char atm[];
+  __shared__ unsigned long long full[2];
+  Real* Xs = reinterpret_cast<Real*>(atm + ((128 - (smem_u32(atm) & 127)) & 127));
+  Real* Zs = Xs + 2 * XSZ;
+  const int tid = threadIdx.x;
+  const int64_t unit = A.u0 + blockIdx.y;
+  const UnitPos up = unit_pos(P, unit);
+  const SubBand& S = P.sb[up.sbi];
+  if (!(s < S.steps || s == P.J)) return;
+  Range in0, in1;
+  step_in(P, S, up, s, in0, in1);
+  const Range a0 = step_out(in0, L2, 0), a1 = step_out(in1, L2, 0);
+  const int nty = (a0.len + TO - 1) / TO, ntxu = (a1.len + TO - 1) / TO;   // this unit's tiles
+  const int t_first = blockIdx.x * tpc;
+  const int t_last = min(t_first + tpc, nty * ntxu);
+  if (t_first >= t_last) return;
+  (void)ntx;
+  (void)ntiles;
+  const CUtensorMap* map = A.amaps + (s - 1) * 4 + (up.sbi - A.kt_sb_first);
+  Real* Xn = reinterpret_cast<Real*>(A.scratch) + int64_t(blockIdx.y) * A.stride + ((s & 1) ? S.offX1 : S.offX0);
+  const int rso = rstride(a1.len);
+  // signed offset of input position g from the window start (g within L2 before the window .. its end)
+  auto sdiff = [](int g, const Range& r) {
+    int d = (g - r.lo) & (r.nl - 1);
+    return d >= r.nl - 2 * L2 ? d - r.nl : d;
+  };
+  auto tile_org = [&](int t, int& d0, int& xs, int& sh, int& j0, int& k0) {
+    const int ty = t / ntxu, tx = t - ty * ntxu;
+    j0 = ty * TO;
+    k0 = tx * TO;
+    d0 = sdiff(2 * (a0.lo + j0), in0);
+    const int d1 = sdiff(2 * (a1.lo + k0), in1);
+    sh = d1 & (VW - 1);
+    xs = d1 - sh;
+  };
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int t, int b) {
+    if (tid == 0 && t < t_last) {
+      int d0, xs, sh, j0, k0;
+      tile_org(t, d0, xs, sh, j0, k0);
+      mbar_expect_tx(&full[b], unsigned(RB * TI * BW));
+      tma_load_3d(Xs + b * XSZ, map, xs, d0, int(blockIdx.y), &full[b]);
+    }
+  };
+  issue(t_first, 0);
+  issue(t_first + 1, 1);
+  for (int t = t_first, it = 0; t < t_last; ++t, ++it) {
+    const int b = it & 1;
+    int d0, xs, sh, j0, k0;
+    tile_org(t, d0, xs, sh, j0, k0);
+    mbar_wait(&full[b], unsigned(it >> 1) & 1u);
+    const Real* X = Xs + b * XSZ;
+    // axis 0: Zs[4jq + q][c] = Σ_t h[t] X[8jq + 2q + t][sh + c]
+    for (int idx = tid; idx < TI * (TO / 4); idx += kB) {
+      const int jq = idx / TI, c = idx - jq * TI;
+      Real x[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) x[i] = X[(8 * jq + i) * BW + sh + c];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        Real acc = Real(0);
+#pragma unroll
+        for (int tt = 0; tt < L2; ++tt) acc = fmaB(TapsOf<Real>::get(P, 0, tt), x[2 * q + tt], acc);
+        Zs[(4 * jq + q) * ZP + c] = acc;
+      }
+    }
+    __syncthreads();   // Zs complete; stage b free
+    issue(t + 2, b);
+    // axis 1: out[j][4kq + q] = Σ_t h[t] Zs[j][8kq + 2q + t]
+    for (int idx = tid; idx < TO * (TO / 4); idx += kB) {
+      const int kq = idx / TO, j = idx - kq * TO;
+      if (j0 + j >= a0.len || k0 + 4 * kq >= a1.len) continue;
+      Real z[NI];
+#pragma unroll
+      for (int i = 0; i < NI; ++i) z[i] = Zs[j * ZP + 8 * kq + i];
+      Real o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        Real acc = Real(0);
+#pragma unroll
+        for (int tt = 0; tt < L2; ++tt) acc = fmaB(TapsOf<Real>::get(P, 0, tt), z[2 * q + tt], acc);
+        o[q] = acc;
+      }
+      Real* dst = Xn + int64_t(j0 + j) * rso + k0 + 4 * kq;   // rso is a multiple of 4: the row has room
+      if constexpr (sizeof(Real) == 4) {
+        *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+      } else {
+        reinterpret_cast<double2*>(dst)[0] = make_double2(o[0], o[1]);
+        reinterpret_cast<double2*>(dst)[1] = make_double2(o[2], o[3]);
+      }
+    }
+    __syncthreads();   // Zs reused by the next tile
+  }
+}
+
+template <typename Real, int L2, int TO>
+static void launch_approx_tma_t(const Plan& P, const BatchArgs& A, int s, int ntx, int nty, int nb, cudaStream_t st) {
+  constexpr int RB = int(sizeof(Real)), VW = 16 / RB;
+  constexpr int TI = 2 * (TO - 1) + L2;
+  constexpr int BW = (TI + VW - 1 + VW - 1) / VW * VW;
+  constexpr int XSZ = (TI * BW + 128 / RB - 1) / (128 / RB) * (128 / RB);
+  constexpr size_t smem = size_t(RB) * (2 * XSZ + TO * (TI | 1)) + 128;
+  auto k = bk_approx_tma<Real, L2, TO>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = true;
+  }
+  const int ntiles = ntx * nty;
+  const int tpc = ntiles <= 4 ? ntiles : (ntiles <= 16 ? 4 : 6);
+  k<<<dim3((ntiles + tpc - 1) / tpc, nb), kB, smem, st>>>(P, A, s, ntx, ntiles, tpc);
+}
+
 template <typename Real, int TO>
 static void launch_approx_to(const Plan& P, const BatchArgs& A, int s, dim3 grid, int ntx, cudaStream_t st) {
   switch (P.L2) {
@@ -640,6 +773,20 @@ static void launch_approx_to(const Plan& P, const BatchArgs& A, int s, dim3 grid
 template <typename Real>
 static void launch_approx(const Plan& P, const BatchArgs& A, int s, int64_t maxA0, int64_t maxA1, int nb,
                           cudaStream_t st) {
+  static const bool no_tma = getenv("PCWD_NO_TMA_APPROX") != nullptr;
+  if (A.amaps && ((A.am_steps >> s) & 1u) && !no_tma) {
+    constexpr int TO = sizeof(Real) == 4 ? 32 : 16;
+    const int ntx = int((maxA1 + TO - 1) / TO), nty = int((maxA0 + TO - 1) / TO);
+    switch (P.L2) {
+      case 2: launch_approx_tma_t<Real, 2, TO>(P, A, s, ntx, nty, nb, st); return;
+      case 4: launch_approx_tma_t<Real, 4, TO>(P, A, s, ntx, nty, nb, st); return;
+      case 6: launch_approx_tma_t<Real, 6, TO>(P, A, s, ntx, nty, nb, st); return;
+      case 8: launch_approx_tma_t<Real, 8, TO>(P, A, s, ntx, nty, nb, st); return;
+      case 10: launch_approx_tma_t<Real, 10, TO>(P, A, s, ntx, nty, nb, st); return;
+      case 12: launch_approx_tma_t<Real, 12, TO>(P, A, s, ntx, nty, nb, st); return;
+      default: break;
+    }
+  }
   if (P.L2 > 12 || (P.L2 & 1)) {
     auto gx = [](int64_t elems) { return int(std::max<int64_t>(1, std::min<int64_t>((elems + kB - 1) / kB, 64))); };
     bk_passA<Real><<<dim3(gx(maxA0 * 2 * maxA1 / 4 + 1), nb), kB, 0, st>>>(P, A, s);

@@ -122,6 +122,8 @@ struct BatchArgs {
   int kt_sb_first;          // tiled k-sum: sub-band of tmT[0]
   int kt_flags;             // tiled k-sum debug: 1 = v strips by cp.async only
   int kt_vh, kt_vw;         // tiled k-sum: rows / columns of the periodically extended v that tmV maps
+  const CUtensorMap* amaps; // approximation steps: device array [step - 1][sub-band - kt_sb_first] of TMA maps
+  unsigned am_steps;        // bit s: step s of every sub-band of the launch has a map (bk_approx_tma)
   const void* v;
   const void* T;
   const int4* stencil;      // .w = level of the partner sub-band
@@ -137,6 +139,10 @@ struct BatchArgs {
 // Template column groups per thread (GZ) of the tiled k-sum for the batched launch over [u0, u1), 0 when the
 // tiled k-sum does not apply (host; api.cu encodes the TMA maps from it).
 int ksum_tiled_gz(const Plan& P, int64_t u0, int64_t u1, int real_bytes);
+// Tile side / input box of bk_approx_tma (TO outputs, TI × BW input box) for the compute type.
+constexpr int ap_to(int rb) { return rb == 4 ? 32 : 16; }
+constexpr int ap_ti(int rb, int L2) { return 2 * (ap_to(rb) - 1) + L2; }
+constexpr int ap_bw(int rb, int L2) { return (ap_ti(rb, L2) + 16 / rb - 1 + 16 / rb - 1) / (16 / rb) * (16 / rb); }
 
 cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, const int64_t* workA,
                                 const int64_t* workB, const int64_t* appr0, const int64_t* appr1, int steps,
