@@ -87,6 +87,8 @@ struct Handle {
   int64_t rows() const { return hp.row1 - hp.row0; }
 };
 
+inline bool L2OK(int L2) { return L2 >= 2 && L2 <= 12 && L2 % 2 == 0; }
+
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
@@ -841,6 +843,15 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           }
         }
         if (ok) B.ba.am_steps |= 1u << st;
+      }
+      // per-unit tail: from the first step ≥ 3 (measured best on c5) whose input window, pass-A output and
+      // approximation fit in 64 KB
+      if (L2OK(P.L2)) {
+        static const int smin = getenv("PCWD_TAIL_S0_MIN") ? atoi(getenv("PCWD_TAIL_S0_MIN")) : 3;
+        for (int st = std::max(2, smin); st <= steps; ++st) {
+          const int64_t am = (B.appr0[st - 1] * B.appr1[st - 1] + 3) & ~int64_t(3);
+          if ((2 * am + B.appr0[st - 1] * B.appr1[st]) * rb <= 64 * 1024) { B.ba.tail_s0 = st; break; }
+        }
       }
       h->bscratch_bytes = std::max(h->bscratch_bytes, size_t(batch) * stride * rb);
       h->launches.push_back(B);

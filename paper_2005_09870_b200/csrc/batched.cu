@@ -905,6 +905,174 @@ __global__ void __launch_bounds__(kB) bk_write(const __grid_constant__ Plan P, c
   }
 }
 
+// Tail of the cascade of one unit (one CTA per unit), steps s0 .. steps in shared memory: the step-s0 input
+// window is read once from the scratch; each step computes its approximation (axis 1 then axis 0, periodic
+// windows through local_index) and the stencil entries of its level — details directly from the step
+// input (2δ × 2δ taps), the coarse block from the approximation (as bk_gather) — then the row (entries of the
+// earlier steps from the stage in the scratch) is sorted by column and written (as bk_write).
+template <typename Real, int L2>
+__global__ void __launch_bounds__(kB) bk_tail(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
+                                              int s0, int steps, int amax, int ymax) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  const int Lp = P.band_Lpad;
+  int* kc = reinterpret_cast<int*>(tsm);
+  Real* kv = reinterpret_cast<Real*>(tsm + ((Lp * 4 + 15) & ~15));
+  Real* buf0 = kv + ((Lp + 3) & ~3);
+  Real* buf1 = buf0 + amax;
+  Real* Ys = buf1 + amax;
+  const int tid = threadIdx.x;
+  const int64_t unit = A.u0 + blockIdx.x;
+  const UnitPos up = unit_pos(P, unit);
+  const SubBand& S = P.sb[up.sbi];
+  const Real* base = reinterpret_cast<const Real*>(A.scratch) + int64_t(blockIdx.x) * A.stride;
+  Range in0, in1;
+  step_in(P, S, up, s0, in0, in1);
+  {  // step-s0 input window
+    const Real* X = base + ((s0 & 1) ? S.offX0 : S.offX1);
+    const int rs = rstride(in1.len);
+    for (int i = tid; i < in0.len * in1.len; i += kB) {
+      const int r = i / in1.len, c = i - r * in1.len;
+      buf0[i] = X[int64_t(r) * rs + c];
+    }
+  }
+  // stage: entries of the steps before s0 come from bk_gather (scratch), the rest are computed below
+  const Real* sv = base + S.offStage;
+  const int* sc = reinterpret_cast<const int*>(sv + Lp);
+  const int4* st = A.stencil + S.stencil_off;
+  for (int j = tid; j < Lp; j += kB) {
+    if (j >= P.band_L) { kc[j] = INT_MAX; kv[j] = Real(0); }
+    else if (st[j].w < s0) { kc[j] = sc[j]; kv[j] = sv[j]; }
+  }
+  __syncthreads();
+  Real* X = buf0;
+  Real* Xn = buf1;
+  for (int s = s0; s <= steps; ++s) {
+    const bool appr = s < S.steps || s == P.J;
+    const Range a0 = step_out(in0, L2, 0), a1 = step_out(in1, L2, 0);
+    if (appr) {
+      // a window clear of wrapping (len + 2·2δ ≤ line) is addressed by a signed offset from its start; a
+      // whole-line window wraps modulo the line; otherwise local_index per tap
+      auto kind = [](const Range& r) { return r.len >= r.nl ? 1 : (r.len + 2 * L2 <= r.nl ? 0 : 2); };
+      auto sdiff = [](int g, const Range& r) {
+        int d = (g - r.lo) & (r.nl - 1);
+        return d >= r.nl - 2 * L2 ? d - r.nl : d;
+      };
+      const int k1 = kind(in1), k0 = kind(in0);
+      // axis 1: Ys[i0][l1] = Σ_t h[t] X[i0][2(a1.lo + l1) + t]
+      for (int i = tid; i < in0.len * a1.len; i += kB) {
+        const int i0 = i / a1.len, l1 = i - i0 * a1.len;
+        const int g = 2 * (a1.lo + l1);
+        const Real* xr = X + i0 * in1.len;
+        Real acc = Real(0);
+        if (k1 == 0) {
+          const int d = sdiff(g, in1);
+#pragma unroll
+          for (int t = 0; t < L2; ++t)
+            if (unsigned(d + t) < unsigned(in1.len)) acc = fmaB(TapsOf<Real>::get(P, 0, t), xr[d + t], acc);
+        } else if (k1 == 1) {
+#pragma unroll
+          for (int t = 0; t < L2; ++t) acc = fmaB(TapsOf<Real>::get(P, 0, t), xr[(g + t - in1.lo) & (in1.nl - 1)], acc);
+        } else {
+#pragma unroll
+          for (int t = 0; t < L2; ++t) {
+            const int c = local_index(in1, g + t);
+            if (c >= 0) acc = fmaB(TapsOf<Real>::get(P, 0, t), xr[c], acc);
+          }
+        }
+        Ys[i] = acc;
+      }
+      __syncthreads();
+      // axis 0: Xn[l0][l1] = Σ_t h[t] Ys[2(a0.lo + l0) + t][l1]
+      for (int i = tid; i < a0.len * a1.len; i += kB) {
+        const int l0 = i / a1.len, l1 = i - l0 * a1.len;
+        const int g = 2 * (a0.lo + l0);
+        const Real* yc = Ys + l1;
+        Real acc = Real(0);
+        if (k0 == 0) {
+          const int d = sdiff(g, in0);
+#pragma unroll
+          for (int t = 0; t < L2; ++t)
+            if (unsigned(d + t) < unsigned(in0.len)) acc = fmaB(TapsOf<Real>::get(P, 0, t), yc[(d + t) * a1.len], acc);
+        } else if (k0 == 1) {
+#pragma unroll
+          for (int t = 0; t < L2; ++t)
+            acc = fmaB(TapsOf<Real>::get(P, 0, t), yc[((g + t - in0.lo) & (in0.nl - 1)) * a1.len], acc);
+        } else {
+#pragma unroll
+          for (int t = 0; t < L2; ++t) {
+            const int r = local_index(in0, g + t);
+            if (r >= 0) acc = fmaB(TapsOf<Real>::get(P, 0, t), yc[r * a1.len], acc);
+          }
+        }
+        Xn[i] = acc;
+      }
+      __syncthreads();
+    }
+    // stencil entries of level s
+    for (int j = tid; j < P.band_L; j += kB) {
+      const int4 e = st[j];
+      if (e.w != s) continue;
+      const SubBand& L = P.sb[e.x];
+      int b0, b1;
+      if (L.level == S.level) { b0 = up.p0; b1 = up.p1; }
+      else if (L.level < S.level) { b0 = up.p0 << (S.level - L.level); b1 = up.p1 << (S.level - L.level); }
+      else { b0 = up.p0 >> (L.level - S.level); b1 = up.p1 >> (L.level - S.level); }
+      const int l0 = (b0 + e.y) & (L.nl - 1), l1 = (b1 + e.z) & (L.nl - 1);
+      Real val = Real(0);
+      if (L.e == 0) {
+        const int li0 = local_index(a0, l0), li1 = local_index(a1, l1);
+        if (appr && li0 >= 0 && li1 >= 0) val = Xn[li0 * a1.len + li1];
+      } else {
+        const int e0 = L.e0, e1 = L.e1;
+        for (int t0 = 0; t0 < L2; ++t0) {
+          const int r = local_index(in0, 2 * l0 + P.to[e0] + t0);
+          if (r < 0) continue;
+          Real row = Real(0);
+#pragma unroll
+          for (int t1 = 0; t1 < L2; ++t1) {
+            const int c = local_index(in1, 2 * l1 + P.to[e1] + t1);
+            if (c >= 0) row = fmaB(TapsOf<Real>::get(P, e1, t1), X[r * in1.len + c], row);
+          }
+          val = fmaB(TapsOf<Real>::get(P, e0, t0), row, val);
+        }
+      }
+      kv[j] = val;
+      kc[j] = int(L.offset + int64_t(l0) * L.nl + l1);
+    }
+    __syncthreads();
+    if (appr) {
+      Real* t = X;
+      X = Xn;
+      Xn = t;
+      in0 = a0;
+      in1 = a1;
+    }
+  }
+  // bitonic sort of the row by column, CSR write (bk_write)
+  for (int k = 2; k <= Lp; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < Lp; i += kB) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up2 = (i & k) == 0;
+          const int ci = kc[i], cj = kc[ixj];
+          if ((ci > cj) == up2) {
+            kc[i] = cj; kc[ixj] = ci;
+            const Real t = kv[i]; kv[i] = kv[ixj]; kv[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int64_t row = (unit - A.row0) * P.band_L;
+  Real* outv = reinterpret_cast<Real*>(A.val);
+  for (int i = tid; i < P.band_L; i += kB) {
+    A.col[row + i] = kc[i];
+    outv[row + i] = kv[i];
+  }
+}
+
 // ----------------------------------------------------------------------------------- launcher
 
 // Tiled k-sum when every window of the launch's level stays inside one period per axis, the shift 2^ℓ is
@@ -1035,7 +1203,9 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
       bk_ksum<Real><<<dim3(gx(maxX0), nb), kB, 0, st>>>(P, A);
     ++*launches;
     static const bool old_passes = getenv("PCWD_OLD_PASSES") != nullptr;
-    for (int s = 1; s <= steps; ++s) {
+    // steps ≥ tail_s0 (windows that fit in shared memory): one per-unit kernel with the gathers and the write
+    const int s0 = A.tail_s0 > 0 && A.tail_s0 <= steps && !getenv("PCWD_NO_TAIL") ? A.tail_s0 : steps + 1;
+    for (int s = 1; s < s0; ++s) {
       if (old_passes) {
         bk_passA<Real><<<dim3(gx(workA[s]), nb), kB, 0, st>>>(P, A, s);
         bk_passB<Real><<<dim3(gx(workB[s]), nb), kB, 0, st>>>(P, A, s);
@@ -1047,9 +1217,30 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
       bk_gather<Real><<<dim3(1, nb), kB, 0, st>>>(P, A, s);
       *launches += 1;
     }
-    const size_t sm = ((P.band_Lpad * 4 + 15) & ~15) + size_t(P.band_Lpad) * sizeof(Real);
-    bk_write<Real><<<nb, kB, sm, st>>>(P, A);
-    ++*launches;
+    if (s0 <= steps) {
+      const int64_t amax = (appr0[s0 - 1] * appr1[s0 - 1] + 3) & ~int64_t(3);
+      const int64_t ymax = appr0[s0 - 1] * appr1[s0];
+      const size_t sm = ((P.band_Lpad * 4 + 15) & ~15) + size_t((P.band_Lpad + 3) & ~3) * sizeof(Real) +
+                        size_t(2 * amax + ymax) * sizeof(Real);
+      auto launch_tail = [&](auto kern) {
+        if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        kern<<<nb, kB, sm, st>>>(P, A, s0, steps, int(amax), int(ymax));
+      };
+      switch (P.L2) {
+        case 2: launch_tail(bk_tail<Real, 2>); break;
+        case 4: launch_tail(bk_tail<Real, 4>); break;
+        case 6: launch_tail(bk_tail<Real, 6>); break;
+        case 8: launch_tail(bk_tail<Real, 8>); break;
+        case 10: launch_tail(bk_tail<Real, 10>); break;
+        case 12: launch_tail(bk_tail<Real, 12>); break;
+        default: return cudaErrorInvalidValue;
+      }
+      ++*launches;
+    } else {
+      const size_t sm = ((P.band_Lpad * 4 + 15) & ~15) + size_t(P.band_Lpad) * sizeof(Real);
+      bk_write<Real><<<nb, kB, sm, st>>>(P, A);
+      ++*launches;
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -124,6 +124,7 @@ struct BatchArgs {
   int kt_vh, kt_vw;         // tiled k-sum: rows / columns of the periodically extended v that tmV maps
   const CUtensorMap* amaps; // approximation steps: device array [step - 1][sub-band - kt_sb_first] of TMA maps
   unsigned am_steps;        // bit s: step s of every sub-band of the launch has a map (bk_approx_tma)
+  int tail_s0;              // first step run by bk_tail (per-unit, shared memory); 0 = none
   const void* v;
   const void* T;
   const int4* stencil;      // .w = level of the partner sub-band
