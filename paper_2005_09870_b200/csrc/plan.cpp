@@ -414,19 +414,24 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
   }
 
   // shard: contiguous unit ranges (Λ order) with equal estimated time.  A unit's time is its algorithmic
-  // FMA count times a per-path weight (measured on B200: coarse-level units — batched / tile kernels — run
-  // ≈3× slower per FMA than units on the fine kernel); the template chain up to level ℓ is charged to the
-  // first unit of level ℓ (its owner builds it).  Boundaries are rounded to 16 units so every shard keeps
-  // whole rounds of the fine and tiled kernels.
+  // FMA count times a per-path weight: time per algorithmic FMA of each level's kernel path relative to
+  // the fine level-1 kernel, measured on B200 at c5 (profiles/r01, build r1d: fine ℓ = 1, 2, 3 at 1.0,
+  // 0.9, 1.5; batched ℓ = 4..7 at 1.36, 1.18, 1.05, 1.26; whole-torus windows 2.65).  The template chain up
+  // to level ℓ is charged to the first unit of level ℓ (its owner builds it).  Boundaries are rounded to
+  // 16 units so every shard keeps whole rounds of the fine and tiled kernels.
   std::vector<double> ucost(ns, 0.0), lump(ns, 0.0);
   for (int s = 0; s < ns; ++s) {
     const SubBand& S = P.sb[s];
-    const bool fine = P.retain == PCWD_RETAIN_BAND && S.fg_m > 0 && S.level <= 3;
-    ucost[s] = S.fma * (P.retain == PCWD_RETAIN_BAND && !fine ? 3.0 : 1.0);
+    double w = 1.0;
+    if (P.retain == PCWD_RETAIN_BAND) {
+      static const double wl[8] = {1.0, 1.0, 0.9, 1.5, 1.36, 1.18, 1.05, 1.26};
+      w = S.any_full ? 2.65 : wl[std::min(S.level, 7)];
+    }
+    ucost[s] = S.fma * w;
   }
   for (int lev = 1; lev <= J; ++lev) {
     const int s = sb_index(P.d, J, lev, 1);   // first detail sub-band of the level in Λ order
-    lump[lev == J ? 0 : s] += hp->tmpl_fma_level[lev] * 2.0;   // fp64 template passes: DFMA at half rate
+    lump[lev == J ? 0 : s] += hp->tmpl_fma_level[lev] * 4.0;   // fp64 template passes (DFMA half rate, L2-bound): ≈4× per FMA
   }
   double total = 0.0;
   for (int s = 0; s < ns; ++s) total += ucost[s] * double(P.sb[s].count) + lump[s];
