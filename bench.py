@@ -87,6 +87,27 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
+def _ncu_traffic(kind: str, level: int):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the newest committed `ncu --set full`
+    raw page (profiles/*/ncu_raw_fine_level{level}_*.csv), or None."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_raw_{kind}_level{level}_*.csv")))
+    if not files:
+        return None, None
+    rows = list(csv.reader(open(files[-1])))
+    if len(rows) < 3:
+        return None, None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        if name not in rows[0]:
+            return None, None
+        i = rows[0].index(name)
+        tot += float(rows[2][i].replace(",", "")) * scale.get(rows[1][i], 1.0)
+    return tot, os.path.relpath(files[-1], ROOT)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -248,8 +269,11 @@ def run_ours(args):
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # derived: SMs × lanes × 2 × clock
     achieved = 2.0 * dom[1] / (dom[0] * 1e-3) / 1e12
+    traffic, traffic_src = _ncu_traffic(dom[2], dom[3])
     roofline = {"bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": None,
+                "frac": achieved / fp32_peak, "traffic": traffic,
+                "traffic_source": f"{traffic_src} (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
+                if traffic_src else None,
                 "kernel": f"{dom[2]} unit kernel, level {dom[3]} (a2 k-sum + a3 cascade + a4 gather)",
                 "kernel_ms": dom[0], "kernel_share_of_step": dom[0] / ms_per_step,
                 "fma_per_launch": dom[1],
