@@ -225,10 +225,11 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         for (int j = 0; j < GU; ++j)
 #pragma unroll
           for (int i = 0; i < GZ; ++i) acc[a][j][i] = Real(0);
+      const int MK = (A.dbg_flags & 32) ? 1 : P.m;   // debug: stage only k = 0
       stage(0, 0);
       const int nst = A.nst;           // staging buffers in use (≤ NST, as many as fit in the R region)
       for (int q = 1; q < nst; ++q)
-        if (q < P.m) stage(q, q);
+        if (q < MK) stage(q, q);
       // per-task offsets into the staged T / v tiles (loop-invariant over k)
       int tofs[NT], vofs[NT];
       bool tact[NT];
@@ -244,13 +245,13 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         vofs[a] = A.TSZ + r * A.VS + sh + z0;
       }
       int b = 0;
-      for (int k = 0; k < P.m; ++k) {
+      for (int k = 0; k < MK; ++k) {
         mbar_wait(&fullbar[b], (phase >> b) & 1u);
         phase ^= 1u << b;
         const Real* Ts = Sbase + b * (A.TSZ + A.VSZ);
 #pragma unroll
         for (int a = 0; a < NT; ++a) {
-          if (tact[a]) {
+          if (tact[a] && !(A.dbg_flags & 8)) {
             const Real* tr = Ts + tofs[a];
             const Real* vr = Ts + vofs[a];
             Real tv[GZ];
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
           }
         }
         __syncthreads();
-        if (k + nst < P.m) stage(k + nst, b);
+        if (k + nst < MK) stage(k + nst, b);
         b = (b + 1 == nst) ? 0 : b + 1;
       }
       // R_j[r][z] (row stride RS), z < R1
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
       // local origin (xr0, xb)
       const int* dn = sd + min(S1, steps - 1) * 32;
       const int bxr = dn[0], bxrl = dn[1], bxc = dn[2], bxcl = dn[3];
-      for (int jj = gt; jj < L; jj += GT) {
+      for (int jj = gt; jj < ((A.dbg_flags & 16) ? 0 : L); jj += GT) {
         const int4 e = st[jj];
         const int s = e.w;                        // level of the partner sub-band
         const SubBand& Lb = P.sb[e.x];

@@ -73,7 +73,8 @@ struct FineArgs {
   int nst;                  // staging buffers used (1 ≤ nst ≤ the kernel's NST)
   int direct;               // 1: partners of the last two levels computed directly in the gather
   unsigned long long* dbg;  // optional phase clock counters (PCWD_DEBUG_PHASES): k-sum, cascade
-  int dbg_flags;            // debug experiments (PCWD_FINE_DBG, results invalid): 2 = no cascade, 4 = step 1 only
+  int dbg_flags;            // debug experiments (PCWD_FINE_DBG, results invalid): 2 = no cascade, 4 = step 1 only,
+                            // 8 = no k-sum FMAs, 16 = no gather, 32 = stage k = 0 only
 };
 
 // Template configuration of the fine kernel for (real_bytes, level): units per round GU, template
