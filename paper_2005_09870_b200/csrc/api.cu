@@ -296,10 +296,13 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
       if (dbg_on) {
         unsigned long long c[8];
         CK(cudaMemcpy(c, dbg, sizeof(c), cudaMemcpyDeviceToHost));
-        const double tot = double(c[0] + c[1] + c[2] + c[3] + c[4]);
-        fprintf(stderr, "[pcwd fine] level %d grid %d: ksum %.1f%% desc %.1f%% step1 %.1f%% steps2+ %.1f%% gather %.1f%%\n",
-                L.level, L.grid, 100.0 * c[0] / tot, 100.0 * c[1] / tot, 100.0 * c[2] / tot, 100.0 * c[3] / tot,
-                100.0 * c[4] / tot);
+        const double tot = double(c[0] + c[1]);
+        double sl = 0.0;
+        for (int q = 2; q < 8; ++q) sl += double(c[q]);
+        fprintf(stderr, "[pcwd fine] level %d grid %d: ksum %.1f%% rest %.1f%% | slot phases: desc %.1f%% passA %.1f%% "
+                "passB %.1f%% direct %.1f%% composite %.1f%% write %.1f%%\n", L.level, L.grid, 100.0 * c[0] / tot,
+                100.0 * c[1] / tot, 100.0 * c[2] / sl, 100.0 * c[3] / sl, 100.0 * c[4] / sl, 100.0 * c[5] / sl,
+                100.0 * c[6] / sl, 100.0 * c[7] / sl);
         cudaFree(dbg);
       }
       continue;
@@ -602,7 +605,9 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         const int TSZ = (R0 * TS + al - 1) / al * al, VSZ = (R0 * VS + al - 1) / al * al;
         // staging ring depth: the ring may use the whole dynamic smem (R, Yt and D regions are all idle
         // during the k-sum); as many buffers as fit, up to the kernel's NST
-        const int64_t regS = SLK + std::max<int64_t>(fc.CG * YSZ, fc.GU * YSZ2) + SLK;
+        // Yt slots (pass-A output of any step, then the gather stage) are max(YSZ, YSZ2) apart
+        const int64_t YSL = std::max<int64_t>(YSZ, YSZ2);
+        const int64_t regS = SLK + std::max<int64_t>(fc.CG * YSL, fc.GU * YSZ2) + SLK;
         const int64_t regD = regR + regS;
         int64_t total_el = regD + fc.GU * DS;
         int nst = int(std::min<int64_t>(fc.NST, (total_el - SLK - al) / (TSZ + VSZ)));
@@ -647,7 +652,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
                                      fl(((nl - fc.GU) << lev) + tmax1) + VS - P.n, 0});
           h->vpad = std::max(h->vpad, (need + 3) / 4 * 4);
           F.box[0] = R0; F.box[1] = TS; F.box[2] = VS;
-          A.RS = RS; A.RSZ = int(RSZ); A.TS = TS; A.VS = VS; A.YS = YS; A.YSZ = int(YSZ); A.DS = int(DS);
+          A.RS = RS; A.RSZ = int(RSZ); A.TS = TS; A.VS = VS; A.YS = YS; A.YSZ = int(YSL); A.DS = int(DS);
           A.YS2 = YS2; A.YSZ2 = int(YSZ2);
           add_generic(u0, a0, scr);
           h->launches.push_back(F);

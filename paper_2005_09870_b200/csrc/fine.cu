@@ -185,6 +185,8 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
   static_assert(NST >= 1 && NST <= 8, "staging depth");
 
   long long t_ksum = 0, t_casc = 0, t_last = 0;
+  long long ph[6] = {0, 0, 0, 0, 0, 0}, tp = 0;   // debug: slot-leader phase clocks
+  auto tick = [&](int q) { if (A.dbg && gt == 0) { const long long t = clock64(); ph[q] += t - tp; tp = t; } };
   for (int64_t rd = blockIdx.x; rd < rounds; rd += gridDim.x) {
     if (A.dbg && tid == 0) t_last = clock64();
     const int64_t ufirst = A.u0 + rd * GU;
@@ -313,6 +315,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     // (CG units at a time, one thread group each; Yt, D and the step descriptors are per group slot)
     for (int w0 = 0; w0 < GU; w0 += CG) {
     const int u = w0 + slot;
+    if (A.dbg && gt == 0) tp = clock64();
     const int p1 = p1f + u;
     const int cls0 = p0 & (S.fg_m - 1), cls1 = p1 & (S.fg_m - 1);
     const FGeom& G = A.geom[S.fg_off + cls0 * S.fg_m + cls1];
@@ -342,6 +345,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     }
     if (gt == 0) { wflag[slot] = 0; nheavy[slot] = 0; }
     bar_group(1 + slot, GT);
+    tick(0);
     int xb = (p1 << LEV) + S.tSu[1] - roff;      // column of X's local index 0 (even)
     int xr0 = c0;                                // row of X's local index 0
     // cascade steps 1..S1; the partners of the last two levels are computed in the gather directly from the
@@ -401,6 +405,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         }
       }
       bar_group(1 + slot, GT);
+      tick(1);
       // pass B: Yt rows (axis 0) -> approximation box (next X) and detail boxes (D); one flat task index
       // over the four boxes (box, row block, column), column fastest
       int nxb = 0, nxr = 0;
@@ -449,6 +454,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         }
       }
       bar_group(1 + slot, GT);
+      tick(2);
       xb = nxb;
       xr0 = nxr;
     }
@@ -524,6 +530,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
       // any partner wraps around the torus -> place by rank of the column
       if (wrap) wflag[slot] = 1;
       bar_group(1 + slot, GT);
+      tick(3);
       // partners two levels past S1: one warp per coefficient, lanes over the (3·2δ − 2) rows of its
       // composite footprint, warp reduction
       {
@@ -570,6 +577,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         }
       }
       bar_group(1 + slot, GT);
+      tick(4);
       wrap = wflag[slot];
       for (int jj = gt; jj < L; jj += GT) {
         const int c = sc[jj];
@@ -582,6 +590,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         outv[base + rank] = sv[jj];
       }
     }
+    tick(5);
     __syncthreads();
     }
     if (A.dbg && tid == 0) { const long long t = clock64(); t_casc += t - t_last; t_last = t; }
@@ -590,6 +599,8 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     atomicAdd(A.dbg, (unsigned long long)t_ksum);
     atomicAdd(A.dbg + 1, (unsigned long long)t_casc);
   }
+  if (A.dbg && gt == 0)
+    for (int q = 0; q < 6; ++q) atomicAdd(A.dbg + 2 + q, (unsigned long long)ph[q]);
 }
 
 // ---------------------------------------------------------------------------------- launcher
