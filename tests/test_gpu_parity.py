@@ -308,3 +308,19 @@ def test_smallest_torus_haar():
     T = op.theta_dense(p)
     g = run(p, "f64")
     assert np.max(np.abs(g["val"].reshape(4, 4) - T)) < 1e-14
+
+
+def test_largest_torus_band_fp32():
+    """2048² (4.2M units, J = 9, the deepest cascade the c5 path plans), band L = 64: CSR shape, finite values,
+    and parity on sampled units of the three finest levels against the oracle rows."""
+    p = C.micro(2048, 2, 4, 9, 4, 6, 46, retain="band", band_L=64)
+    g = run(p, "f32")
+    assert g["nnz"] == p.N * 64 and np.all(np.isfinite(g["val"]))
+    from oracle import basis
+    rng = np.random.default_rng(5)
+    units = []
+    for (lev, e, off, nl) in basis.subbands(p.d, p.n, p.J):
+        if lev <= 3:
+            units.extend(int(off + x) for x in rng.choice(nl * nl, size=2, replace=False))
+    units = sorted(set(units))
+    compare(p, g, units, R.rows(p, units), "f32")
