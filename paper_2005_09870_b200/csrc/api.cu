@@ -297,12 +297,8 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
         unsigned long long c[8];
         CK(cudaMemcpy(c, dbg, sizeof(c), cudaMemcpyDeviceToHost));
         const double tot = double(c[0] + c[1]);
-        double sl = 0.0;
-        for (int q = 2; q < 8; ++q) sl += double(c[q]);
-        fprintf(stderr, "[pcwd fine] level %d grid %d: ksum %.1f%% rest %.1f%% | slot phases: desc %.1f%% passA %.1f%% "
-                "passB %.1f%% direct %.1f%% composite %.1f%% write %.1f%%\n", L.level, L.grid, 100.0 * c[0] / tot,
-                100.0 * c[1] / tot, 100.0 * c[2] / sl, 100.0 * c[3] / sl, 100.0 * c[4] / sl, 100.0 * c[5] / sl,
-                100.0 * c[6] / sl, 100.0 * c[7] / sl);
+        fprintf(stderr, "[pcwd fine] level %d grid %d: ksum %.1f%% cascade+gather %.1f%%\n", L.level, L.grid,
+                100.0 * c[0] / tot, 100.0 * c[1] / tot);
         cudaFree(dbg);
       }
       continue;
@@ -637,7 +633,13 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           A.regS = regR; A.regD = regD;
           A.TSZ = TSZ; A.VSZ = VSZ;
           A.nst = nst;
-          A.direct = getenv("PCWD_NO_DIRECT") ? 0 : 1;
+          // partner levels computed directly from the last cascade approximation: PCWD_FINE_DIRECT = "d1,d2,d3"
+          // per fine level (2 = one step of 2δ × 2δ taps plus one composite step, 1 = the 2δ × 2δ step only)
+          {
+            int dl[3] = {2, 2, 1};   // measured on c5: level 3 faster with one more cascade step
+            if (const char* e = getenv("PCWD_FINE_DIRECT")) sscanf(e, "%d,%d,%d", &dl[0], &dl[1], &dl[2]);
+            A.direct = getenv("PCWD_NO_DIRECT") ? 0 : std::max(0, std::min(2, dl[lev - 1]));
+          }
           (void)stg;
           A.sb_first = s;
           // halo of the padded v that every round's boxes stay inside

@@ -185,8 +185,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
   static_assert(NST >= 1 && NST <= 8, "staging depth");
 
   long long t_ksum = 0, t_casc = 0, t_last = 0;
-  long long ph[6] = {0, 0, 0, 0, 0, 0}, tp = 0;   // debug: slot-leader phase clocks
-  auto tick = [&](int q) { if (A.dbg && gt == 0) { const long long t = clock64(); ph[q] += t - tp; tp = t; } };
   for (int64_t rd = blockIdx.x; rd < rounds; rd += gridDim.x) {
     if (A.dbg && tid == 0) t_last = clock64();
     const int64_t ufirst = A.u0 + rd * GU;
@@ -227,11 +225,10 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         for (int j = 0; j < GU; ++j)
 #pragma unroll
           for (int i = 0; i < GZ; ++i) acc[a][j][i] = Real(0);
-      const int MK = (A.dbg_flags & 32) ? 1 : P.m;   // debug: stage only k = 0
       stage(0, 0);
       const int nst = A.nst;           // staging buffers in use (≤ NST, as many as fit in the R region)
       for (int q = 1; q < nst; ++q)
-        if (q < MK) stage(q, q);
+        if (q < P.m) stage(q, q);
       // per-task offsets into the staged T / v tiles (loop-invariant over k)
       int tofs[NT], vofs[NT];
       bool tact[NT];
@@ -247,13 +244,13 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         vofs[a] = A.TSZ + r * A.VS + sh + z0;
       }
       int b = 0;
-      for (int k = 0; k < MK; ++k) {
+      for (int k = 0; k < P.m; ++k) {
         mbar_wait(&fullbar[b], (phase >> b) & 1u);
         phase ^= 1u << b;
         const Real* Ts = Sbase + b * (A.TSZ + A.VSZ);
 #pragma unroll
         for (int a = 0; a < NT; ++a) {
-          if (tact[a] && !(A.dbg_flags & 8)) {
+          if (tact[a]) {
             const Real* tr = Ts + tofs[a];
             const Real* vr = Ts + vofs[a];
             Real tv[GZ];
@@ -271,7 +268,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
           }
         }
         __syncthreads();
-        if (k + nst < MK) stage(k + nst, b);
+        if (k + nst < P.m) stage(k + nst, b);
         b = (b + 1 == nst) ? 0 : b + 1;
       }
       // R_j[r][z] (row stride RS), z < R1
@@ -315,7 +312,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     // (CG units at a time, one thread group each; Yt, D and the step descriptors are per group slot)
     for (int w0 = 0; w0 < GU; w0 += CG) {
     const int u = w0 + slot;
-    if (A.dbg && gt == 0) tp = clock64();
     const int p1 = p1f + u;
     const int cls0 = p0 & (S.fg_m - 1), cls1 = p1 & (S.fg_m - 1);
     const FGeom& G = A.geom[S.fg_off + cls0 * S.fg_m + cls1];
@@ -345,13 +341,12 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     }
     if (gt == 0) { wflag[slot] = 0; nheavy[slot] = 0; }
     bar_group(1 + slot, GT);
-    tick(0);
     int xb = (p1 << LEV) + S.tSu[1] - roff;      // column of X's local index 0 (even)
     int xr0 = c0;                                // row of X's local index 0
     // cascade steps 1..S1; the partners of the last two levels are computed in the gather directly from the
     // step-S1 approximation (2δ × 2δ taps for level S1 + 1, composite (3·2δ − 2)² taps for S1 + 2), which
     // replaces the two smallest, latency-bound cascade steps
-    const int S1 = A.direct ? (steps <= 2 ? 1 : steps - 2) : steps;
+    const int S1 = steps <= A.direct ? 1 : steps - A.direct;   // A.direct levels (≤ 2) computed directly in the gather
     int steps_run = (A.dbg_flags & 2) ? 0 : (A.dbg_flags & 4) ? 1 : steps;   // debug: skip cascade steps
     steps_run = min(steps_run, S1);
     for (int s = 1; s <= steps_run; ++s) {
@@ -405,7 +400,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         }
       }
       bar_group(1 + slot, GT);
-      tick(1);
       // pass B: Yt rows (axis 0) -> approximation box (next X) and detail boxes (D); one flat task index
       // over the four boxes (box, row block, column), column fastest
       int nxb = 0, nxr = 0;
@@ -454,7 +448,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         }
       }
       bar_group(1 + slot, GT);
-      tick(2);
       xb = nxb;
       xr0 = nxr;
     }
@@ -474,7 +467,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
       // local origin (xr0, xb)
       const int* dn = sd + min(S1, steps - 1) * 32;
       const int bxr = dn[0], bxrl = dn[1], bxc = dn[2], bxcl = dn[3];
-      for (int jj = gt; jj < ((A.dbg_flags & 16) ? 0 : L); jj += GT) {
+      for (int jj = gt; jj < L; jj += GT) {
         const int4 e = st[jj];
         const int s = e.w;                        // level of the partner sub-band
         const SubBand& Lb = P.sb[e.x];
@@ -530,7 +523,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
       // any partner wraps around the torus -> place by rank of the column
       if (wrap) wflag[slot] = 1;
       bar_group(1 + slot, GT);
-      tick(3);
       // partners two levels past S1: one warp per coefficient, lanes over the (3·2δ − 2) rows of its
       // composite footprint, warp reduction
       {
@@ -577,7 +569,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         }
       }
       bar_group(1 + slot, GT);
-      tick(4);
       wrap = wflag[slot];
       for (int jj = gt; jj < L; jj += GT) {
         const int c = sc[jj];
@@ -590,7 +581,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
         outv[base + rank] = sv[jj];
       }
     }
-    tick(5);
     __syncthreads();
     }
     if (A.dbg && tid == 0) { const long long t = clock64(); t_casc += t - t_last; t_last = t; }
@@ -599,8 +589,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     atomicAdd(A.dbg, (unsigned long long)t_ksum);
     atomicAdd(A.dbg + 1, (unsigned long long)t_casc);
   }
-  if (A.dbg && gt == 0)
-    for (int q = 0; q < 6; ++q) atomicAdd(A.dbg + 2 + q, (unsigned long long)ph[q]);
 }
 
 // ---------------------------------------------------------------------------------- launcher

@@ -71,10 +71,9 @@ struct FineArgs {
   int YS2, YSZ2;            // Yt row stride and per-unit size for steps ≥ 2 and the gather stage (GU units)
   int DS;                   // per-unit D size
   int nst;                  // staging buffers used (1 ≤ nst ≤ the kernel's NST)
-  int direct;               // 1: partners of the last two levels computed directly in the gather
+  int direct;               // partner levels (0, 1 or 2, the coarsest ones) computed directly in the gather
   unsigned long long* dbg;  // optional phase clock counters (PCWD_DEBUG_PHASES): k-sum, cascade
-  int dbg_flags;            // debug experiments (PCWD_FINE_DBG, results invalid): 2 = no cascade, 4 = step 1 only,
-                            // 8 = no k-sum FMAs, 16 = no gather, 32 = stage k = 0 only
+  int dbg_flags;            // debug experiments (PCWD_FINE_DBG, results invalid): 2 = no cascade, 4 = step 1 only
 };
 
 // Template configuration of the fine kernel for (real_bytes, level): units per round GU, template
