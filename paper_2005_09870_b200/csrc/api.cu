@@ -832,6 +832,18 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         B.ba.kt_sb_first = s;
       }
       B.ba.kt_sb_first = s;
+      // whole-torus k-sum with TMA (2^ℓ = 256, a sub-band row of 2 or 4 units): v and template maps, 256 × 2 boxes
+      if (!gz && P.d == 2 && lev == 8 && (1 << lev) * P.sb[s].nl == P.n && (P.sb[s].nl == 4 || P.sb[s].nl == 2) &&
+          e - s <= 4 && !getenv("PCWD_NO_TMA_KSUM")) {
+        bool full = true;
+        for (int q = s; q < e; ++q) full = full && P.sb[q].tW[0] >= P.n && P.sb[q].tW[1] >= P.n;
+        int rc2 = full ? encode_map3(&B.ba.tmV, h->v_d, rb, P.n, P.n, P.m, P.n, int64_t(P.n) * P.n, 256, 2) : 1;
+        for (int q = s, i = 0; full && q < e && !rc2; ++q, ++i)
+          rc2 = encode_map3(&B.ba.tmT[i], static_cast<char*>(h->T_d) + P.sb[q].toff * rb, rb, P.sb[q].tRS, P.n, P.m,
+                            P.sb[q].tRS, P.sb[q].tstride, 256, 2);
+        if (full && rc2) return bail(PCWD_E_CUDA, "cuTensorMapEncodeTiled (whole-torus k-sum) failed: " + std::to_string(rc2));
+        if (full) B.ba.kf_rows = 2;
+      }
       // approximation steps on the TMA path: every participating sub-band's step-s input window has one size
       // over its units and stays clear of wrapping (maps encoded once the scratch exists)
       for (int st = 1; st <= steps && st < 32; ++st) {

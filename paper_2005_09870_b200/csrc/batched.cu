@@ -315,6 +315,88 @@ constexpr size_t ksum_tma_smem() {
   return sizeof(Real) * 3 * size_t(NTB * TR * SH * QT + NVB * VBOX) + 128;
 }
 
+// Whole-torus k-sum with TMA staging, for 2^ℓ = 256 (n = 256·NL): as bk_ksum_full (units of a sub-band row
+// share the v row; template columns shifted by 2^ℓ u), but a thread owns TRT rows, and the v rows (NL boxes of
+// 256 columns) and the template strip (2NL − 1 boxes of 256 columns, each starting on a multiple of 256 so
+// none crosses the torus seam) are TMA boxes in a 3-stage mbarrier ring.
+template <typename Real, int NL, int TRT>
+__global__ void __launch_bounds__(kB) bk_ksum_full_tma(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A) {
+  constexpr int SH = 256, G = NL, NTS = NL + G - 1;
+  constexpr int BOX = TRT * SH;                     // elements per box
+  constexpr int STAGE = (NL + NTS) * BOX;
+  constexpr int NST = 3;
+  extern __shared__ __align__(16) unsigned char kfm[];
+  __shared__ unsigned long long full[NST];
+  Real* stg = reinterpret_cast<Real*>(kfm + ((128 - (smem_u32(kfm) & 127)) & 127));
+  const int tid = threadIdx.x;
+  const int n = P.n, mask = n - 1;
+  const int64_t ug = A.u0 + int64_t(blockIdx.y) * G;
+  const UnitPos up = unit_pos(P, ug);
+  const SubBand& S = P.sb[up.sbi];
+  const int z0 = blockIdx.x * TRT;
+  const int sy = up.p0 * SH;
+  const int x0 = (-(up.p1 * SH + SH * (G - 1))) & mask;   // template column of strip column 0
+  const int yt = (z0 - sy) & mask;                          // template row of tile row 0 (TRT | n: no wrap)
+  const CUtensorMap* tmT = &A.tmT[up.sbi - A.kt_sb_first];
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int k) {
+    if (tid == 0 && k < P.m) {
+      Real* b = stg + (k % NST) * STAGE;
+      mbar_expect_tx(&full[k % NST], unsigned(sizeof(Real) * STAGE));
+#pragma unroll
+      for (int i = 0; i < NL; ++i) tma_load_3d(b + i * BOX, &A.tmV, i * SH, z0, k, &full[k % NST]);
+#pragma unroll
+      for (int j = 0; j < NTS; ++j)
+        tma_load_3d(b + (NL + j) * BOX, tmT, (x0 + j * SH) & mask, yt, k, &full[k % NST]);
+    }
+  };
+  Real acc[TRT][G][NL];
+#pragma unroll
+  for (int t = 0; t < TRT; ++t)
+#pragma unroll
+    for (int u = 0; u < G; ++u)
+#pragma unroll
+      for (int i = 0; i < NL; ++i) acc[t][u][i] = Real(0);
+#pragma unroll
+  for (int q = 0; q < NST - 1; ++q) issue(q);
+  for (int k = 0; k < P.m; ++k) {
+    issue(k + NST - 1);
+    mbar_wait(&full[k % NST], unsigned(k / NST) & 1u);
+    const Real* Vb = stg + (k % NST) * STAGE;
+    const Real* Tb = Vb + NL * BOX;
+#pragma unroll
+    for (int t = 0; t < TRT; ++t) {
+      Real vv[NL];
+#pragma unroll
+      for (int i = 0; i < NL; ++i) vv[i] = Vb[i * BOX + t * SH + tid];
+      // unit u, column tid + SH i: strip chunk i − u + G − 1
+#pragma unroll
+      for (int mm = 0; mm < NTS; ++mm) {
+        const Real tm = Tb[mm * BOX + t * SH + tid];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const int i = mm + u - (G - 1);
+          if (i >= 0 && i < NL) acc[t][u][i] = fmaB(vv[i], tm, acc[t][u][i]);
+        }
+      }
+    }
+    __syncthreads();   // stage k % NST is refilled by issue(k + NST) next iteration
+  }
+  const int rs = rstride(n);
+#pragma unroll
+  for (int u = 0; u < G; ++u) {
+    Real* X0 = reinterpret_cast<Real*>(A.scratch) + (ug + u - A.u0) * A.stride + S.offX0;
+#pragma unroll
+    for (int t = 0; t < TRT; ++t)
+#pragma unroll
+      for (int i = 0; i < NL; ++i) X0[int64_t(z0 + t) * rs + tid + SH * i] = acc[t][u][i];
+  }
+}
+
 // Tiled k-sum for windows covering the whole torus on both axes (coarsest levels): the window is the torus,
 // R(y) = Σ_k v_k(y) T_k((y - 2^ℓ p) mod n); G units adjacent along axis 1 read the same v tile and
 // template columns shifted by 2^ℓ u.  A thread owns tile row r and the NL columns res + 2^ℓ i of one residue
@@ -1176,6 +1258,20 @@ static bool launch_ksum_full(const Plan& P, const BatchArgs& A, int nb, cudaStre
   for (int q = s0; q <= s1; ++q)
     if (P.sb[q].level != lev || P.sb[q].tW[0] < P.n || P.sb[q].tW[1] < P.n) return false;
   if (nb % nl || (A.u0 - S.offset) % nl) return false;
+  if (A.kf_rows == 2 && lev == 8 && (nl == 4 || nl == 2) && !getenv("PCWD_NO_TMA_KSUM")) {
+    auto launch = [&](auto kern, int NLV) {
+      const size_t smem = sizeof(Real) * 3 * size_t(2 * NLV - 1 + NLV) * 2 * 256 + 128;
+      static bool attr[2] = {false, false};
+      if (!attr[NLV == 4]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr[NLV == 4] = true;
+      }
+      kern<<<dim3(P.n / 2, nb / NLV), kB, smem, st>>>(P, A);
+    };
+    if (nl == 4) launch(bk_ksum_full_tma<Real, 4, 2>, 4);
+    else launch(bk_ksum_full_tma<Real, 2, 2>, 2);
+    return true;
+  }
   const int TR = std::max(1, kB >> lev);
   const dim3 grid((P.n + TR - 1) / TR, nb / nl);
 #define PCWD_KF(L, NLV)                                                                      \

@@ -117,7 +117,9 @@ constexpr int kt_vbox_n(int SH, int Q0, int rb) {
 
 struct BatchArgs {
   CUtensorMap tmV;          // tiled k-sum: TMA map of v (3-D: x, y, k), box (SH·qV + kt_vpadx) × TR × 1
-  CUtensorMap tmT[3];       // tiled k-sum: TMA maps of the level's templates, box SH·qT × TR × 1
+  CUtensorMap tmT[4];       // tiled k-sum: TMA maps of the level's templates, box SH·qT × TR × 1 (whole-torus
+                            // k-sum: box 256 × kf_rows × 1, one per sub-band of the level incl. the coarse block)
+  int kf_rows;              // whole-torus k-sum with TMA (bk_ksum_full_tma): rows per thread; 0 = not planned
   int kt_gz;                // tiled k-sum: template column groups per thread (0 ⇒ not planned)
   int kt_sb_first;          // tiled k-sum: sub-band of tmT[0]
   int kt_flags;             // tiled k-sum debug: 1 = v strips by cp.async only
