@@ -52,7 +52,7 @@ struct Handle {
   void* vpad_d = nullptr;   // periodically padded v (fine path TMA source)
   void* vwrap_d = nullptr;  // v extended periodically by kt_pr rows / kt_pc columns (tiled k-sum TMA source)
   CUtensorMap* amaps_d = nullptr;   // TMA maps of the batched approximation steps
-  int kt_pr = 0, kt_pc = 0;
+  int kt_pr = 0, kt_pc = 0, kt_offx = 0;
   int vpad = 0;
   void* gscratch = nullptr;
   int64_t gstride = 0;
@@ -912,7 +912,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     }
   }
   if (h->kt_pc > 0) {   // v extended periodically by kt_pr rows and kt_pc columns: every k-sum v box is one TMA copy
-    h->kt_pc = (h->kt_pc + 31) / 32 * 32;
+    h->kt_offx = ((P.zhi[1] % 4) + 4) % 4;   // strip starts ≡ −zhi (mod 4) at levels ≥ 2: shift them onto 16 bytes
+    h->kt_pc = (h->kt_pc + h->kt_offx + 31) / 32 * 32;
     const int H = P.n + h->kt_pr, W = P.n + h->kt_pc;
     CKB(dalloc(&h->vwrap_d, size_t(P.m) * H * W * rb));
     for (Launch& L : h->launches) {
@@ -923,6 +924,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       if (rc2) return bail(PCWD_E_CUDA, "cuTensorMapEncodeTiled (k-sum v) failed: " + std::to_string(rc2));
       L.ba.kt_vh = H;
       L.ba.kt_vw = W;
+      L.ba.kt_offx = h->kt_offx;
     }
   }
   // fine path: periodically padded v (K1) and the TMA descriptors of every fine launch
@@ -1012,7 +1014,7 @@ int pcwd_decompose(void* handle, void* stream) {
       h->nlaunch++;
     }
     if (h->vwrap_d) {  // periodic extension of v, the TMA source of the tiled coarse k-sums
-      CK(launch_wrap_v(h->v_d, h->vwrap_d, P.n, 0, P.n + h->kt_pr, P.n + h->kt_pc, P.m, h->hp.real_bytes, st));
+      CK(launch_wrap_v(h->v_d, h->vwrap_d, P.n, 0, h->kt_offx, P.n + h->kt_pr, P.n + h->kt_pc, P.m, h->hp.real_bytes, st));
       h->nlaunch++;
     }
     if ((rc = build_templates(h, st))) return rc;

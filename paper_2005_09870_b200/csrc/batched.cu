@@ -225,10 +225,11 @@ __global__ void __launch_bounds__(kB) bk_ksum_tma(const __grid_constant__ Plan P
   const int z0 = t0 * TR, zc = t1 * SH * GZ;
   const int yr = ((up.p0 << LEV) + S.tSu[0] + z0) & mask;              // first v row of the tile
   const int xc = ((up.p1 << LEV) + S.tSu[1] + zc) & mask;              // first v column of the strip
-  const int sh = xc & (VW - 1), xa = xc - sh;                          // 16-byte aligned box start
+  // v_wrap column of the strip start (kt_offx makes it 16-byte aligned: sh = 0 for every level ≥ 2)
+  const int xw = xc + A.kt_offx, sh = xw & (VW - 1), xa = xw - sh;
   // each v box starts at its own wrapped column; the periodic extension (kt_vh × kt_vw ≥ (n + TR) × (n + VBW))
   // makes every box one TMA copy, wherever the strip crosses the torus seam
-  const bool tma_v = yr + TR <= A.kt_vh && VBW <= A.kt_vw - n && !(A.kt_flags & 1);
+  const bool tma_v = yr + TR <= A.kt_vh && VBW + A.kt_offx <= A.kt_vw - n && sh + SH * QV <= VBW && !(A.kt_flags & 1);
   const CUtensorMap* tmT = &A.tmT[up.sbi - A.kt_sb_first];
   if (tid == 0) {
     for (int q = 0; q < NST; ++q) mbar_init(&full[q], 1);
@@ -246,7 +247,8 @@ __global__ void __launch_bounds__(kB) bk_ksum_tma(const __grid_constant__ Plan P
         if (tma_v) {
 #pragma unroll
           for (int j = 0; j < NVB; ++j)
-            tma_load_3d(b + NTB * TBOX + j * VBOX, &A.tmV, (xa + j * SH * QV) & mask, yr, k, &full[k % NST]);
+            tma_load_3d(b + NTB * TBOX + j * VBOX, &A.tmV, ((xa + j * SH * QV - A.kt_offx) & mask) + A.kt_offx, yr, k,
+                        &full[k % NST]);
         }
       }
       if (!tma_v) {   // strip across the torus seam: element copies into the same layout

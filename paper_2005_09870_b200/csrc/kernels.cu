@@ -144,13 +144,13 @@ __global__ void tmpl_passB(const __grid_constant__ Plan P, const __grid_constant
   }
 }
 
-// Periodic extension of v: out[k][y][x] = v[k][(y - off) mod n][(x - off) mod n], y < H, x < W (row pitch W).
+// Periodic extension of v: out[k][y][x] = v[k][(y - offy) mod n][(x - offx) mod n], y < H, x < W (row pitch W).
 // Grid (ceil(W / 256), H, m): one thread per output element, coalesced along x.
 template <typename Real>
-__global__ void wrap_v_kernel(const Real* __restrict__ v, Real* __restrict__ out, int n, int off, int H, int W) {
+__global__ void wrap_v_kernel(const Real* __restrict__ v, Real* __restrict__ out, int n, int offy, int offx, int H, int W) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, k = blockIdx.z;
   if (x >= W) return;
-  const int sy = (y - off + n * 4) & (n - 1), sx = (x - off + n * 4) & (n - 1);
+  const int sy = (y - offy + n * 4) & (n - 1), sx = (x - offx + n * 4) & (n - 1);
   out[(int64_t(k) * H + y) * W + x] = v[(int64_t(k) * n + sy) * n + sx];
 }
 
@@ -560,13 +560,14 @@ cudaError_t launch_tmpl_level(const Plan& P, const TmplArgs& A, int real_bytes, 
 }
 
 cudaError_t launch_pad_v(const void* v, void* vpad, int n, int P, int m, int real_bytes, cudaStream_t st) {
-  return launch_wrap_v(v, vpad, n, P, n + 2 * P, n + 2 * P, m, real_bytes, st);
+  return launch_wrap_v(v, vpad, n, P, P, n + 2 * P, n + 2 * P, m, real_bytes, st);
 }
 
-cudaError_t launch_wrap_v(const void* v, void* out, int n, int off, int H, int W, int m, int real_bytes, cudaStream_t st) {
+cudaError_t launch_wrap_v(const void* v, void* out, int n, int offy, int offx, int H, int W, int m, int real_bytes,
+                          cudaStream_t st) {
   const dim3 grid((W + 255) / 256, H, m);
-  if (real_bytes == 4) wrap_v_kernel<float><<<grid, 256, 0, st>>>((const float*)v, (float*)out, n, off, H, W);
-  else wrap_v_kernel<double><<<grid, 256, 0, st>>>((const double*)v, (double*)out, n, off, H, W);
+  if (real_bytes == 4) wrap_v_kernel<float><<<grid, 256, 0, st>>>((const float*)v, (float*)out, n, offy, offx, H, W);
+  else wrap_v_kernel<double><<<grid, 256, 0, st>>>((const double*)v, (double*)out, n, offy, offx, H, W);
   return cudaGetLastError();
 }
 

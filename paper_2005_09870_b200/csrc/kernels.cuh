@@ -99,11 +99,11 @@ constexpr int kt_box_n(int SH, int Q0) {
   return nb;
 }
 constexpr int kt_units(int real_bytes) { return real_bytes == 4 ? 8 : 4; }   // G: units per tiled k-sum group
-// The v strip starts at an arbitrary column but a TMA box must start on a 16-byte boundary: each v box covers
-// SH·q columns from an aligned-down start plus kt_vpadx extra columns (the shift and bank padding): SH
-// for SH ≤ 16 with q even (fp32: a warp reads 32/SH rows, a row pitch ≡ SH mod 2SH keeps them in distinct
-// banks), else one 16-byte vector.
-constexpr int kt_vpadx(int SH, int rb) { return rb == 8 ? 2 : (SH <= 16 ? SH : 4); }
+// A TMA box must start on a 16-byte boundary.  The periodic extension of v is built with a column offset
+// (kt_offx) that puts every strip start of the levels ≥ 2 on one (their starts are ≡ −zhi mod 4), so a
+// v box covers SH·q columns plus kt_vpadx columns of bank padding: SH for SH ≤ 16 with q even (fp32: a
+// warp reads 32/SH rows, a row pitch ≡ SH mod 2SH keeps them in distinct banks), else none.
+constexpr int kt_vpadx(int SH, int rb) { return rb == 8 ? 0 : (SH <= 16 ? SH : 0); }
 constexpr int kt_vbox_q(int SH, int Q0, int nb, int rb) {
   int q = (Q0 + nb - 1) / nb;
   if (rb == 4 && SH <= 16 && q % 2 == 1) ++q;
@@ -124,6 +124,7 @@ struct BatchArgs {
   int kt_sb_first;          // tiled k-sum: sub-band of tmT[0]
   int kt_flags;             // tiled k-sum debug: 1 = v strips by cp.async only
   int kt_vh, kt_vw;         // tiled k-sum: rows / columns of the periodically extended v that tmV maps
+  int kt_offx;              // its column offset: v_wrap[y][x] = v[y mod n][(x − kt_offx) mod n]
   const CUtensorMap* amaps; // approximation steps: device array [step - 1][sub-band - kt_sb_first] of TMA maps
   unsigned am_steps;        // bit s: step s of every sub-band of the launch has a map (bk_approx_tma)
   int tail_s0;              // first step run by bk_tail (per-unit, shared memory); 0 = none
@@ -174,8 +175,9 @@ cudaError_t launch_support_check(const double* u, int64_t total, int n, int d, c
                                  int* flag, cudaStream_t st);
 // K1: v_pad[k][y][x] = v[k][(y - P) mod n][(x - P) mod n], side n + 2P (compute type)
 cudaError_t launch_pad_v(const void* v, void* vpad, int n, int P, int m, int real_bytes, cudaStream_t st);
-// out[k][y][x] = v[k][(y - off) mod n][(x - off) mod n] for y < H, x < W (off ≤ 4n; n a power of two).
-cudaError_t launch_wrap_v(const void* v, void* out, int n, int off, int H, int W, int m, int real_bytes, cudaStream_t st);
+// out[k][y][x] = v[k][(y - offy) mod n][(x - offx) mod n] for y < H, x < W (offsets ≤ 4n; n a power of two).
+cudaError_t launch_wrap_v(const void* v, void* out, int n, int offy, int offx, int H, int W, int m, int real_bytes,
+                          cudaStream_t st);
 cudaError_t launch_units(const Plan& P, const UnitArgs& A, int mode, int real_bytes, int out_bytes,
                          int grid, size_t smem, cudaStream_t st);
 size_t unit_smem_limit();
