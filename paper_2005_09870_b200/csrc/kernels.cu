@@ -61,14 +61,14 @@ __global__ void tmpl_passA(const __grid_constant__ Plan P, const __grid_constant
   const int Win0 = A.Win[0], Win1 = A.Win[1], Wout1 = A.Wout[1];
   const int ngr = (Wout1 + dil * QT - 1) / (dil * QT);   // groups of QT outputs per residue
   const int64_t total = int64_t(P.m) * 2 * Win0 * dil * ngr;
-  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int r = int(idx % dil);
-    int64_t t = idx / dil;
-    const int g = int(t % ngr);
-    t /= ngr;
-    const int i0 = int(t % Win0);
-    t /= Win0;
+  // index decomposition in 32 bits (the grids of every plan this library accepts stay below 2^31 threads)
+  for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < unsigned(total); idx += gridDim.x * blockDim.x) {
+    const int r = int(idx % unsigned(dil));
+    unsigned t = idx / unsigned(dil);
+    const int g = int(t % unsigned(ngr));
+    t /= unsigned(ngr);
+    const int i0 = int(t % unsigned(Win0));
+    t /= unsigned(Win0);
     const int e1 = int(t & 1);
     const int64_t k = t >> 1;
     const int o = e1 ? 2 - L2 : 0;
@@ -109,14 +109,13 @@ __global__ void tmpl_passB(const __grid_constant__ Plan P, const __grid_constant
   const int64_t per = int64_t(Wout0) * Wout1;
   const int64_t total = int64_t(P.m) * 4 * dil * ngr * Wout1;
   Real* T = reinterpret_cast<Real*>(A.T);
-  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int j1 = int(idx % Wout1);
-    int64_t t = idx / Wout1;
-    const int r = int(t % dil);
-    t /= dil;
-    const int g = int(t % ngr);
-    t /= ngr;
+  for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < unsigned(total); idx += gridDim.x * blockDim.x) {
+    const int j1 = int(idx % unsigned(Wout1));
+    unsigned t = idx / unsigned(Wout1);
+    const int r = int(t % unsigned(dil));
+    t /= unsigned(dil);
+    const int g = int(t % unsigned(ngr));
+    t /= unsigned(ngr);
     const int ec = int(t & 3);
     const int64_t k = t >> 2;
     const int e0 = ec >> 1, e1 = ec & 1;
@@ -528,28 +527,30 @@ cudaError_t launch_phi0(const Plan& P, const double* u, double* phi0, int S0, in
 }
 
 template <typename Real, int L2>
-static void launch_tmpl_t(const Plan& P, const TmplArgs& A, int level, cudaStream_t st) {
+static cudaError_t launch_tmpl_t(const Plan& P, const TmplArgs& A, int level, cudaStream_t st) {
   const int64_t ngA = (A.Wout[1] + int64_t(A.dil) * QT - 1) / (int64_t(A.dil) * QT);
   const int64_t ngB = (A.Wout[0] + int64_t(A.dil) * QT - 1) / (int64_t(A.dil) * QT);
   const int64_t totA = int64_t(P.m) * 2 * A.Win[0] * A.dil * ngA;
   const int64_t totB = int64_t(P.m) * 4 * A.dil * ngB * A.Wout[1];
+  if (totA >= (int64_t(1) << 31) || totB >= (int64_t(1) << 31)) return cudaErrorInvalidValue;   // 32-bit indices
   tmpl_passA<Real, L2><<<grid_for(totA), kBlock, 0, st>>>(P, A, P.J, level);
   if (P.d == 2) tmpl_passB<Real, L2><<<grid_for(totB), kBlock, 0, st>>>(P, A, P.J, level);
+  return cudaSuccess;
 }
 
 template <typename Real>
 static cudaError_t launch_tmpl_r(const Plan& P, const TmplArgs& A, int level, cudaStream_t st) {
   switch (P.L2) {
-    case 2: launch_tmpl_t<Real, 2>(P, A, level, st); break;
-    case 4: launch_tmpl_t<Real, 4>(P, A, level, st); break;
-    case 6: launch_tmpl_t<Real, 6>(P, A, level, st); break;
-    case 8: launch_tmpl_t<Real, 8>(P, A, level, st); break;
-    case 10: launch_tmpl_t<Real, 10>(P, A, level, st); break;
-    case 12: launch_tmpl_t<Real, 12>(P, A, level, st); break;
-    case 14: launch_tmpl_t<Real, 14>(P, A, level, st); break;
-    case 16: launch_tmpl_t<Real, 16>(P, A, level, st); break;
-    case 18: launch_tmpl_t<Real, 18>(P, A, level, st); break;
-    case 20: launch_tmpl_t<Real, 20>(P, A, level, st); break;
+    case 2: if (cudaError_t e = launch_tmpl_t<Real, 2>(P, A, level, st)) return e; break;
+    case 4: if (cudaError_t e = launch_tmpl_t<Real, 4>(P, A, level, st)) return e; break;
+    case 6: if (cudaError_t e = launch_tmpl_t<Real, 6>(P, A, level, st)) return e; break;
+    case 8: if (cudaError_t e = launch_tmpl_t<Real, 8>(P, A, level, st)) return e; break;
+    case 10: if (cudaError_t e = launch_tmpl_t<Real, 10>(P, A, level, st)) return e; break;
+    case 12: if (cudaError_t e = launch_tmpl_t<Real, 12>(P, A, level, st)) return e; break;
+    case 14: if (cudaError_t e = launch_tmpl_t<Real, 14>(P, A, level, st)) return e; break;
+    case 16: if (cudaError_t e = launch_tmpl_t<Real, 16>(P, A, level, st)) return e; break;
+    case 18: if (cudaError_t e = launch_tmpl_t<Real, 18>(P, A, level, st)) return e; break;
+    case 20: if (cudaError_t e = launch_tmpl_t<Real, 20>(P, A, level, st)) return e; break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
