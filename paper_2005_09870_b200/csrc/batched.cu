@@ -1132,28 +1132,23 @@ __global__ void __launch_bounds__(kB) bk_tail(const __grid_constant__ Plan P, co
       in1 = a1;
     }
   }
-  // bitonic sort of the row by column, CSR write (bk_write)
-  for (int k = 2; k <= Lp; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < Lp; i += kB) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up2 = (i & k) == 0;
-          const int ci = kc[i], cj = kc[ixj];
-          if ((ci > cj) == up2) {
-            kc[i] = cj; kc[ixj] = ci;
-            const Real t = kv[i]; kv[i] = kv[ixj]; kv[ixj] = t;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  const int64_t row = (unit - A.row0) * P.band_L;
+  // CSR write in column order: the stencil order already is the column order unless a partner wraps around
+  // the torus; then each entry goes to its rank (columns are distinct)
+  const int L = P.band_L;
+  int unsorted = 0;
+  for (int i = tid; i + 1 < L; i += kB) unsorted |= kc[i] > kc[i + 1];
+  unsorted = __syncthreads_or(unsorted);
+  const int64_t row = (unit - A.row0) * L;
   Real* outv = reinterpret_cast<Real*>(A.val);
-  for (int i = tid; i < P.band_L; i += kB) {
-    A.col[row + i] = kc[i];
-    outv[row + i] = kv[i];
+  for (int i = tid; i < L; i += kB) {
+    const int c = kc[i];
+    int rank = i;
+    if (unsorted) {
+      rank = 0;
+      for (int j = 0; j < L; ++j) rank += kc[j] < c;
+    }
+    A.col[row + rank] = c;
+    outv[row + rank] = kv[i];
   }
 }
 
