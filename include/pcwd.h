@@ -132,6 +132,25 @@ int pcwd_decompose_to_host(void* handle, int64_t* row_ptr, int32_t* col, void* v
  * This is the Θ_L z product of Eq. (7).  Enqueued on stream. */
 int pcwd_apply(void* handle, const void* x, void* y, int transpose, void* stream);
 
+/* ---- consumer of the decomposition ------------------------------------ */
+
+/* Periodic orthogonal wavelet transform on the handle's grid, basis and depth:
+ * inverse = 0: out = Ψ* in (coefficients in Λ order, the order of Θ's rows and columns);
+ * inverse = 1: out = Ψ in.  in, out: DEVICE arrays of N values of the handle's dtype, not aliased.
+ * Enqueued on stream (uses handle-owned scratch: one transform or FISTA per handle at a time). */
+int pcwd_wavelet_transform(void* handle, const void* in, void* out, int inverse, void* stream);
+
+/* FISTA in the wavelet domain on the decomposed Θ_L:
+ *   z^(i) = Prox^Σ_{‖·‖_{1,w}}(y^(i) − τ Σ Θ_Lᵀ(Θ_L y^(i) − z0)),  y^(i+1) = z^(i) + (i−1)/(i+2)(z^(i) − z^(i−1)),
+ * z^(0) = y^(1) = 0, for i = 1..iters.  precond = 0: Σ = I (FISTA-W); 1: Σ = diag(Θ_LᵀΘ_L)⁻¹ (FISTA-WP, Jacobi;
+ * reading R-F1 of DESIGN.md).  Prox^Σ is the soft threshold at τ Σ_λλ w[λ].  *tau > 0 is used as the step;
+ * *tau ≤ 0 computes τ = 0.99 / ‖Σ^½ Θ_LᵀΘ_L Σ^½‖₂ (100 power iterations) and returns it in *tau (this
+ * synchronises the stream once).  z0 (= Ψ* f0), w (weights ≥ 0), z_out (= z^(iters)): DEVICE arrays of N values
+ * of the handle's dtype.  Needs a decompose first and world = 1 (the whole Θ on this handle).  Θᵀ products use
+ * atomics: iterates are reproducible to rounding, not bit-exactly. */
+int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int precond, double* tau, void* z_out,
+               void* stream);
+
 int pcwd_info(void* handle, pcwd_info_t* out);
 
 /* Phase timing with CUDA events recorded on the decompose stream around each phase

@@ -84,6 +84,8 @@ struct Handle {
   struct Sink { int64_t width; int32_t* col; char* val; int ob; };
   const Sink* sink = nullptr;       // decompose_to_host: caller buffers the finished rows go to
   int* flag_d = nullptr;            // set_kernels: support check flag
+  void* fbuf = nullptr;             // FISTA / wavelet transform scratch (allocated on first use)
+  size_t fbuf_bytes = 0;
   int64_t rows() const { return hp.row1 - hp.row0; }
 };
 
@@ -114,7 +116,7 @@ bool is_device_ptr(const void* p) {
 
 void free_all(Handle* h) {
   void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->vwrap_d, h->amaps_d, h->gscratch, h->bscratch,
-                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->ustage, h->vstage, h->flag_d};
+                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->ustage, h->vstage, h->flag_d, h->fbuf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->cev) cudaEventDestroy(e);
@@ -1150,6 +1152,70 @@ int pcwd_decompose_to_host(void* handle, int64_t* row_ptr, int32_t* col, void* v
   if (!h->cjoin) CK(cudaEventCreateWithFlags(&h->cjoin, cudaEventDisableTiming));
   CK(cudaEventRecord(h->cjoin, h->cs));
   CK(cudaStreamWaitEvent(st, h->cjoin, 0));
+  return PCWD_OK;
+}
+
+// FISTA / transform scratch: 8 vectors of N compute-type elements + N + 1 doubles, 256-byte aligned slices
+int fista_scratch(Handle* h, char** base, size_t* slice) {
+  const int64_t N = h->hp.P.N;
+  const size_t sl = (size_t(N) * h->hp.out_bytes + 255) & ~size_t(255);
+  const size_t need = 8 * sl + ((size_t(N + 1) * 8 + 255) & ~size_t(255));
+  if (h->fbuf_bytes < need) {
+    if (h->fbuf) cudaFree(h->fbuf);
+    h->fbuf = nullptr;
+    h->fbuf_bytes = 0;
+    CK(dalloc(&h->fbuf, need));
+    h->fbuf_bytes = need;
+  }
+  *base = static_cast<char*>(h->fbuf);
+  *slice = sl;
+  return PCWD_OK;
+}
+
+int pcwd_wavelet_transform(void* handle, const void* in, void* out, int inverse, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !in || !out) return fail(PCWD_E_PARAM, "NULL argument");
+  if (in == out) return fail(PCWD_E_PARAM, "in and out must not alias");
+  CK(cudaSetDevice(h->desc.device));
+  char* base;
+  size_t sl;
+  if (int rc = fista_scratch(h, &base, &sl)) return rc;
+  CK(launch_wavelet_transform(h->hp.P, in, out, base + 6 * sl, base + 7 * sl, inverse, h->hp.out_bytes,
+                              static_cast<cudaStream_t>(stream)));
+  return PCWD_OK;
+}
+
+int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int precond, double* tau, void* z_out,
+               void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !z0 || !w || !z_out || !tau) return fail(PCWD_E_PARAM, "NULL argument");
+  if (!h->decomposed) return fail(PCWD_E_STATE, "decompose first");
+  if (h->rows() != h->hp.P.N) return fail(PCWD_E_STATE, "FISTA needs the whole Θ on one handle (world = 1)");
+  if (iters < 0) return fail(PCWD_E_PARAM, "iters < 0");
+  CK(cudaSetDevice(h->desc.device));
+  char* base;
+  size_t sl;
+  if (int rc = fista_scratch(h, &base, &sl)) return rc;
+  FistaArgs F{};
+  F.N = h->hp.P.N;
+  F.nnz = h->nnz;
+  F.row_ptr = h->row_ptr;
+  F.col = h->col;
+  F.val = h->val;
+  F.z0 = z0;
+  F.w = w;
+  F.y = base;
+  F.zprev = base + sl;
+  F.r = base + 2 * sl;
+  F.g = base + 3 * sl;
+  F.sigma = base + 4 * sl;
+  F.sqrt_sigma = base + 5 * sl;
+  F.dbuf = reinterpret_cast<double*>(base + 8 * sl);
+  F.z_out = z_out;
+  F.iters = iters;
+  F.precond = precond ? 1 : 0;
+  F.power_iters = 100;
+  CK(launch_fista(h->hp.P, F, h->hp.out_bytes, static_cast<cudaStream_t>(stream), tau));
   return PCWD_OK;
 }
 

@@ -148,6 +148,24 @@ constexpr int ap_to(int rb) { return rb == 4 ? 32 : 16; }
 constexpr int ap_ti(int rb, int L2) { return 2 * (ap_to(rb) - 1) + L2; }
 constexpr int ap_bw(int rb, int L2) { return (ap_ti(rb, L2) + 16 / rb - 1 + 16 / rb - 1) / (16 / rb) * (16 / rb); }
 
+// FISTA-W / FISTA-WP on a single-shard CSR Θ (fista.cu).  All arrays device, N entries of the compute type
+// unless noted; dbuf: N + 1 doubles.
+struct FistaArgs {
+  int64_t N, nnz;
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const void* val;
+  const void* z0;     // Ψ* f0
+  const void* w;      // ℓ1 weights w[λ]
+  void *y, *zprev, *r, *g, *sigma, *sqrt_sigma, *z_out;
+  double* dbuf;
+  int iters, precond, power_iters;
+};
+cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t st, double* tau_io);
+// Ψ* (inverse = 0) or Ψ (inverse = 1) of one length-N array on the plan's grid; work0/1: N elements each.
+cudaError_t launch_wavelet_transform(const Plan& P, const void* in, void* out, void* work0, void* work1, int inverse,
+                                     int rb, cudaStream_t st);
+
 cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, const int64_t* workA,
                                 const int64_t* workB, const int64_t* appr0, const int64_t* appr1, int steps,
                                 cudaStream_t st, int* launches);

@@ -53,7 +53,7 @@ EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_m
            "pcwd_copy_csr", "pcwd_apply", "pcwd_info", "pcwd_destroy", "pcwd_error_string",
            "pcwd_last_error", "pcwd_validate", "pcwd_plan_shard", "pcwd_plan_stencil",
            "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile",
-           "pcwd_set_kernels", "pcwd_decompose_to_host"]
+           "pcwd_set_kernels", "pcwd_decompose_to_host", "pcwd_wavelet_transform", "pcwd_fista"]
 
 _lib = None
 
@@ -88,6 +88,8 @@ def lib():
         L.pcwd_launch_profile.argtypes = [vp, ctypes.c_int, i32p, dp, dp, i32p, i32p]
         L.pcwd_set_kernels.argtypes = [vp, vp, vp, vp]
         L.pcwd_decompose_to_host.argtypes = [vp, vp, vp, vp, vp]
+        L.pcwd_wavelet_transform.argtypes = [vp, vp, vp, ctypes.c_int, vp]
+        L.pcwd_fista.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), vp, vp]
         for f in EXPORTS:
             getattr(L, f)  # every declared symbol must exist
         _lib = L
@@ -167,6 +169,23 @@ class Decomposition:
         _check(lib().pcwd_decompose_to_host(self._h, ctypes.c_void_p(_ptr(row_ptr)), ctypes.c_void_p(_ptr(col)),
                                             ctypes.c_void_p(_ptr(val)), ctypes.c_void_p(stream)),
                "pcwd_decompose_to_host")
+
+    def wavelet_transform(self, x, inverse: bool = False, stream: int = 0):
+        """Ψ* x (or Ψ x) on this handle's grid: x a CUDA tensor of N values of the handle's dtype."""
+        import torch
+        out = torch.empty_like(x)
+        _check(lib().pcwd_wavelet_transform(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(out)),
+                                            int(inverse), ctypes.c_void_p(stream)), "pcwd_wavelet_transform")
+        return out
+
+    def fista(self, z0, w, iters: int, precond: bool = False, tau: float = 0.0, stream: int = 0):
+        """FISTA-W (precond=False) / FISTA-WP on the decomposed Θ_L (pcwd_fista); returns (z, τ)."""
+        import torch
+        z = torch.empty_like(z0)
+        t = ctypes.c_double(tau)
+        _check(lib().pcwd_fista(self._h, ctypes.c_void_p(_ptr(z0)), ctypes.c_void_p(_ptr(w)), int(iters), int(precond),
+                                ctypes.byref(t), ctypes.c_void_p(_ptr(z)), ctypes.c_void_p(stream)), "pcwd_fista")
+        return z, t.value
 
     def local_max(self, stream: int = 0) -> float:
         out = ctypes.c_double()
