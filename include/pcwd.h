@@ -129,7 +129,10 @@ int pcwd_decompose_to_host(void* handle, int64_t* row_ptr, int32_t* col, void* v
 
 /* y = Θ_ret x (transpose = 0: x has N entries, y has n_rows) or y = Θ_retᵀ x (transpose = 1:
  * x has n_rows entries, y has N, overwritten).  x, y: DEVICE arrays of type dtype.
- * This is the Θ_L z product of Eq. (7).  Enqueued on stream. */
+ * This is the Θ_L z product of Eq. (7).  Both are gathers (warp per row) in a fixed order:
+ * the transposed product runs on a transposed copy of the CSR (columns' entries in increasing row
+ * order; nnz·(4 + dtype size) bytes plus sort scratch), built by the first transposed call after each
+ * decompose.  Enqueued on stream. */
 int pcwd_apply(void* handle, const void* x, void* y, int transpose, void* stream);
 
 /* ---- consumer of the decomposition ------------------------------------ */
@@ -146,8 +149,9 @@ int pcwd_wavelet_transform(void* handle, const void* in, void* out, int inverse,
  * reading R-F1 of DESIGN.md).  Prox^Σ is the soft threshold at τ Σ_λλ w[λ].  *tau > 0 is used as the step;
  * *tau ≤ 0 computes τ = 0.99 / ‖Σ^½ Θ_LᵀΘ_L Σ^½‖₂ (100 power iterations) and returns it in *tau (this
  * synchronises the stream once).  z0 (= Ψ* f0), w (weights ≥ 0), z_out (= z^(iters)): DEVICE arrays of N values
- * of the handle's dtype.  Needs a decompose first and world = 1 (the whole Θ on this handle).  Θᵀ products use
- * atomics: iterates are reproducible to rounding, not bit-exactly. */
+ * of the handle's dtype.  Needs a decompose first and world = 1 (the whole Θ on this handle).  Θᵀ products are
+ * gathers over a transposed copy of the CSR (built once per decompose, as for pcwd_apply with transpose = 1); the
+ * Jacobi diagonal and the power-iteration norms accumulate in fp64 with atomics. */
 int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int precond, double* tau, void* z_out,
                void* stream);
 

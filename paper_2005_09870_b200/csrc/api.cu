@@ -86,6 +86,13 @@ struct Handle {
   int* flag_d = nullptr;            // set_kernels: support check flag
   void* fbuf = nullptr;             // FISTA / wavelet transform scratch (allocated on first use)
   size_t fbuf_bytes = 0;
+  int64_t* rpT = nullptr;           // Θᵀ as CSR over the columns (apply ᵀ, FISTA), built on first use per decompose
+  int32_t* rowT = nullptr;
+  void* valT = nullptr;
+  void* twork = nullptr;
+  size_t twork_bytes = 0;
+  int64_t tcap = -1;
+  bool tvalid = false;
   int64_t rows() const { return hp.row1 - hp.row0; }
 };
 
@@ -116,7 +123,7 @@ bool is_device_ptr(const void* p) {
 
 void free_all(Handle* h) {
   void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->vwrap_d, h->amaps_d, h->gscratch, h->bscratch,
-                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->ustage, h->vstage, h->flag_d, h->fbuf};
+                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->ustage, h->vstage, h->flag_d, h->fbuf, h->rpT, h->rowT, h->valT, h->twork};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->cev) cudaEventDestroy(e);
@@ -1008,6 +1015,7 @@ int pcwd_decompose(void* handle, void* stream) {
   const int64_t rows = h->rows();
   int rc;
   if (P.retain != PCWD_RETAIN_THRESHOLD || !h->M_set) h->nlaunch = 0;
+  h->tvalid = false;
   auto rec = [&](int i) { if (h->profile) cudaEventRecord(h->ev[i], st); };
   if (P.retain == PCWD_RETAIN_BAND) {
     rec(0);
@@ -1172,6 +1180,30 @@ int fista_scratch(Handle* h, char** base, size_t* slice) {
   return PCWD_OK;
 }
 
+// Θᵀ of the shard's CSR (deterministic order), built once per decompose
+int ensure_transpose(Handle* h, cudaStream_t st) {
+  if (h->tvalid) return PCWD_OK;
+  const int64_t N = h->hp.P.N, nnz = h->nnz;
+  const int vb = h->hp.out_bytes;
+  if (nnz > h->tcap) {
+    void* ptrs[] = {h->rpT, h->rowT, h->valT, h->twork};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    h->rpT = nullptr; h->rowT = nullptr; h->valT = nullptr; h->twork = nullptr;
+    const int64_t cap = std::max<int64_t>(nnz, 1);
+    CK(dalloc(&h->rpT, (N + 1) * sizeof(int64_t)));
+    CK(dalloc(&h->rowT, cap * sizeof(int32_t)));
+    CK(dalloc(&h->valT, cap * vb));
+    h->twork_bytes = csr_transpose_bytes(cap, N, vb) + ((N + 1) * 8 + 255) + (cap * 4 + 255) + (cap * vb + 255);
+    CK(dalloc(&h->twork, h->twork_bytes));
+    h->tcap = cap;
+  }
+  CK(csr_transpose(h->row_ptr, h->col, h->val, h->rows(), nnz, N, vb, h->rpT, h->rowT, h->valT, h->twork,
+                   h->twork_bytes, st));
+  h->tvalid = true;
+  return PCWD_OK;
+}
+
 int pcwd_wavelet_transform(void* handle, const void* in, void* out, int inverse, void* stream) {
   Handle* h = static_cast<Handle*>(handle);
   if (!h || !in || !out) return fail(PCWD_E_PARAM, "NULL argument");
@@ -1212,6 +1244,10 @@ int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int preco
   F.sqrt_sigma = base + 5 * sl;
   F.dbuf = reinterpret_cast<double*>(base + 8 * sl);
   F.z_out = z_out;
+  if (int rc = ensure_transpose(h, static_cast<cudaStream_t>(stream))) return rc;
+  F.row_ptrT = h->rpT;
+  F.rowT = h->rowT;
+  F.valT = h->valT;
   F.iters = iters;
   F.precond = precond ? 1 : 0;
   F.power_iters = 100;
@@ -1224,8 +1260,14 @@ int pcwd_apply(void* handle, const void* x, void* y, int transpose, void* stream
   if (!h || !x || !y) return fail(PCWD_E_PARAM, "NULL argument");
   if (!h->decomposed) return fail(PCWD_E_STATE, "decompose first");
   CK(cudaSetDevice(h->desc.device));
-  CK(launch_spmv(h->row_ptr, h->col, h->val, x, y, h->rows(), h->hp.P.N, transpose, h->hp.out_bytes,
-                 static_cast<cudaStream_t>(stream)));
+  if (transpose) {   // Θᵀ x as a gather over the transposed CSR (deterministic)
+    if (int rc = ensure_transpose(h, static_cast<cudaStream_t>(stream))) return rc;
+    CK(launch_spmv(h->rpT, h->rowT, h->valT, x, y, h->hp.P.N, h->rows(), 0, h->hp.out_bytes,
+                   static_cast<cudaStream_t>(stream)));
+  } else {
+    CK(launch_spmv(h->row_ptr, h->col, h->val, x, y, h->rows(), h->hp.P.N, 0, h->hp.out_bytes,
+                   static_cast<cudaStream_t>(stream)));
+  }
   return PCWD_OK;
 }
 

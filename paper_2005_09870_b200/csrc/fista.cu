@@ -8,6 +8,7 @@
 //   idwt_step   its adjoint (the step is orthogonal), as a gather over the taps that reach each output
 //   fista_*     the iteration of P:1537-1546: z = Prox^Σ(y − τ Σ Θᵀ(Θ y − z0)), y ← z + (i−1)/(i+2)(z − z_prev),
 //               with Σ = I (FISTA-W) or the Jacobi preconditioner diag(ΘᵀΘ)⁻¹ (FISTA-WP, reading R-F1), the
+//               Θᵀ products as gathers over the transposed CSR (deterministic), the
 //               weighted soft threshold as the Σ-metric prox, τ = 0.99 / ‖Σ^½ ΘᵀΘ Σ^½‖₂ by power iteration.
 #include <cstdint>
 
@@ -277,7 +278,7 @@ cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t
           copy_kernel<Real><<<grid_of(N), kFB, 0, st>>>(v, g, N);
         }
         if ((e = launch_spmv(F.row_ptr, F.col, F.val, g, r, N, N, 0, rb, st))) return e;
-        if ((e = launch_spmv(F.row_ptr, F.col, F.val, r, g, N, N, 1, rb, st))) return e;
+        if ((e = launch_spmv(F.row_ptrT, F.rowT, F.valT, r, g, N, N, 0, rb, st))) return e;
         if ((e = cudaMemsetAsync(nrm, 0, sizeof(double), st))) return e;
         scale_norm<Real><<<grid_of(N), kFB, 0, st>>>(g, ssig, r, N, nrm);
         normalize<Real><<<grid_of(N), kFB, 0, st>>>(r, v, N, nrm);
@@ -294,7 +295,7 @@ cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t
     for (int i = 1; i <= F.iters; ++i) {
       if ((e = launch_spmv(F.row_ptr, F.col, F.val, y, r, N, N, 0, rb, st))) return e;    // r = Θ y
       sub_kernel<Real><<<grid_of(N), kFB, 0, st>>>(r, z0, N);                              // r −= z0
-      if ((e = launch_spmv(F.row_ptr, F.col, F.val, r, g, N, N, 1, rb, st))) return e;    // g = Θᵀ r
+      if ((e = launch_spmv(F.row_ptrT, F.rowT, F.valT, r, g, N, N, 0, rb, st))) return e;   // g = Θᵀ r (gather)
       const Real beta = Real(double(i - 1) / double(i + 2));
       fista_update<Real><<<grid_of(N), kFB, 0, st>>>(y, zp, zo, g, w, sig, Real(tau), beta, N);
     }

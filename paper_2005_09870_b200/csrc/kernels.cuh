@@ -155,6 +155,9 @@ struct FistaArgs {
   const int64_t* row_ptr;
   const int32_t* col;
   const void* val;
+  const int64_t* row_ptrT;   // Θᵀ as CSR over the columns (rows of Θ ascending in every column)
+  const int32_t* rowT;
+  const void* valT;
   const void* z0;     // Ψ* f0
   const void* w;      // ℓ1 weights w[λ]
   void *y, *zprev, *r, *g, *sigma, *sqrt_sigma, *z_out;
@@ -206,6 +209,11 @@ cudaError_t launch_row_counts(const int32_t* cnt, int64_t rows, int nsb, int64_t
 cudaError_t launch_max_reduce(const double* x, int64_t n, double* out, cudaStream_t st);
 cudaError_t launch_spmv(const int64_t* row_ptr, const int32_t* col, const void* val, const void* x,
                         void* y, int64_t rows, int64_t N, int transpose, int bytes, cudaStream_t st);
+// Θᵀ of a CSR (rows × ncols) as CSR over the columns, entries of each column in increasing row order (deterministic).
+size_t csr_transpose_bytes(int64_t nnz, int64_t ncols, int vbytes);
+cudaError_t csr_transpose(const int64_t* rp, const int32_t* col, const void* val, int64_t rows, int64_t nnz,
+                          int64_t ncols, int vbytes, int64_t* rpT, int32_t* rowT, void* valT, void* work,
+                          size_t work_bytes, cudaStream_t st);
 cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* tmp, size_t* tmp_bytes,
                                cudaStream_t st);
 
