@@ -262,7 +262,7 @@ def run_ours(args):
         for i, (ms, fma, kind, lev) in enumerate(lp):
             klist[i][0] += ms / len(lp_acc)
             klist[i][1], klist[i][2], klist[i][3] = fma, kind, lev
-    dom = max(klist, key=lambda x: x[0])
+    dom = max(klist, key=lambda x: x[1])   # the launch with the most algorithmic work (coarse levels may overlap)
     ms_units = phase[1] / args.steps
     ms_tmpl = phase[0] / args.steps
     peaks = _peaks()

@@ -36,6 +36,7 @@ struct Launch {
   int64_t appr0[kMaxJ + 1] = {}, appr1[kMaxJ + 1] = {};   // batched: per-step max approximation window
   int steps = 0;
   int gu = 1;       // fine: units per round (chunks of a launch are multiples of it)
+  size_t bs_off = 0;  // batched: byte offset of this launch's slice of the batched scratch
 };
 
 struct Handle {
@@ -58,6 +59,10 @@ struct Handle {
   int64_t gstride = 0;
   void* bscratch = nullptr;
   size_t bscratch_bytes = 0;
+  bool conc = false;                // coarse levels on concurrent streams (each with its own scratch slice)
+  static constexpr int kNCS = 5;
+  cudaStream_t cstream[kNCS] = {};
+  cudaEvent_t efork = nullptr, ejoin[kNCS] = {};
   int ggrid = 0;
   std::vector<Launch> launches;
   int64_t* row_ptr = nullptr;
@@ -132,6 +137,14 @@ void free_all(Handle* h) {
   h->cjoin = nullptr;
   if (h->cs) cudaStreamDestroy(h->cs);
   h->cs = nullptr;
+  for (int i = 0; i < Handle::kNCS; ++i) {
+    if (h->cstream[i]) cudaStreamDestroy(h->cstream[i]);
+    if (h->ejoin[i]) cudaEventDestroy(h->ejoin[i]);
+    h->cstream[i] = nullptr;
+    h->ejoin[i] = nullptr;
+  }
+  if (h->efork) cudaEventDestroy(h->efork);
+  h->efork = nullptr;
 }
 
 template <typename T>
@@ -225,6 +238,7 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
   // copy stream, ordered by an event; the largest level runs first so that the copies start early
   const Handle::Sink* sk = h->sink;
   int ci = 0;
+  cudaStream_t ls = st;   // stream of the current launch
   auto emit = [&](int64_t a, int64_t b) -> int {
     if (!sk || b <= a) return PCWD_OK;
     if (ci >= int(h->cev.size())) {
@@ -233,7 +247,7 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
       h->cev.push_back(e);
     }
     cudaEvent_t e = h->cev[ci++];
-    CK(cudaEventRecord(e, st));
+    CK(cudaEventRecord(e, ls));
     CK(cudaStreamWaitEvent(h->cs, e, 0));
     const int64_t off = (a - h->hp.row0) * sk->width, cnt = (b - a) * sk->width;
     if (sk->col) CK(cudaMemcpyAsync(sk->col + off, h->col + off, cnt * sizeof(int32_t), cudaMemcpyDefault, h->cs));
@@ -242,27 +256,65 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
                          cudaMemcpyDefault, h->cs));
     return PCWD_OK;
   };
+  // coarse (batched) levels are independent: each runs on its own stream with its own scratch slice,
+  // forked from `st` after the templates and joined back before the next non-batched launch
+  const bool conc = h->conc && mode == MODE_BAND;
+  // the fine kernels (on `st`) may also run beside the coarse streams: they share no data (all but the first,
+  // largest one, which runs alone)
+  static const bool overlap = getenv("PCWD_COARSE_OVERLAP") ? atoi(getenv("PCWD_COARSE_OVERLAP")) != 0 : true;
+  bool forked = false;
+  int bi = 0, used = 0;
+  auto fork = [&]() -> int {
+    if (forked) return PCWD_OK;
+    CK(cudaEventRecord(h->efork, st));
+    for (int i = 0; i < Handle::kNCS; ++i) CK(cudaStreamWaitEvent(h->cstream[i], h->efork, 0));
+    forked = true;
+    used = 0;
+    return PCWD_OK;
+  };
+  auto join = [&]() -> int {
+    if (!forked) return PCWD_OK;
+    for (int i = 0; i < used; ++i) {
+      CK(cudaEventRecord(h->ejoin[i], h->cstream[i]));
+      CK(cudaStreamWaitEvent(st, h->ejoin[i], 0));
+    }
+    forked = false;
+    return PCWD_OK;
+  };
   const int nL = int(h->launches.size());
   for (int it = 0; it < nL; ++it) {
-    const int li = sk ? nL - 1 - it : it;
+    // order: the largest level (the finest) first when the output streams to the host or the coarse
+    // levels overlap the other fine levels; it runs alone, then the coarse streams fork beside the rest
+    const int li = (sk || (conc && overlap)) ? nL - 1 - it : it;
     const Launch& L = h->launches[li];
-    if (h->profile) cudaEventRecord(h->lev[2 * li], st);
+    ls = st;
+    if (conc && overlap && it == 1)
+      if (int rc = fork()) return rc;   // after the first launch: coarse streams wait for it only
+    if (L.batched && conc) {
+      if (int rc = fork()) return rc;
+      const int k = bi++ % Handle::kNCS;
+      ls = h->cstream[k];
+      used = std::max(used, k + 1);
+    } else if (forked && !overlap) {
+      if (int rc = join()) return rc;
+    }
+    if (h->profile) cudaEventRecord(h->lev[2 * li], ls);
     struct Rec {   // record the launch's end event on every path out of this iteration
       Handle* h; int i; cudaStream_t st;
       ~Rec() { if (h->profile) cudaEventRecord(h->lev[2 * i + 1], st); }
-    } rec_end{h, li, st};
+    } rec_end{h, li, ls};
     if (L.batched) {
       if (mode != MODE_BAND) return fail(PCWD_E_STATE, "batched launch outside BAND mode");
       BatchArgs B = L.ba;
       B.v = h->v_d;
       B.T = h->T_d;
       B.stencil = h->stencil_d;
-      B.scratch = h->bscratch;
+      B.scratch = static_cast<char*>(h->bscratch) + L.bs_off;
       B.row0 = h->hp.row0;
       B.col = h->col;
       B.val = h->val;
       int nl = 0;
-      CK(launch_band_batched(P, B, h->hp.real_bytes, L.maxX0, L.workA, L.workB, L.appr0, L.appr1, L.steps, st, &nl));
+      CK(launch_band_batched(P, B, h->hp.real_bytes, L.maxX0, L.workA, L.workB, L.appr0, L.appr1, L.steps, ls, &nl));
       h->nlaunch += nl;
       if (int rc = emit(L.u0, L.u1)) return rc;
       continue;
@@ -366,7 +418,7 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     if (mode == MODE_BAND || mode == MODE_FULL)
       if (int rc = emit(L.u0, L.u1)) return rc;
   }
-  return PCWD_OK;
+  return join();
 }
 
 int local_max_impl(Handle* h, cudaStream_t st, double* out) {
@@ -523,6 +575,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     CKB(cudaMemcpy(h->fgeom_d, h->hp.fgeom.data(), h->hp.fgeom.size() * sizeof(FGeom), cudaMemcpyHostToDevice));
   }
   int64_t gmax = 0;
+  h->conc = P.retain == PCWD_RETAIN_BAND && !getenv("PCWD_COARSE_SERIAL");
   auto add_generic = [&](int64_t u0, int64_t u1, int64_t scr) {
     if (u1 <= u0) return;
     size_t bytes = size_t(scr) * rb;
@@ -881,7 +934,12 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           if ((2 * am + B.appr0[st - 1] * B.appr1[st]) * rb <= 64 * 1024) { B.ba.tail_s0 = st; break; }
         }
       }
-      h->bscratch_bytes = std::max(h->bscratch_bytes, size_t(batch) * stride * rb);
+      if (h->conc) {   // concurrent coarse levels: one scratch slice each
+        B.bs_off = h->bscratch_bytes;
+        h->bscratch_bytes += (size_t(batch) * stride * rb + 1023) & ~size_t(1023);
+      } else {
+        h->bscratch_bytes = std::max(h->bscratch_bytes, size_t(batch) * stride * rb);
+      }
       h->launches.push_back(B);
       s = e;
       continue;
@@ -890,6 +948,18 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     s = e;
   }
   if (h->bscratch_bytes) CKB(dalloc(&h->bscratch, h->bscratch_bytes + 1024));   // + vector over-read slack
+  {
+    int nb = 0;
+    for (const Launch& L : h->launches) nb += L.batched;
+    h->conc = h->conc && nb > 1;
+    if (h->conc) {
+      CKB(cudaEventCreateWithFlags(&h->efork, cudaEventDisableTiming));
+      for (int i = 0; i < Handle::kNCS; ++i) {
+        CKB(cudaStreamCreateWithFlags(&h->cstream[i], cudaStreamNonBlocking));
+        CKB(cudaEventCreateWithFlags(&h->ejoin[i], cudaEventDisableTiming));
+      }
+    }
+  }
   {  // TMA maps of the approximation steps: [launch][step - 1][sub-band - first] over the scratch input buffer
     std::vector<CUtensorMap> maps;
     std::vector<size_t> first;
@@ -906,7 +976,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           if (!(st < Sq.steps || st == P.J)) continue;
           Range w0 = unit_window(P, Sq, 0, 0), w1 = unit_window(P, Sq, 1, 0);
           for (int t = 1; t < st; ++t) { w0 = step_out(w0, P.L2, 0); w1 = step_out(w1, P.L2, 0); }
-          char* base = static_cast<char*>(h->bscratch) + ((st & 1) ? Sq.offX0 : Sq.offX1) * rb;
+          char* base = static_cast<char*>(h->bscratch) + L.bs_off + ((st & 1) ? Sq.offX0 : Sq.offX1) * rb;
           const int rc2 = encode_map3(&M[(st - 1) * 4 + i], base, rb, w1.len, w0.len, L.ba.batch, (w1.len + 3) & ~3,
                                       L.ba.stride, BW, TI);
           if (rc2) return bail(PCWD_E_CUDA, "cuTensorMapEncodeTiled (approximation) failed: " + std::to_string(rc2));
