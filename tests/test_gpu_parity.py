@@ -324,3 +324,13 @@ def test_largest_torus_band_fp32():
             units.extend(int(off + x) for x in rng.choice(nl * nl, size=2, replace=False))
     units = sorted(set(units))
     compare(p, g, units, R.rows(p, units), "f32")
+
+
+def test_c5_band_fp64():
+    """The c5 workload in fp64 (fine kernel double configurations, TMA coarse path in double): parity on sampled
+    units at the fp64 bar."""
+    p = C.get("c5")
+    g = run(p, "f64")
+    assert g["nnz"] == p.N * 128
+    units = _sample_units(p, 2, 1, 3, seed=2)
+    compare(p, g, units, R.rows(p, units), "f64")
