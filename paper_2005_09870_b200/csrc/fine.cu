@@ -608,9 +608,9 @@ bool fine_config(int real_bytes, int level, int L2, FineCfg* c) {
     if (level == 2) { *c = wide ? FineCfg{8, 15, 1, 2, 4} : FineCfg{4, 15, 1, 2, 4}; return true; }
     if (level == 3) { *c = wide ? FineCfg{4, 11, 3, 2, 4} : FineCfg{2, 11, 3, 1, 2}; return true; }
   } else {
-    if (level == 1) { *c = FineCfg{4, 11, 1, 1, 4}; return true; }
-    if (level == 2) { *c = FineCfg{2, 15, 1, 1, 2}; return true; }
-    if (level == 3) { *c = FineCfg{1, 11, 3, 1, 1}; return true; }
+    if (level == 1) { *c = FineCfg{4, 11, 1, 4, 4}; return true; }
+    if (level == 2) { *c = FineCfg{2, 15, 1, 4, 2}; return true; }
+    if (level == 3) { *c = FineCfg{2, 11, 3, 4, 2}; return true; }
   }
   return false;
 }
@@ -644,9 +644,9 @@ static cudaError_t launch_fine_l2(const Plan& P, const FineArgs& A, int real_byt
       return launch_fine_t<float, L2, 3, 2, 11, 3, 1, 2, 2>(P, A, grid, smem, st);
     }
   } else {
-    if (level == 1) return launch_fine_t<double, L2, 1, 4, 11, 1, 1, 4, 2>(P, A, grid, smem, st);
-    if (level == 2) return launch_fine_t<double, L2, 2, 2, 15, 1, 1, 2, 2>(P, A, grid, smem, st);
-    if (level == 3) return launch_fine_t<double, L2, 3, 1, 11, 3, 1, 1, 2>(P, A, grid, smem, st);
+    if (level == 1) return launch_fine_t<double, L2, 1, 4, 11, 1, 4, 4, 1>(P, A, grid, smem, st);
+    if (level == 2) return launch_fine_t<double, L2, 2, 2, 15, 1, 4, 2, 2>(P, A, grid, smem, st);
+    if (level == 3) return launch_fine_t<double, L2, 3, 2, 11, 3, 4, 2, 1>(P, A, grid, smem, st);
   }
   return cudaErrorInvalidValue;
 }
