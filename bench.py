@@ -212,7 +212,7 @@ def run_ours(args):
     p = C.get(args.config)
     u_d = torch.from_numpy(p.u).to(dev)
     v_d = torch.from_numpy(p.v).to(dev)
-    spec = Spec(p.d, p.n, p.J, p.h, u_d, v_d, dtype="f32", retain=p.retain, tau_rel=p.tau_rel,
+    spec = Spec(p.d, p.n, p.J, p.h, u_d, v_d, dtype=args.dtype, retain=p.retain, tau_rel=p.tau_rel,
                 band_L=p.band_L, rank=rank, world=world, device=dev)
     dec = Decomposition(spec)
     dec.profile(True)
@@ -268,8 +268,10 @@ def run_ours(args):
     peaks = _peaks()
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # derived: SMs × lanes × 2 × clock
+    if args.dtype == "f64":
+        fp32_peak /= 2.0                                  # FP64 pipe: half the FP32 rate on B200 (ffma_peak: 36 TF)
     achieved = 2.0 * dom[1] / (dom[0] * 1e-3) / 1e12
-    traffic, traffic_src = _ncu_traffic(dom[2], dom[3])
+    traffic, traffic_src = _ncu_traffic(dom[2], dom[3]) if args.dtype == "f32" else (None, None)
     roofline = {"bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": traffic,
                 "traffic_source": f"{traffic_src} (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
@@ -277,7 +279,8 @@ def run_ours(args):
                 "kernel": f"{dom[2]} unit kernel, level {dom[3]} (a2 k-sum + a3 cascade + a4 gather)",
                 "kernel_ms": dom[0], "kernel_share_of_step": dom[0] / ms_per_step,
                 "fma_per_launch": dom[1],
-                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz of MEASURED_PEAKS.json",
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz of MEASURED_PEAKS.json"
+                + (" / 2 (FP64)" if args.dtype == "f64" else ""),
                 "all_unit_kernels": {"ms": ms_units, "tflops": 2.0 * fma3[1] / (ms_units * 1e-3) / 1e12,
                                      "frac": 2.0 * fma3[1] / (ms_units * 1e-3) / 1e12 / fp32_peak},
                 "templates_ms": ms_tmpl,
@@ -298,12 +301,12 @@ def run_ours(args):
         meta = dec.csr_meta()
         rp_h = torch.empty(meta.n_rows + 1, dtype=torch.int64).pin_memory()
         col_h = torch.empty(meta.nnz, dtype=torch.int32).pin_memory()
-        val_h = torch.empty(meta.nnz, dtype=torch.float32).pin_memory()
+        val_h = torch.empty(meta.nnz, dtype=torch.float32 if args.dtype == "f32" else torch.float64).pin_memory()
         from paper_2005_09870_b200 import pcwd as P
         import ctypes
 
         def spec_h():
-            return Spec(p.d, p.n, p.J, p.h, u_h.numpy(), v_h.numpy(), dtype="f32", retain=p.retain,
+            return Spec(p.d, p.n, p.J, p.h, u_h.numpy(), v_h.numpy(), dtype=args.dtype, retain=p.retain,
                         tau_rel=p.tau_rel, band_L=p.band_L, rank=rank, world=world, device=dev)
         dplan = Decomposition(spec_h())
         times = []
@@ -329,7 +332,7 @@ def run_ours(args):
             d2.close()
         e2e = {"value": meta.nnz / t_e2e * (nnz_all / max(nnz, 1)), "unit": "entries/s",
                "h2d_bytes_per_step": int(p.u.nbytes + p.v.nbytes),
-               "d2h_bytes_per_step": int(rp_h.numel() * 8 + col_h.numel() * 4 + val_h.numel() * 4),
+               "d2h_bytes_per_step": int(rp_h.numel() * 8 + col_h.numel() * 4 + val_h.numel() * val_h.element_size()),
                "ms_per_step": t_e2e * 1e3, "calls": "pcwd_set_kernels + pcwd_decompose_to_host (plan built once)",
                "with_create_ms": statistics.median(times_c[1:]) * 1e3,
                "timing": "wall clock, synchronize on both sides, median"}
@@ -340,7 +343,7 @@ def run_ours(args):
             cb, _ = cpu_oracle_rate(p, budget_s=15.0)
         line = {"metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "scaling": "strong", "vs_baseline": None, "dtype": args.dtype,
                 "data": "synthetic (seeded, synth/configs.py; no dataset in the paper's path)",
                 "config": {"workload": WORKLOAD.get(args.config, args.config), "config": args.config,
                            "units": p.N, "retained_per_unit": p.band_L, "nnz": nnz_all,
@@ -364,6 +367,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"], help="compute dtype (the headline is f32)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
