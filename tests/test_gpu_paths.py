@@ -1,0 +1,70 @@
+"""GPU: the alternative kernel paths (environment switches read once per process, so each runs in a
+subprocess) give the same CSR as the default path on c3 and a 128² fp64 case: pattern bit-exact, values within
+the fp32 / fp64 rounding of a different summation order.  The default path is the one the oracle parity tests
+check; these keep the fallbacks (non-TMA k-sum, cp.async approximation steps, no tail, serial coarse levels,
+no fine kernel, no direct partners, generic kernels) correct."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2005_09870_b200 import Decomposition, Spec
+from synth import configs as C
+name, dtype, out = sys.argv[1], sys.argv[2], sys.argv[3]
+p = C.get(name) if name.startswith("c") else C.micro(128, 2, 4, 5, 3, 4, 45, retain="band", band_L=64)
+dec = Decomposition(Spec(p.d, p.n, p.J, p.h, p.u, p.v, dtype=dtype, retain=p.retain, tau_rel=p.tau_rel,
+                         band_L=p.band_L))
+dec.decompose()
+rp, col, val = (t.numpy() for t in dec.csr(device="cpu"))
+np.savez(out, rp=rp, col=col, val=val.astype(np.float64))
+"""
+
+SWITCHES = [
+    {"PCWD_NO_TMA_KSUM": "1"},
+    {"PCWD_NO_TMA_APPROX": "1"},
+    {"PCWD_NO_TAIL": "1"},
+    {"PCWD_COARSE_SERIAL": "1"},
+    {"PCWD_COARSE_OVERLAP": "0"},
+    {"PCWD_NO_FINE": "1"},
+    {"PCWD_NO_DIRECT": "1"},
+    {"PCWD_FINE_DIRECT": "1,1,1"},
+    {"PCWD_NO_FINE": "1", "PCWD_NO_TILE": "1", "PCWD_NO_BATCHED": "1"},
+]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2005_09870_b200 import _build
+    _build.build()
+
+
+def _run(tmp_path, name, dtype, env):
+    out = str(tmp_path / f"{name}_{dtype}_{abs(hash(tuple(sorted(env.items()))))}.npz")
+    e = dict(os.environ)
+    e.update(env)
+    subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT), name, dtype, out], env=e, check=True,
+                   timeout=600)
+    return np.load(out)
+
+
+@pytest.mark.parametrize("case", [("c3", "f32"), ("micro128", "f64")], ids=["c3-f32", "128-f64"])
+@pytest.mark.parametrize("env", SWITCHES, ids=["+".join(f"{k}={v}" for k, v in s.items()) for s in SWITCHES])
+def test_switch_matches_default_path(tmp_path, case, env):
+    name, dtype = case
+    ref = _run(tmp_path, name, dtype, {})
+    got = _run(tmp_path, name, dtype, env)
+    assert np.array_equal(got["rp"], ref["rp"]) and np.array_equal(got["col"], ref["col"])
+    err = np.linalg.norm(got["val"] - ref["val"]) / np.linalg.norm(ref["val"])
+    assert err <= (2e-6 if dtype == "f32" else 1e-13), err
