@@ -324,7 +324,11 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     // step descriptors: the class record's FStep fields translated to this unit (lane-parallel).
     // field layout (FStep): 0 xr 1 xrl 2 xc 3 xcl 4 ar 5 arl 6 hlo 7 hlen 8 glo 9 glen
     //                       10+ec blo0  14+ec blen0  18+ec blo1  22+ec blen1  26+ec doff
-    for (int i = gt; i < steps * 32; i += GT) {
+    // only what is read: every field of the cascade steps 1..S1, and the input box (fields 0-3) of step S1 + 1
+    // (the X_{S1} box of the direct partners)
+    const int S1 = steps <= A.direct ? 1 : steps - A.direct;   // A.direct levels (≤ 2) computed directly in the gather
+    const int nfield = S1 * 32 + (S1 < steps ? 4 : 0);
+    for (int i = gt; i < nfield; i += GT) {
       const int si = i >> 5, fi = i & 31;
       int val = 0;
       if (fi < 30) {
@@ -346,7 +350,6 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     // cascade steps 1..S1; the partners of the last two levels are computed in the gather directly from the
     // step-S1 approximation (2δ × 2δ taps for level S1 + 1, composite (3·2δ − 2)² taps for S1 + 2), which
     // replaces the two smallest, latency-bound cascade steps
-    const int S1 = steps <= A.direct ? 1 : steps - A.direct;   // A.direct levels (≤ 2) computed directly in the gather
     int steps_run = (A.dbg_flags & 2) ? 0 : (A.dbg_flags & 4) ? 1 : steps;   // debug: skip cascade steps
     steps_run = min(steps_run, S1);
     for (int s = 1; s <= steps_run; ++s) {
