@@ -281,6 +281,16 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     forked = false;
     return PCWD_OK;
   };
+  struct JoinGuard {   // on an error return the coarse streams are still joined back into `st`
+    Handle* h; cudaStream_t st; bool* forked; int* used;
+    ~JoinGuard() {
+      if (!*forked) return;
+      for (int i = 0; i < *used; ++i) {
+        cudaEventRecord(h->ejoin[i], h->cstream[i]);
+        cudaStreamWaitEvent(st, h->ejoin[i], 0);
+      }
+    }
+  } join_guard{h, st, &forked, &used};
   const int nL = int(h->launches.size());
   for (int it = 0; it < nL; ++it) {
     // order: the largest level (the finest) first when the output streams to the host or the coarse

@@ -830,11 +830,7 @@ static void launch_approx_tma_t(const Plan& P, const BatchArgs& A, int s, int nt
   constexpr int XSZ = (TI * BW + 128 / RB - 1) / (128 / RB) * (128 / RB);
   constexpr size_t smem = size_t(RB) * (2 * XSZ + TO * (TI | 1)) + 128;
   auto k = bk_approx_tma<Real, L2, TO>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
-  }
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));   // per device, cheap
   const int ntiles = ntx * nty;
   const int tpc = ntiles <= 4 ? ntiles : (ntiles <= 16 ? 4 : 6);
   k<<<dim3((ntiles + tpc - 1) / tpc, nb), kB, smem, st>>>(P, A, s, ntx, ntiles, tpc);
@@ -1162,11 +1158,7 @@ static void launch_tiled_t(const Plan& P, const BatchArgs& A, dim3 grid, int nti
   constexpr int VS = SH * (GZ + G - 1) + VW;
   constexpr size_t smem = sizeof(Real) * 2 * (size_t(TR) * TW + size_t(TR) * VS);
   auto k = bk_ksum_tiled<Real, LEV, G, GZ>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
-  }
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));   // per device, cheap
   k<<<grid, kB, smem, st>>>(P, A, ntile1);
 }
 
@@ -1174,11 +1166,7 @@ template <typename Real, int LEV, int G, int GZ>
 static void launch_tma_t(const Plan& P, const BatchArgs& A, dim3 grid, int ntile1, cudaStream_t st) {
   constexpr size_t smem = ksum_tma_smem<Real, LEV, G, GZ>();
   auto k = bk_ksum_tma<Real, LEV, G, GZ>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = true;
-  }
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));   // per device, cheap
   BatchArgs B = A;
   B.kt_flags = getenv("PCWD_KT_FLAGS") ? atoi(getenv("PCWD_KT_FLAGS")) : 0;
   if (getenv("PCWD_KT_LEVMASK") && !((atoi(getenv("PCWD_KT_LEVMASK")) >> LEV) & 1)) B.kt_flags |= 1;
@@ -1258,11 +1246,7 @@ static bool launch_ksum_full(const Plan& P, const BatchArgs& A, int nb, cudaStre
   if (A.kf_rows == 2 && lev == 8 && (nl == 4 || nl == 2) && !getenv("PCWD_NO_TMA_KSUM")) {
     auto launch = [&](auto kern, int NLV) {
       const size_t smem = sizeof(Real) * 3 * size_t(2 * NLV - 1 + NLV) * 2 * 256 + 128;
-      static bool attr[2] = {false, false};
-      if (!attr[NLV == 4]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr[NLV == 4] = true;
-      }
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       kern<<<dim3(P.n / 2, nb / NLV), kB, smem, st>>>(P, A);
     };
     if (nl == 4) launch(bk_ksum_full_tma<Real, 4, 2>, 4);
