@@ -415,8 +415,9 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
 
   // shard: contiguous unit ranges (Λ order) with equal estimated time.  A unit's time is its algorithmic
   // FMA count times a per-path weight: time per algorithmic FMA of each level's kernel path relative to
-  // the fine level-1 kernel, measured on B200 at c5 (profiles/r01, build r1d: fine ℓ = 1, 2, 3 at 1.0,
-  // 0.9, 1.5; batched ℓ = 4..7 at 1.36, 1.18, 1.05, 1.26; whole-torus windows 2.65).  The template chain up
+  // the fine level-1 kernel, measured on B200 at c5 (profiles/r01: fine ℓ = 1, 2, 3 at 1.0, 0.9, 1.5;
+  // batched ℓ = 4..7 at 1.36, 1.06, 0.95, 1.13, whole-torus windows 2.4 — ℓ ≥ 5 at the r1d figures × 0.9, the coarse
+  // levels of a shard running on concurrent streams since r1f).  The template chain up
   // to level ℓ is charged to the first unit of level ℓ (its owner builds it).  Boundaries are rounded to
   // 16 units so every shard keeps whole rounds of the fine and tiled kernels.
   std::vector<double> ucost(ns, 0.0), lump(ns, 0.0);
@@ -424,8 +425,8 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
     const SubBand& S = P.sb[s];
     double w = 1.0;
     if (P.retain == PCWD_RETAIN_BAND) {
-      static const double wl[8] = {1.0, 1.0, 0.9, 1.5, 1.36, 1.18, 1.05, 1.26};
-      w = S.any_full ? 2.65 : wl[std::min(S.level, 7)];
+      static const double wl[8] = {1.0, 1.0, 0.9, 1.5, 1.36, 1.06, 0.95, 1.13};
+      w = S.any_full ? 2.4 : wl[std::min(S.level, 7)];
     }
     ucost[s] = S.fma * w;
   }
