@@ -334,3 +334,17 @@ def test_c5_band_fp64():
     assert g["nnz"] == p.N * 128
     units = _sample_units(p, 2, 1, 3, seed=2)
     compare(p, g, units, R.rows(p, units), "f64")
+
+
+@pytest.mark.parametrize("retain", ["band", "full"])
+def test_zero_filter_gives_exact_zeros(retain):
+    """u = 0 (empty support: the plan's window degenerates to one point): the retained pattern is unchanged
+    and every value is exactly 0."""
+    p = C.micro(16, 2, 4, 3, 2, 2, 47, retain=retain, band_L=24 if retain == "band" else 0)
+    p.u = np.zeros_like(p.u)
+    g = run(p, "f32")
+    assert g["nnz"] == p.N * (24 if retain == "band" else p.N) and np.all(g["val"] == 0.0)
+    if retain == "band":
+        ref = ret.band_pattern_dense(p, 24)
+        for mu in (0, 5, p.N - 1):
+            assert np.array_equal(g["col"][g["rp"][mu]:g["rp"][mu + 1]], ref[mu])
