@@ -147,7 +147,7 @@ int pcwd_wavelet_transform(void* handle, const void* in, void* out, int inverse,
  *   z^(i) = Prox^Σ_{‖·‖_{1,w}}(y^(i) − τ Σ Θ_Lᵀ(Θ_L y^(i) − z0)),  y^(i+1) = z^(i) + (i−1)/(i+2)(z^(i) − z^(i−1)),
  * z^(0) = y^(1) = 0, for i = 1..iters.  precond = 0: Σ = I (FISTA-W); 1: Σ = diag(Θ_LᵀΘ_L)⁻¹ (FISTA-WP, Jacobi;
  * reading R-F1 of DESIGN.md).  Prox^Σ is the soft threshold at τ Σ_λλ w[λ].  *tau > 0 is used as the step;
- * *tau ≤ 0 computes τ = 0.99 / ‖Σ^½ Θ_LᵀΘ_L Σ^½‖₂ (100 power iterations) and returns it in *tau (this
+ * *tau ≤ 0 computes τ = 0.99 / ‖Σ^½ Θ_LᵀΘ_L Σ^½‖₂ (power iteration until ‖M v‖ changes by < 1e-6 over 8 steps, at most 100) and returns it in *tau (this
  * synchronises the stream once).  z0 (= Ψ* f0), w (weights ≥ 0), z_out (= z^(iters)): DEVICE arrays of N values
  * of the handle's dtype.  Needs a decompose first and world = 1 (the whole Θ on this handle).  Θᵀ products are
  * gathers over a transposed copy of the CSR (built once per decompose, as for pcwd_apply with transpose = 1); the

@@ -1330,7 +1330,7 @@ int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int preco
   F.valT = h->valT;
   F.iters = iters;
   F.precond = precond ? 1 : 0;
-  F.power_iters = 100;
+  F.power_iters = 100;   // at most; stops earlier when ‖M v‖ settles (relative change < 1e-6 over 8 iterations)
   CK(launch_fista(h->hp.P, F, h->hp.out_bytes, static_cast<cudaStream_t>(stream), tau));
   return PCWD_OK;
 }

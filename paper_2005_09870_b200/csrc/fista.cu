@@ -282,6 +282,14 @@ cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t
         if ((e = cudaMemsetAsync(nrm, 0, sizeof(double), st))) return e;
         scale_norm<Real><<<grid_of(N), kFB, 0, st>>>(g, ssig, r, N, nrm);
         normalize<Real><<<grid_of(N), kFB, 0, st>>>(r, v, N, nrm);
+        // every 8 iterations: stop once ‖M v‖ changes by less than 1e-6 (relative)
+        if ((it + 1) % 8 == 0 && it + 1 < F.power_iters) {
+          double cur = 0.0;
+          if ((e = cudaMemcpyAsync(&cur, nrm, sizeof(double), cudaMemcpyDeviceToHost, st))) return e;
+          if ((e = cudaStreamSynchronize(st))) return e;
+          if (lam > 0.0 && fabs(cur - lam) <= 1e-6 * cur) break;
+          lam = cur;
+        }
       }
       if ((e = cudaMemcpyAsync(&lam, nrm, sizeof(double), cudaMemcpyDeviceToHost, st))) return e;
       if ((e = cudaStreamSynchronize(st))) return e;
