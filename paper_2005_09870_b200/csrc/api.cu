@@ -75,6 +75,8 @@ struct Handle {
   void* cubtmp = nullptr;
   size_t cubbytes = 0;
   double* dmax = nullptr;
+  double* cand = nullptr;           // THRESHOLD store-then-filter: candidate values (hp.cand_total fp64)
+  bool cand_valid = false;
   double M = 0.0;
   bool M_set = false, tmpl_fresh = false, decomposed = false;
   int nlaunch = 0;
@@ -128,7 +130,7 @@ bool is_device_ptr(const void* p) {
 
 void free_all(Handle* h) {
   void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->vwrap_d, h->amaps_d, h->gscratch, h->bscratch,
-                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->ustage, h->vstage, h->flag_d, h->fbuf, h->rpT, h->rowT, h->valT, h->twork};
+                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->cand, h->ustage, h->vstage, h->flag_d, h->fbuf, h->rpT, h->rowT, h->valT, h->twork};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->cev) cudaEventDestroy(e);
@@ -423,6 +425,7 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     A.cnt = h->cnt;
     A.tau = tau;
     A.use_smem = L.smem > 0;
+    A.cand = h->cand;
     CK(launch_units(P, A, mode, h->hp.real_bytes, h->hp.out_bytes, L.grid, L.smem, st));
     h->nlaunch++;
     if (mode == MODE_BAND || mode == MODE_FULL)
@@ -434,8 +437,11 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
 int local_max_impl(Handle* h, cudaStream_t st, double* out) {
   int rc = build_templates(h, st);
   if (rc) return rc;
-  rc = run_units(h, MODE_TMAX, st, 0.0);
+  // with a candidate buffer the one cascade pass also stores every structural partner (store-then-filter:
+  // the count and write passes then only read it); without one, they recompute the cascade
+  rc = run_units(h, h->cand ? MODE_TSTORE : MODE_TMAX, st, 0.0);
   if (rc) return rc;
+  h->cand_valid = h->cand != nullptr;
   CK(launch_max_reduce(h->unitmax, h->rows(), h->dmax, st));
   h->nlaunch++;
   CK(cudaMemcpyAsync(out, h->dmax, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1057,6 +1063,13 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     h->cubbytes = tb;
     CKB(dalloc(&h->cubtmp, tb));
     h->cap = 0;
+    // store-then-filter buffer: if it does not fit, the count / write passes recompute
+    if (h->hp.cand_total > 0 && !getenv("PCWD_NO_CAND")) {
+      if (dalloc(&h->cand, size_t(h->hp.cand_total) * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        h->cand = nullptr;
+      }
+    }
   }
   if (h->cap > 0) {
     CKB(dalloc(&h->col, h->cap * sizeof(int32_t)));
@@ -1135,7 +1148,12 @@ int pcwd_decompose(void* handle, void* stream) {
     }
     const double tau = h->desc.tau_rel * h->M;
     CK(cudaMemsetAsync(h->cnt, 0, size_t(std::max<int64_t>(rows * P.nsb, 1)) * sizeof(int32_t), st));
-    if ((rc = run_units(h, MODE_TCOUNT, st, tau))) return rc;
+    if (h->cand_valid) {
+      CK(launch_cand_filter(P, h->cand, h->hp.row0, rows, tau, 0, h->cnt, nullptr, nullptr, nullptr, h->hp.out_bytes, st));
+      h->nlaunch++;
+    } else if ((rc = run_units(h, MODE_TCOUNT, st, tau))) {
+      return rc;
+    }
     CK(launch_row_counts(h->cnt, rows, P.nsb, h->rowcnt, st));
     size_t tb = h->cubbytes;
     CK(exclusive_scan_i64(h->rowcnt, h->row_ptr, rows + 1, h->cubtmp, &tb, st));
@@ -1154,9 +1172,16 @@ int pcwd_decompose(void* handle, void* stream) {
       h->cap = cap;
     }
     h->nnz = nnz;
-    if ((rc = run_units(h, MODE_TWRITE, st, tau))) return rc;
+    if (h->cand_valid) {
+      CK(launch_cand_filter(P, h->cand, h->hp.row0, rows, tau, 1, h->cnt, h->row_ptr, h->col, h->val,
+                            h->hp.out_bytes, st));
+      h->nlaunch++;
+    } else if ((rc = run_units(h, MODE_TWRITE, st, tau))) {
+      return rc;
+    }
     h->M_set = false;
     h->tmpl_fresh = false;
+    h->cand_valid = false;
   }
   h->decomposed = true;
   return PCWD_OK;
@@ -1214,6 +1239,7 @@ int pcwd_set_kernels(void* handle, const double* u, const double* v, void* strea
   else CK(launch_cast(static_cast<const double*>(h->vstage), h->v_d, mN, 4, st));
   h->M_set = false;
   h->tmpl_fresh = false;
+  h->cand_valid = false;
   h->decomposed = false;
   return PCWD_OK;
 }

@@ -25,7 +25,7 @@ constexpr int kMaxJ = 16;
 constexpr int kMaxSB = 1 + 3 * kMaxJ;
 constexpr int kMaxTaps = 20;
 
-enum Mode : int { MODE_FULL = 0, MODE_BAND = 1, MODE_TMAX = 2, MODE_TCOUNT = 3, MODE_TWRITE = 4 };
+enum Mode : int { MODE_FULL = 0, MODE_BAND = 1, MODE_TMAX = 2, MODE_TCOUNT = 3, MODE_TWRITE = 4, MODE_TSTORE = 5 };
 
 struct Range {
   int lo, len, nl;
@@ -95,6 +95,8 @@ struct SubBand {
   int64_t wk_offY, wk_offD, wk_offStage, wk_scratch;
   double fma;       // algorithmic FMA per unit (k-sum + cascade, max windows)
   int fg_off, fg_m; // fine path: first geometry record of this sub-band, class modulus per axis (geom.h)
+  // THRESHOLD store-then-filter: candidate slot of this sub-band's first shard unit, and per-unit slot size
+  int64_t cand_off, cand_slot;
 };
 
 struct Plan {

@@ -260,6 +260,9 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
     Real* nxt = X1;
     Range in0 = r0, in1 = r1;
     double tmax = 0.0;
+    int64_t crun = 0;   // TSTORE: candidates of this unit stored so far
+    double* cbase = nullptr;
+    if (MODE == MODE_TSTORE) cbase = A.cand + S.cand_off + (unit - (S.offset > A.row0 ? S.offset : A.row0)) * S.cand_slot;
     for (int s = 1; s <= S.steps; ++s) {
       const Range a0 = D == 2 ? step_out(in0, L2, 0) : Range{0, 1, 1};
       const Range d0 = D == 2 ? step_out(in0, L2, 1) : Range{0, 1, 1};
@@ -379,6 +382,18 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
           const int tot = w[wi].r0.len * w[wi].r1.len;
           for (int idx = tid; idx < tot; idx += kBlock) tmax = fmax(tmax, fabs(double(w[wi].buf[idx])));
         }
+      } else if (MODE == MODE_TSTORE) {   // TMAX + every value stored in column (sorted) order
+        for (int wi = 0; wi < nw; ++wi) {
+          const OutWin<Real>& W = w[wi];
+          const int tot = W.r0.len * W.r1.len;
+          for (int k = tid; k < tot; k += kBlock) {
+            const int ks0 = k / W.r1.len, ks1 = k - ks0 * W.r1.len;
+            const double x = double(W.buf[sorted_to_local(W.r0, ks0) * W.r1.len + sorted_to_local(W.r1, ks1)]);
+            tmax = fmax(tmax, fabs(x));
+            cbase[crun + k] = x;
+          }
+          crun += tot;
+        }
       } else if (MODE == MODE_TCOUNT) {
         for (int wi = 0; wi < nw; ++wi) {
           int c = 0;
@@ -451,9 +466,94 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
         A.col[base + j] = stage_col[j];
         outv[base + j] = OutT(stage_val[j]);
       }
-    } else if (MODE == MODE_TMAX) {
+    } else if (MODE == MODE_TMAX || MODE == MODE_TSTORE) {
       const double mx = block_reduce_max(tmax, red_d);
       if (tid == 0) A.unitmax[row] = mx;
+    }
+    __syncthreads();
+  }
+}
+
+// THRESHOLD store-then-filter: one CTA per unit walks the unit's window chain (the emission order of unit_kernel)
+// over the candidates MODE_TSTORE stored in column order; WRITE = 0 counts per (unit, sub-band) the values with
+// |x| ≥ tau (cnt), WRITE = 1 compacts them into the CSR (row_ptr from the counts).
+template <typename OutT, int D, int WRITE>
+__global__ void __launch_bounds__(kBlock) cand_filter_kernel(const __grid_constant__ Plan P, const double* __restrict__ cand,
+                                                             int64_t row0, int64_t rows, double tau, int32_t* cnt,
+                                                             const int64_t* __restrict__ row_ptr, int32_t* col, OutT* val) {
+  __shared__ int red_i[kBlock / 32];
+  using BlockScan = cub::BlockScan<int, kBlock>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  const int tid = threadIdx.x, L2 = P.L2;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t unit = row0 + row;
+    const int sbi = find_subband(P, unit);
+    const SubBand& S = P.sb[sbi];
+    const int64_t pos = unit - S.offset;
+    const int p0 = D == 2 ? int(pos / S.nl) : 0;
+    const int p1 = D == 2 ? int(pos - int64_t(p0) * S.nl) : int(pos);
+    Range in0 = D == 2 ? unit_window(P, S, 0, p0) : Range{0, 1, 1};
+    Range in1 = unit_window(P, S, 1, p1);
+    const double* cb = cand + S.cand_off + (unit - (S.offset > row0 ? S.offset : row0)) * S.cand_slot;
+    int64_t crun = 0;
+    int64_t base = 0;
+    if (WRITE) base = row_ptr[row];
+    for (int s = 1; s <= S.steps; ++s) {
+      const Range a0 = D == 2 ? step_out(in0, L2, 0) : Range{0, 1, 1};
+      const Range d0 = D == 2 ? step_out(in0, L2, 1) : Range{0, 1, 1};
+      const Range a1 = step_out(in1, L2, 0);
+      const Range d1 = step_out(in1, L2, 1);
+      Range wr0[4], wr1[4];
+      int wsb[4], nw = 0;
+      const int base_sb = 1 + (P.J - s) * (D == 2 ? 3 : 1);
+      if (D == 2) {
+        wr0[nw] = a0; wr1[nw] = d1; wsb[nw++] = base_sb + 0;
+        wr0[nw] = d0; wr1[nw] = a1; wsb[nw++] = base_sb + 1;
+        wr0[nw] = d0; wr1[nw] = d1; wsb[nw++] = base_sb + 2;
+      } else {
+        wr0[nw] = Range{0, 1, 1}; wr1[nw] = d1; wsb[nw++] = base_sb;
+      }
+      if (s == P.J) { wr0[nw] = a0; wr1[nw] = a1; wsb[nw++] = 0; }
+      for (int wi = 0; wi < nw; ++wi) {
+        const int tot = wr0[wi].len * wr1[wi].len;
+        const double* cw = cb + crun;
+        if (!WRITE) {
+          int c = 0;
+          for (int k = tid; k < tot; k += kBlock) c += fabs(cw[k]) >= tau;
+          c = block_reduce_sum(c, red_i);
+          if (tid == 0) cnt[row * P.nsb + wsb[wi]] = c;
+        } else {
+          const SubBand& L = P.sb[wsb[wi]];
+          int64_t b = base;
+          for (int q = 0; q < wsb[wi]; ++q) b += cnt[row * P.nsb + q];
+          int running = 0;
+          for (int k0 = 0; k0 < tot; k0 += kBlock) {
+            const int k = k0 + tid;
+            int keep = 0, colv = 0;
+            double x = 0.0;
+            if (k < tot) {
+              x = cw[k];
+              keep = fabs(x) >= tau;
+              const int ks0 = k / wr1[wi].len, ks1 = k - ks0 * wr1[wi].len;
+              const int i0 = sorted_to_local(wr0[wi], ks0), i1 = sorted_to_local(wr1[wi], ks1);
+              const int g0 = (wr0[wi].lo + i0) & (wr0[wi].nl - 1);
+              const int g1 = (wr1[wi].lo + i1) & (wr1[wi].nl - 1);
+              colv = int(L.offset + int64_t(g0) * L.nl + g1);
+            }
+            int posn, agg;
+            BlockScan(scan_tmp).ExclusiveSum(keep, posn, agg);
+            if (keep) {
+              col[b + running + posn] = colv;
+              val[b + running + posn] = OutT(x);
+            }
+            running += agg;
+            __syncthreads();
+          }
+        }
+        crun += tot;
+      }
+      in0 = a0;
+      in1 = a1;
     }
     __syncthreads();
   }
@@ -629,6 +729,8 @@ cudaError_t launch_units(const Plan& P, const UnitArgs& A, int mode, int real_by
                              : launch_d<double, double, MODE_BAND>(P, A, grid, smem, st);
     case MODE_TMAX:
       return launch_d<double, double, MODE_TMAX>(P, A, grid, smem, st);
+    case MODE_TSTORE:
+      return launch_d<double, double, MODE_TSTORE>(P, A, grid, smem, st);
     case MODE_TCOUNT:
       return launch_d<double, double, MODE_TCOUNT>(P, A, grid, smem, st);
     case MODE_TWRITE:
@@ -647,6 +749,23 @@ cudaError_t launch_fill_band_rowptr(int64_t* row_ptr, int64_t rows, int64_t L, c
 
 cudaError_t launch_fill_full(int64_t* row_ptr, int32_t* col, int64_t rows, int64_t N, cudaStream_t st) {
   fill_full<<<grid_for(rows * N), kBlock, 0, st>>>(row_ptr, col, rows, N);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cand_filter(const Plan& P, const double* cand, int64_t row0, int64_t rows, double tau, int write,
+                               int32_t* cnt, const int64_t* row_ptr, int32_t* col, void* val, int out_bytes,
+                               cudaStream_t st) {
+  const int grid = int(std::min<int64_t>(std::max<int64_t>(rows, 1), 148 * 8));
+  if (rows <= 0) return cudaSuccess;
+#define PCWD_CF(OT, DD, W) cand_filter_kernel<OT, DD, W><<<grid, kBlock, 0, st>>>(P, cand, row0, rows, tau, cnt, row_ptr, col, static_cast<OT*>(val))
+  if (!write) {
+    if (P.d == 2) PCWD_CF(double, 2, 0); else PCWD_CF(double, 1, 0);
+  } else if (out_bytes == 4) {
+    if (P.d == 2) PCWD_CF(float, 2, 1); else PCWD_CF(float, 1, 1);
+  } else {
+    if (P.d == 2) PCWD_CF(double, 2, 1); else PCWD_CF(double, 1, 1);
+  }
+#undef PCWD_CF
   return cudaGetLastError();
 }
 

@@ -23,6 +23,7 @@ struct UnitArgs {
   int32_t* cnt;             // TCOUNT / TWRITE: [row][sb]
   double tau;               // threshold (fp64)
   int use_smem;
+  double* cand;             // TSTORE: every structural partner value of the unit, window by window in column order
 };
 
 struct TileArgs {
@@ -205,6 +206,10 @@ size_t unit_smem_limit();
 cudaError_t set_unit_smem_attr(size_t bytes);
 cudaError_t launch_fill_band_rowptr(int64_t* row_ptr, int64_t rows, int64_t L, cudaStream_t st);
 cudaError_t launch_fill_full(int64_t* row_ptr, int32_t* col, int64_t rows, int64_t N, cudaStream_t st);
+// THRESHOLD store-then-filter: per unit of the shard, count / write the candidates ≥ tau stored by MODE_TSTORE.
+cudaError_t launch_cand_filter(const Plan& P, const double* cand, int64_t row0, int64_t rows, double tau, int write,
+                               int32_t* cnt, const int64_t* row_ptr, int32_t* col, void* val, int out_bytes,
+                               cudaStream_t st);
 cudaError_t launch_row_counts(const int32_t* cnt, int64_t rows, int nsb, int64_t* rowcnt, cudaStream_t st);
 cudaError_t launch_max_reduce(const double* x, int64_t n, double* out, cudaStream_t st);
 cudaError_t launch_spmv(const int64_t* row_ptr, const int32_t* col, const void* val, const void* x,

@@ -453,6 +453,38 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
   hp->row0 = d->rank == 0 ? 0 : align16(unit_at_cost(total * d->rank / d->world));
   hp->row1 = d->rank == d->world - 1 ? P.N : align16(unit_at_cost(total * (d->rank + 1) / d->world));
   if (hp->row1 < hp->row0) hp->row1 = hp->row0;
+  // THRESHOLD store-then-filter: every structural partner value of a unit (the windows the cascade emits, in
+  // emission order) gets a slot; per sub-band, the slot is the per-axis worst case over positions
+  hp->cand_total = 0;
+  if (d->retain == PCWD_RETAIN_THRESHOLD) {
+    for (int s = 0; s < ns; ++s) {
+      SubBand& S = P.sb[s];
+      int mA[2][kMaxJ + 1] = {}, mD[2][kMaxJ + 1] = {};
+      for (int a = (P.d == 2 ? 0 : 1); a < 2; ++a)
+        for (int p = 0; p < S.nl; ++p) {
+          Range in = unit_window(P, S, a, p);
+          for (int st = 1; st <= S.steps; ++st) {
+            const Range ra = step_out(in, L2, 0), rd = step_out(in, L2, 1);
+            mA[a][st] = std::max(mA[a][st], ra.len);
+            mD[a][st] = std::max(mD[a][st], rd.len);
+            in = ra;
+          }
+        }
+      int64_t slot = 0;
+      for (int st = 1; st <= S.steps; ++st) {
+        if (P.d == 2) {
+          slot += int64_t(mA[0][st]) * mD[1][st] + int64_t(mD[0][st]) * mA[1][st] + int64_t(mD[0][st]) * mD[1][st];
+          if (st == J) slot += int64_t(mA[0][st]) * mA[1][st];
+        } else {
+          slot += mD[1][st] + (st == J ? mA[1][st] : 0);
+        }
+      }
+      const int64_t a0 = std::max(hp->row0, S.offset), a1 = std::min(hp->row1, S.offset + S.count);
+      S.cand_slot = slot;
+      S.cand_off = hp->cand_total;
+      if (a1 > a0) hp->cand_total += (a1 - a0) * slot;
+    }
+  }
   double f = 0.0;
   for (int s = 0; s < ns; ++s) {
     int64_t a = std::max(hp->row0, P.sb[s].offset);

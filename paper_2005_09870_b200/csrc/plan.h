@@ -30,6 +30,7 @@ struct HostPlan {
   double fma_templates = 0.0;
   double tmpl_fma_level[kMaxJ + 1] = {};   // template FMAs of each level's à-trous step
   std::vector<FGeom> fgeom;       // BAND, fine levels: class geometry records (SubBand::fg_off / fg_m)
+  int64_t cand_total = 0;         // THRESHOLD: candidate slots of the shard (store-then-filter), fp64 values
 };
 
 // Returns a pcwd_status; msg receives the reason on error.

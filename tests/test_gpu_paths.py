@@ -59,6 +59,16 @@ def _run(tmp_path, name, dtype, env):
     return np.load(out)
 
 
+def test_threshold_recompute_matches_store_then_filter(tmp_path):
+    """Threshold rule: the count / write passes recomputing the cascade (PCWD_NO_CAND) give the CSR the
+    store-then-filter path gives (the same fp64 values, bit for bit)."""
+    for name, dtype in (("c2", "f32"), ("c2", "f64")):
+        ref = _run(tmp_path, name, dtype, {})
+        got = _run(tmp_path, name, dtype, {"PCWD_NO_CAND": "1"})
+        for k in ("rp", "col", "val"):
+            assert np.array_equal(got[k], ref[k])
+
+
 @pytest.mark.parametrize("case", [("c3", "f32"), ("micro128", "f64")], ids=["c3-f32", "128-f64"])
 @pytest.mark.parametrize("env", SWITCHES, ids=["+".join(f"{k}={v}" for k, v in s.items()) for s in SWITCHES])
 def test_switch_matches_default_path(tmp_path, case, env):
