@@ -269,9 +269,17 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
       const Range a1 = step_out(in1, L2, 0);
       const Range d1 = step_out(in1, L2, 1);
       int s01 = 0, s10 = 0;
+      // window addressing: a window clear of wrapping (len + 2·2δ ≤ line) by a signed offset from its start, a
+      // whole-line window modulo the line, otherwise local_index per tap
+      auto kind = [&](const Range& r) { return r.len >= r.nl ? 1 : (r.len + 2 * L2 <= r.nl ? 0 : 2); };
+      auto sdiff = [&](int g, const Range& r) {
+        int dd = (g - r.lo) & (r.nl - 1);
+        return dd >= r.nl - 2 * L2 ? dd - r.nl : dd;
+      };
       if (D == 2) {
         const int ycols = a1.len + d1.len;
         const int totA = in0.len * ycols;
+        const int k1 = kind(in1);
         for (int idx = tid; idx < totA; idx += kBlock) {       // pass A: axis 1
           const int i0 = idx / ycols, j = idx - i0 * ycols;
           const int e1 = j >= a1.len;
@@ -280,14 +288,26 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
           const int q = 2 * (R.lo + jj) + P.to[e1];
           const Real* line = cur + i0 * in1.len;
           Real acc = Real(0);
+          if (k1 == 0) {
+            const int dq = sdiff(q, in1);
 #pragma unroll 4
-          for (int t = 0; t < L2; ++t) {
-            const int c = local_index(in1, q + t);
-            if (c >= 0) acc = fmaT(TapsOf<Real>::get(P, e1, t), line[c], acc);
+            for (int t = 0; t < L2; ++t)
+              if (unsigned(dq + t) < unsigned(in1.len)) acc = fmaT(TapsOf<Real>::get(P, e1, t), line[dq + t], acc);
+          } else if (k1 == 1) {
+#pragma unroll 4
+            for (int t = 0; t < L2; ++t)
+              acc = fmaT(TapsOf<Real>::get(P, e1, t), line[(q + t - in1.lo) & (in1.nl - 1)], acc);
+          } else {
+#pragma unroll 4
+            for (int t = 0; t < L2; ++t) {
+              const int c = local_index(in1, q + t);
+              if (c >= 0) acc = fmaT(TapsOf<Real>::get(P, e1, t), line[c], acc);
+            }
           }
           Y[idx] = acc;
         }
         __syncthreads();
+        const int k0 = kind(in0);
         const int s00 = a0.len * a1.len;
         s01 = a0.len * d1.len;
         s10 = d0.len * a1.len;
@@ -304,10 +324,21 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
           const int q = 2 * (R.lo + j0) + P.to[e0];
           const int colY = (e1 ? a1.len : 0) + j1;
           Real acc = Real(0);
+          if (k0 == 0) {
+            const int dq = sdiff(q, in0);
 #pragma unroll 4
-          for (int t = 0; t < L2; ++t) {
-            const int r = local_index(in0, q + t);
-            if (r >= 0) acc = fmaT(TapsOf<Real>::get(P, e0, t), Y[r * ycols + colY], acc);
+            for (int t = 0; t < L2; ++t)
+              if (unsigned(dq + t) < unsigned(in0.len)) acc = fmaT(TapsOf<Real>::get(P, e0, t), Y[(dq + t) * ycols + colY], acc);
+          } else if (k0 == 1) {
+#pragma unroll 4
+            for (int t = 0; t < L2; ++t)
+              acc = fmaT(TapsOf<Real>::get(P, e0, t), Y[((q + t - in0.lo) & (in0.nl - 1)) * ycols + colY], acc);
+          } else {
+#pragma unroll 4
+            for (int t = 0; t < L2; ++t) {
+              const int r = local_index(in0, q + t);
+              if (r >= 0) acc = fmaT(TapsOf<Real>::get(P, e0, t), Y[r * ycols + colY], acc);
+            }
           }
           *dst = acc;
         }
