@@ -596,13 +596,15 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     if (u1 <= u0) return;
     size_t bytes = size_t(scr) * rb;
     Launch L{u0, u1, 0, 0};
-    if (bytes <= budget) {
+    // shared-memory scratch only while ≥ 3 units fit per SM; larger windows work in global (L2) scratch with
+    // 4 units per SM in flight
+    if (bytes <= std::min<size_t>(budget, 72 * 1024)) {
       L.smem = std::max<size_t>(bytes, 16);
       int per_sm = int(std::min<size_t>(8, (228 * 1024) / (L.smem + 2048)));
       per_sm = std::max(per_sm, 1);
       L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * per_sm));
     } else {
-      L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * 2));
+      L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * 4));
       gmax = std::max(gmax, scr);
       h->ggrid = std::max(h->ggrid, L.grid);
     }

@@ -505,18 +505,18 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
   }
 }
 
-// THRESHOLD store-then-filter: one CTA per unit walks the unit's window chain (the emission order of unit_kernel)
+// THRESHOLD store-then-filter: one warp per unit walks the unit's window chain (the emission order of unit_kernel)
 // over the candidates MODE_TSTORE stored in column order; WRITE = 0 counts per (unit, sub-band) the values with
-// |x| ≥ tau (cnt), WRITE = 1 compacts them into the CSR (row_ptr from the counts).
+// |x| ≥ tau (cnt), WRITE = 1 compacts them into the CSR (row_ptr from the counts) with ballot / popc.
 template <typename OutT, int D, int WRITE>
 __global__ void __launch_bounds__(kBlock) cand_filter_kernel(const __grid_constant__ Plan P, const double* __restrict__ cand,
                                                              int64_t row0, int64_t rows, double tau, int32_t* cnt,
                                                              const int64_t* __restrict__ row_ptr, int32_t* col, OutT* val) {
-  __shared__ int red_i[kBlock / 32];
-  using BlockScan = cub::BlockScan<int, kBlock>;
-  __shared__ typename BlockScan::TempStorage scan_tmp;
-  const int tid = threadIdx.x, L2 = P.L2;
-  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+  const int lane = threadIdx.x & 31, L2 = P.L2;
+  const int64_t warp0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t row = warp0; row < rows; row += nwarps) {
     const int64_t unit = row0 + row;
     const int sbi = find_subband(P, unit);
     const SubBand& S = P.sb[sbi];
@@ -550,16 +550,16 @@ __global__ void __launch_bounds__(kBlock) cand_filter_kernel(const __grid_consta
         const double* cw = cb + crun;
         if (!WRITE) {
           int c = 0;
-          for (int k = tid; k < tot; k += kBlock) c += fabs(cw[k]) >= tau;
-          c = block_reduce_sum(c, red_i);
-          if (tid == 0) cnt[row * P.nsb + wsb[wi]] = c;
+          for (int k = lane; k < tot; k += 32) c += fabs(cw[k]) >= tau;
+          c = __reduce_add_sync(0xffffffffu, c);
+          if (lane == 0) cnt[row * P.nsb + wsb[wi]] = c;
         } else {
           const SubBand& L = P.sb[wsb[wi]];
           int64_t b = base;
           for (int q = 0; q < wsb[wi]; ++q) b += cnt[row * P.nsb + q];
           int running = 0;
-          for (int k0 = 0; k0 < tot; k0 += kBlock) {
-            const int k = k0 + tid;
+          for (int k0 = 0; k0 < tot; k0 += 32) {
+            const int k = k0 + lane;
             int keep = 0, colv = 0;
             double x = 0.0;
             if (k < tot) {
@@ -571,14 +571,13 @@ __global__ void __launch_bounds__(kBlock) cand_filter_kernel(const __grid_consta
               const int g1 = (wr1[wi].lo + i1) & (wr1[wi].nl - 1);
               colv = int(L.offset + int64_t(g0) * L.nl + g1);
             }
-            int posn, agg;
-            BlockScan(scan_tmp).ExclusiveSum(keep, posn, agg);
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (keep) {
+              const int posn = __popc(m & lt);
               col[b + running + posn] = colv;
               val[b + running + posn] = OutT(x);
             }
-            running += agg;
-            __syncthreads();
+            running += __popc(m);
           }
         }
         crun += tot;
@@ -586,7 +585,6 @@ __global__ void __launch_bounds__(kBlock) cand_filter_kernel(const __grid_consta
       in0 = a0;
       in1 = a1;
     }
-    __syncthreads();
   }
 }
 
@@ -786,7 +784,7 @@ cudaError_t launch_fill_full(int64_t* row_ptr, int32_t* col, int64_t rows, int64
 cudaError_t launch_cand_filter(const Plan& P, const double* cand, int64_t row0, int64_t rows, double tau, int write,
                                int32_t* cnt, const int64_t* row_ptr, int32_t* col, void* val, int out_bytes,
                                cudaStream_t st) {
-  const int grid = int(std::min<int64_t>(std::max<int64_t>(rows, 1), 148 * 8));
+  const int grid = int(std::min<int64_t>((std::max<int64_t>(rows, 1) * 32 + kBlock - 1) / kBlock, 148 * 16));
   if (rows <= 0) return cudaSuccess;
 #define PCWD_CF(OT, DD, W) cand_filter_kernel<OT, DD, W><<<grid, kBlock, 0, st>>>(P, cand, row0, rows, tau, cnt, row_ptr, col, static_cast<OT*>(val))
   if (!write) {
