@@ -37,6 +37,7 @@ struct Launch {
   int steps = 0;
   int gu = 1;       // fine: units per round (chunks of a launch are multiples of it)
   size_t bs_off = 0;  // batched: byte offset of this launch's slice of the batched scratch
+  int64_t gs_off = -1, gs_stride = 0;   // generic, global scratch: element offset of this launch's slice, per-CTA stride
 };
 
 struct Handle {
@@ -60,6 +61,7 @@ struct Handle {
   void* bscratch = nullptr;
   size_t bscratch_bytes = 0;
   bool conc = false;                // coarse levels on concurrent streams (each with its own scratch slice)
+  bool conc_t = false;              // threshold rule: the generic launches of the one cascade pass on concurrent streams
   static constexpr int kNCS = 5;
   cudaStream_t cstream[kNCS] = {};
   cudaEvent_t efork = nullptr, ejoin[kNCS] = {};
@@ -261,6 +263,7 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
   // coarse (batched) levels are independent: each runs on its own stream with its own scratch slice,
   // forked from `st` after the templates and joined back before the next non-batched launch
   const bool conc = h->conc && mode == MODE_BAND;
+  const bool conc_t = h->conc_t && (mode == MODE_TSTORE || mode == MODE_TMAX);
   // the fine kernels (on `st`) may also run beside the coarse streams: they share no data (all but the first,
   // largest one, which runs alone)
   static const bool overlap = getenv("PCWD_COARSE_OVERLAP") ? atoi(getenv("PCWD_COARSE_OVERLAP")) != 0 : true;
@@ -302,7 +305,12 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     ls = st;
     if (conc && overlap && it == 1)
       if (int rc = fork()) return rc;   // after the first launch: coarse streams wait for it only
-    if (L.batched && conc) {
+    if (conc_t) {   // threshold rule's cascade pass: every level on its own stream (own scratch slices)
+      if (int rc = fork()) return rc;
+      const int k = bi++ % Handle::kNCS;
+      ls = h->cstream[k];
+      used = std::max(used, k + 1);
+    } else if (L.batched && conc) {
       if (int rc = fork()) return rc;
       const int k = bi++ % Handle::kNCS;
       ls = h->cstream[k];
@@ -413,8 +421,8 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     A.v = h->v_d;
     A.T = h->T_d;
     A.stencil = h->stencil_d;
-    A.gscratch = h->gscratch;
-    A.gscratch_stride = h->gstride;
+    A.gscratch = L.gs_off >= 0 ? static_cast<char*>(h->gscratch) + size_t(L.gs_off) * h->hp.real_bytes : nullptr;
+    A.gscratch_stride = L.gs_stride;
     A.u0 = L.u0;
     A.u1 = L.u1;
     A.row0 = h->hp.row0;
@@ -426,7 +434,7 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     A.tau = tau;
     A.use_smem = L.smem > 0;
     A.cand = h->cand;
-    CK(launch_units(P, A, mode, h->hp.real_bytes, h->hp.out_bytes, L.grid, L.smem, st));
+    CK(launch_units(P, A, mode, h->hp.real_bytes, h->hp.out_bytes, L.grid, L.smem, ls));
     h->nlaunch++;
     if (mode == MODE_BAND || mode == MODE_FULL)
       if (int rc = emit(L.u0, L.u1)) return rc;
@@ -603,10 +611,11 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       int per_sm = int(std::min<size_t>(8, (228 * 1024) / (L.smem + 2048)));
       per_sm = std::max(per_sm, 1);
       L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * per_sm));
-    } else {
+    } else {   // its own slice of the global scratch (launches may run concurrently)
       L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * 4));
-      gmax = std::max(gmax, scr);
-      h->ggrid = std::max(h->ggrid, L.grid);
+      L.gs_stride = (scr + 31) & ~int64_t(31);
+      L.gs_off = gmax;
+      gmax += L.gs_stride * L.grid;
     }
     h->launches.push_back(L);
   };
@@ -970,7 +979,10 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     int nb = 0;
     for (const Launch& L : h->launches) nb += L.batched;
     h->conc = h->conc && nb > 1;
-    if (h->conc) {
+    int ng = 0;
+    for (const Launch& L : h->launches) ng += !L.batched && !L.fine && !L.tile;
+    h->conc_t = P.retain == PCWD_RETAIN_THRESHOLD && ng > 1 && !getenv("PCWD_COARSE_SERIAL");
+    if (h->conc || h->conc_t) {
       CKB(cudaEventCreateWithFlags(&h->efork, cudaEventDisableTiming));
       for (int i = 0; i < Handle::kNCS; ++i) {
         CKB(cudaStreamCreateWithFlags(&h->cstream[i], cudaStreamNonBlocking));
@@ -1043,10 +1055,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       }
     }
   }
-  if (gmax > 0) {
-    h->gstride = (gmax + 31) & ~int64_t(31);
-    CKB(dalloc(&h->gscratch, size_t(h->gstride) * h->ggrid * rb));
-  }
+  if (gmax > 0) CKB(dalloc(&h->gscratch, size_t(gmax) * rb));
 
   // output CSR
   const int64_t rows = h->rows();
