@@ -57,7 +57,6 @@ struct Handle {
   int kt_pr = 0, kt_pc = 0, kt_offx = 0;
   int vpad = 0;
   void* gscratch = nullptr;
-  int64_t gstride = 0;
   void* bscratch = nullptr;
   size_t bscratch_bytes = 0;
   bool conc = false;                // coarse levels on concurrent streams (each with its own scratch slice)
@@ -65,7 +64,6 @@ struct Handle {
   static constexpr int kNCS = 5;
   cudaStream_t cstream[kNCS] = {};
   cudaEvent_t efork = nullptr, ejoin[kNCS] = {};
-  int ggrid = 0;
   std::vector<Launch> launches;
   int64_t* row_ptr = nullptr;
   int32_t* col = nullptr;
