@@ -869,7 +869,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       B.batched = 1;
       int64_t stride = (scr + 31) & ~int64_t(31);
       // batch so that the per-unit slots stay L2-resident next to v and the templates
-      static const size_t cap = size_t(getenv("PCWD_BATCH_MB") ? atol(getenv("PCWD_BATCH_MB")) : 8192) << 20;
+      static const size_t cap = size_t(getenv("PCWD_BATCH_MB") ? atol(getenv("PCWD_BATCH_MB")) : 32768) << 20;
       int64_t batch = std::max<int64_t>(1, std::min<int64_t>(u1 - u0, int64_t(cap / (size_t(stride) * rb))));
       batch = std::min<int64_t>(batch, 65535);
       B.ba.stride = stride;
@@ -902,7 +902,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       // tiled k-sum with TMA staging (levels ≤ 5): maps of the level's templates here, of the periodically
       // extended v once its extent (max strip over the levels) is known
       B.level = lev;
-      static const int tma_maxlev = getenv("PCWD_TMA_KSUM_MAXLEV") ? atoi(getenv("PCWD_TMA_KSUM_MAXLEV")) : 7;
+      static const int tma_maxlev = getenv("PCWD_TMA_KSUM_MAXLEV") ? atoi(getenv("PCWD_TMA_KSUM_MAXLEV")) : 8;
       const int gz = lev <= tma_maxlev && !getenv("PCWD_NO_TMA_KSUM") ? ksum_tiled_gz(P, u0, u1, rb) : 0;
       if (gz) {
         const int SH = 1 << lev, TR = 256 / SH, G = kt_units(rb);

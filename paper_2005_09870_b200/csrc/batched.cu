@@ -1179,7 +1179,7 @@ int ksum_tiled_gz(const Plan& P, int64_t u0, int64_t u1, int real_bytes) {
   const int s0 = find_subband_host(P, u0), s1 = find_subband_host(P, u1 - 1);
   const SubBand& S = P.sb[s0];
   const int lev = S.level;
-  if (lev < 3 || lev > 7 || S.nl % G || (u0 - S.offset) % G || (u1 - u0) % G) return 0;
+  if (lev < 3 || lev > 8 || S.nl % G || (u0 - S.offset) % G || (u1 - u0) % G) return 0;
   for (int q = s0; q <= s1; ++q)
     if (P.sb[q].level != lev || P.sb[q].tW[0] >= P.n || P.sb[q].tW[1] >= P.n || P.sb[q].tW[0] != S.tW[0] ||
         P.sb[q].tW[1] != S.tW[1] || P.sb[q].e == 0)
@@ -1223,9 +1223,10 @@ static bool launch_ksum_tiled(const Plan& P, const BatchArgs& A, int nb, cudaStr
     PCWD_KT(5, 8) PCWD_KT(5, 9) PCWD_KT(5, 10) PCWD_KT(5, 6) PCWD_KT(5, 5) PCWD_KT(5, 4)
     PCWD_KT(6, 8) PCWD_KT(6, 9) PCWD_KT(6, 10) PCWD_KT(6, 6) PCWD_KT(6, 5) PCWD_KT(6, 4)
     PCWD_KT(7, 8) PCWD_KT(7, 9) PCWD_KT(7, 10) PCWD_KT(7, 6) PCWD_KT(7, 5) PCWD_KT(7, 4)
+    PCWD_KT(8, 8) PCWD_KT(8, 9) PCWD_KT(8, 10) PCWD_KT(8, 6) PCWD_KT(8, 5) PCWD_KT(8, 4)
   } else {
     PCWD_KT(3, 4) PCWD_KT(3, 2) PCWD_KT(4, 4) PCWD_KT(4, 2) PCWD_KT(5, 4) PCWD_KT(5, 2)
-    PCWD_KT(6, 4) PCWD_KT(6, 2) PCWD_KT(7, 4) PCWD_KT(7, 2)
+    PCWD_KT(6, 4) PCWD_KT(6, 2) PCWD_KT(7, 4) PCWD_KT(7, 2) PCWD_KT(8, 4) PCWD_KT(8, 2)
   }
 #undef PCWD_KT
   return false;
