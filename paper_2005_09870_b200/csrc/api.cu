@@ -920,16 +920,21 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       }
       B.ba.kt_sb_first = s;
       // whole-torus k-sum with TMA (2^ℓ = 256, a sub-band row of 2 or 4 units): v and template maps, 256 × 2 boxes
-      if (!gz && P.d == 2 && lev == 8 && (1 << lev) * P.sb[s].nl == P.n && (P.sb[s].nl == 4 || P.sb[s].nl == 2) &&
-          e - s <= 4 && !getenv("PCWD_NO_TMA_KSUM")) {
+      // (2^ℓ = 256·SHM with SHM ∈ {1, 2, 4}: rows per thread 2 at SHM = 1, else 1)
+      const int kshm = lev >= 8 && lev <= 10 ? (1 << lev) / 256 : 0;
+      const int knl = P.sb[s].nl;
+      const bool kf_ok = (kshm == 1 && (knl == 2 || knl == 4)) || (kshm == 2 && (knl == 2 || knl == 4)) ||
+                         (kshm == 4 && knl == 2);
+      if (!gz && P.d == 2 && kf_ok && (1 << lev) * knl == P.n && e - s <= 4 && !getenv("PCWD_NO_TMA_KSUM")) {
+        const int trt = kshm == 1 ? 2 : 1;
         bool full = true;
         for (int q = s; q < e; ++q) full = full && P.sb[q].tW[0] >= P.n && P.sb[q].tW[1] >= P.n;
-        int rc2 = full ? encode_map3(&B.ba.tmV, h->v_d, rb, P.n, P.n, P.m, P.n, int64_t(P.n) * P.n, 256, 2) : 1;
+        int rc2 = full ? encode_map3(&B.ba.tmV, h->v_d, rb, P.n, P.n, P.m, P.n, int64_t(P.n) * P.n, 256, trt) : 1;
         for (int q = s, i = 0; full && q < e && !rc2; ++q, ++i)
           rc2 = encode_map3(&B.ba.tmT[i], static_cast<char*>(h->T_d) + P.sb[q].toff * rb, rb, P.sb[q].tRS, P.n, P.m,
-                            P.sb[q].tRS, P.sb[q].tstride, 256, 2);
+                            P.sb[q].tRS, P.sb[q].tstride, 256, trt);
         if (full && rc2) return bail(PCWD_E_CUDA, "cuTensorMapEncodeTiled (whole-torus k-sum) failed: " + std::to_string(rc2));
-        if (full) B.ba.kf_rows = 2;
+        if (full) B.ba.kf_rows = trt;
       }
       // approximation steps on the TMA path: every participating sub-band's step-s input window has one size
       // over its units and stays clear of wrapping (maps encoded once the scratch exists)

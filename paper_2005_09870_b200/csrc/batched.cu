@@ -317,15 +317,15 @@ constexpr size_t ksum_tma_smem() {
   return sizeof(Real) * 3 * size_t(NTB * TR * SH * QT + NVB * VBOX) + 128;
 }
 
-// Whole-torus k-sum with TMA staging, for 2^ℓ = 256 (n = 256·NL): as bk_ksum_full (units of a sub-band row
-// share the v row; template columns shifted by 2^ℓ u), but a thread owns TRT rows, and the v rows (NL boxes of
-// 256 columns) and the template strip (2NL − 1 boxes of 256 columns, each starting on a multiple of 256 so
-// none crosses the torus seam) are TMA boxes in a 3-stage mbarrier ring.
-template <typename Real, int NL, int TRT>
+// Whole-torus k-sum with TMA staging, for 2^ℓ = 256·SHM (n = 2^ℓ·NL): as bk_ksum_full (units of a sub-band row
+// share the v row; template columns shifted by 2^ℓ u), but a thread owns TRT rows and SHM residues (tid + 256 r),
+// and the v rows (NL·SHM boxes of 256 columns) and the template strip ((2NL − 1)·SHM boxes of 256 columns, each
+// starting on a multiple of 256 so none crosses the torus seam) are TMA boxes in a 3-stage mbarrier ring.
+template <typename Real, int NL, int TRT, int SHM>
 __global__ void __launch_bounds__(kB) bk_ksum_full_tma(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A) {
-  constexpr int SH = 256, G = NL, NTS = NL + G - 1;
-  constexpr int BOX = TRT * SH;                     // elements per box
-  constexpr int STAGE = (NL + NTS) * BOX;
+  constexpr int SH = 256 * SHM, G = NL, NTS = NL + G - 1;
+  constexpr int BOX = TRT * 256;                    // elements per box (256 columns × TRT rows)
+  constexpr int STAGE = (NL + NTS) * SHM * BOX;
   constexpr int NST = 3;
   extern __shared__ __align__(16) unsigned char kfm[];
   __shared__ unsigned long long full[NST];
@@ -350,42 +350,46 @@ __global__ void __launch_bounds__(kB) bk_ksum_full_tma(const __grid_constant__ P
       Real* b = stg + (k % NST) * STAGE;
       mbar_expect_tx(&full[k % NST], unsigned(sizeof(Real) * STAGE));
 #pragma unroll
-      for (int i = 0; i < NL; ++i) tma_load_3d(b + i * BOX, &A.tmV, i * SH, z0, k, &full[k % NST]);
+      for (int i = 0; i < NL * SHM; ++i) tma_load_3d(b + i * BOX, &A.tmV, i * 256, z0, k, &full[k % NST]);
 #pragma unroll
-      for (int j = 0; j < NTS; ++j)
-        tma_load_3d(b + (NL + j) * BOX, tmT, (x0 + j * SH) & mask, yt, k, &full[k % NST]);
+      for (int j = 0; j < NTS * SHM; ++j)
+        tma_load_3d(b + (NL * SHM + j) * BOX, tmT, (x0 + j * 256) & mask, yt, k, &full[k % NST]);
     }
   };
-  Real acc[TRT][G][NL];
+  Real acc[TRT][SHM][G][NL];
 #pragma unroll
   for (int t = 0; t < TRT; ++t)
 #pragma unroll
-    for (int u = 0; u < G; ++u)
+    for (int r2 = 0; r2 < SHM; ++r2)
 #pragma unroll
-      for (int i = 0; i < NL; ++i) acc[t][u][i] = Real(0);
+      for (int u = 0; u < G; ++u)
+#pragma unroll
+        for (int i = 0; i < NL; ++i) acc[t][r2][u][i] = Real(0);
 #pragma unroll
   for (int q = 0; q < NST - 1; ++q) issue(q);
   for (int k = 0; k < P.m; ++k) {
     issue(k + NST - 1);
     mbar_wait(&full[k % NST], unsigned(k / NST) & 1u);
     const Real* Vb = stg + (k % NST) * STAGE;
-    const Real* Tb = Vb + NL * BOX;
+    const Real* Tb = Vb + NL * SHM * BOX;
 #pragma unroll
-    for (int t = 0; t < TRT; ++t) {
-      Real vv[NL];
+    for (int t = 0; t < TRT; ++t)
 #pragma unroll
-      for (int i = 0; i < NL; ++i) vv[i] = Vb[i * BOX + t * SH + tid];
-      // unit u, column tid + SH i: strip chunk i − u + G − 1
+      for (int r2 = 0; r2 < SHM; ++r2) {
+        Real vv[NL];
 #pragma unroll
-      for (int mm = 0; mm < NTS; ++mm) {
-        const Real tm = Tb[mm * BOX + t * SH + tid];
+        for (int i = 0; i < NL; ++i) vv[i] = Vb[(i * SHM + r2) * BOX + t * 256 + tid];
+        // unit u, column (tid + 256 r2) + SH i: strip chunk i − u + G − 1
 #pragma unroll
-        for (int u = 0; u < G; ++u) {
-          const int i = mm + u - (G - 1);
-          if (i >= 0 && i < NL) acc[t][u][i] = fmaB(vv[i], tm, acc[t][u][i]);
+        for (int mm = 0; mm < NTS; ++mm) {
+          const Real tm = Tb[(mm * SHM + r2) * BOX + t * 256 + tid];
+#pragma unroll
+          for (int u = 0; u < G; ++u) {
+            const int i = mm + u - (G - 1);
+            if (i >= 0 && i < NL) acc[t][r2][u][i] = fmaB(vv[i], tm, acc[t][r2][u][i]);
+          }
         }
       }
-    }
     __syncthreads();   // stage k % NST is refilled by issue(k + NST) next iteration
   }
   const int rs = rstride(n);
@@ -395,7 +399,9 @@ __global__ void __launch_bounds__(kB) bk_ksum_full_tma(const __grid_constant__ P
 #pragma unroll
     for (int t = 0; t < TRT; ++t)
 #pragma unroll
-      for (int i = 0; i < NL; ++i) X0[int64_t(z0 + t) * rs + tid + SH * i] = acc[t][u][i];
+      for (int r2 = 0; r2 < SHM; ++r2)
+#pragma unroll
+        for (int i = 0; i < NL; ++i) X0[int64_t(z0 + t) * rs + tid + 256 * r2 + SH * i] = acc[t][r2][u][i];
   }
 }
 
@@ -1239,21 +1245,29 @@ static bool launch_ksum_full(const Plan& P, const BatchArgs& A, int nb, cudaStre
   const int s0 = find_subband_host(P, A.u0), s1 = find_subband_host(P, A.u1 - 1);
   const SubBand& S = P.sb[s0];
   const int lev = S.level, nl = S.nl;
-  if (P.d != 2 || (1 << lev) > kB || (nl != 2 && nl != 4 && nl != 8) || (nl << lev) != P.n) return false;
-  if (sizeof(Real) == 8 && nl == 8) return false;   // static smem
+  if (P.d != 2 || (1 << lev) > 4 * kB || (nl != 2 && nl != 4 && nl != 8) || (nl << lev) != P.n) return false;
   for (int q = s0; q <= s1; ++q)
     if (P.sb[q].level != lev || P.sb[q].tW[0] < P.n || P.sb[q].tW[1] < P.n) return false;
   if (nb % nl || (A.u0 - S.offset) % nl) return false;
-  if (A.kf_rows == 2 && lev == 8 && (nl == 4 || nl == 2) && !getenv("PCWD_NO_TMA_KSUM")) {
-    auto launch = [&](auto kern, int NLV) {
-      const size_t smem = sizeof(Real) * 3 * size_t(2 * NLV - 1 + NLV) * 2 * 256 + 128;
+  if (A.kf_rows > 0 && lev >= 8 && lev <= 10 && (nl == 2 || nl == 4 || nl == 8) && !getenv("PCWD_NO_TMA_KSUM")) {
+    const int shm = (1 << lev) / 256;
+    auto launch = [&](auto kern, int NLV, int TRT, int SHMV) {
+      const size_t smem = sizeof(Real) * 3 * size_t(2 * NLV - 1 + NLV) * SHMV * TRT * 256 + 128;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      kern<<<dim3(P.n / 2, nb / NLV), kB, smem, st>>>(P, A);
+      kern<<<dim3(P.n / TRT, nb / NLV), kB, smem, st>>>(P, A);
     };
-    if (nl == 4) launch(bk_ksum_full_tma<Real, 4, 2>, 4);
-    else launch(bk_ksum_full_tma<Real, 2, 2>, 2);
-    return true;
+    if (shm == 1 && A.kf_rows == 2) {
+      if (nl == 4) { launch(bk_ksum_full_tma<Real, 4, 2, 1>, 4, 2, 1); return true; }
+      if (nl == 2) { launch(bk_ksum_full_tma<Real, 2, 2, 1>, 2, 2, 1); return true; }
+    } else if (shm == 2 && A.kf_rows == 1) {
+      if (nl == 4) { launch(bk_ksum_full_tma<Real, 4, 1, 2>, 4, 1, 2); return true; }
+      if (nl == 2) { launch(bk_ksum_full_tma<Real, 2, 1, 2>, 2, 1, 2); return true; }
+    } else if (shm == 4 && A.kf_rows == 1) {
+      if (nl == 2) { launch(bk_ksum_full_tma<Real, 2, 1, 4>, 2, 1, 4); return true; }
+    }
   }
+  // cp.async kernel: 2^ℓ ≤ 256 (one residue per thread), static shared memory
+  if ((1 << lev) > kB || (sizeof(Real) == 8 && nl == 8)) return false;
   const int TR = std::max(1, kB >> lev);
   const dim3 grid((P.n + TR - 1) / TR, nb / nl);
 #define PCWD_KF(L, NLV)                                                                      \
