@@ -199,6 +199,11 @@ __device__ __forceinline__ int block_reduce_sum(int x, int* red) {
   return red[0];
 }
 
+// a / b for a ≥ 0, b ≥ 1: through a float reciprocal below 2^20 (the +0.5 keeps the truncation exact), else integer
+__device__ __forceinline__ int qdiv(int a, int b, float inv_b) {
+  return a < (1 << 20) ? __float2int_rz((float(a) + 0.5f) * inv_b) : a / b;
+}
+
 template <typename Real, typename OutT, int D, int MODE>
 __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Plan P,
                                                       const __grid_constant__ UnitArgs A) {
@@ -279,9 +284,10 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
       if (D == 2) {
         const int ycols = a1.len + d1.len;
         const int totA = in0.len * ycols;
+        const float inv_y = 1.0f / float(ycols), inv_a1 = 1.0f / float(a1.len), inv_d1 = 1.0f / float(d1.len);
         const int k1 = kind(in1);
         for (int idx = tid; idx < totA; idx += kBlock) {       // pass A: axis 1
-          const int i0 = idx / ycols, j = idx - i0 * ycols;
+          const int i0 = qdiv(idx, ycols, inv_y), j = idx - i0 * ycols;
           const int e1 = j >= a1.len;
           const int jj = e1 ? j - a1.len : j;
           const Range& R = e1 ? d1 : a1;
@@ -316,10 +322,10 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
         for (int idx = tid; idx < totB; idx += kBlock) {       // pass B: axis 0
           int e0, e1, j0, j1, rem;
           Real* dst;
-          if (idx < s00) { e0 = 0; e1 = 0; rem = idx; j0 = rem / a1.len; j1 = rem - j0 * a1.len; dst = nxt + rem; }
-          else if (idx < s00 + s01) { e0 = 0; e1 = 1; rem = idx - s00; j0 = rem / d1.len; j1 = rem - j0 * d1.len; dst = Dd + rem; }
-          else if (idx < s00 + s01 + s10) { e0 = 1; e1 = 0; rem = idx - s00 - s01; j0 = rem / a1.len; j1 = rem - j0 * a1.len; dst = Dd + s01 + rem; }
-          else { e0 = 1; e1 = 1; rem = idx - s00 - s01 - s10; j0 = rem / d1.len; j1 = rem - j0 * d1.len; dst = Dd + s01 + s10 + rem; }
+          if (idx < s00) { e0 = 0; e1 = 0; rem = idx; j0 = qdiv(rem, a1.len, inv_a1); j1 = rem - j0 * a1.len; dst = nxt + rem; }
+          else if (idx < s00 + s01) { e0 = 0; e1 = 1; rem = idx - s00; j0 = qdiv(rem, d1.len, inv_d1); j1 = rem - j0 * d1.len; dst = Dd + rem; }
+          else if (idx < s00 + s01 + s10) { e0 = 1; e1 = 0; rem = idx - s00 - s01; j0 = qdiv(rem, a1.len, inv_a1); j1 = rem - j0 * a1.len; dst = Dd + s01 + rem; }
+          else { e0 = 1; e1 = 1; rem = idx - s00 - s01 - s10; j0 = qdiv(rem, d1.len, inv_d1); j1 = rem - j0 * d1.len; dst = Dd + s01 + s10 + rem; }
           const Range& R = e0 ? d0 : a0;
           const int q = 2 * (R.lo + j0) + P.to[e0];
           const int colY = (e1 ? a1.len : 0) + j1;
@@ -417,8 +423,9 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
         for (int wi = 0; wi < nw; ++wi) {
           const OutWin<Real>& W = w[wi];
           const int tot = W.r0.len * W.r1.len;
+          const float inv_w = 1.0f / float(W.r1.len);
           for (int k = tid; k < tot; k += kBlock) {
-            const int ks0 = k / W.r1.len, ks1 = k - ks0 * W.r1.len;
+            const int ks0 = qdiv(k, W.r1.len, inv_w), ks1 = k - ks0 * W.r1.len;
             const double x = double(W.buf[sorted_to_local(W.r0, ks0) * W.r1.len + sorted_to_local(W.r1, ks1)]);
             tmax = fmax(tmax, fabs(x));
             cbase[crun + k] = x;
