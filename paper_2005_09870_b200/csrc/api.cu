@@ -602,9 +602,11 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     if (u1 <= u0) return;
     size_t bytes = size_t(scr) * rb;
     Launch L{u0, u1, 0, 0};
-    // shared-memory scratch only while ≥ 3 units fit per SM; larger windows work in global (L2) scratch with
+    // shared-memory scratch only up to 48 KB per unit (c4 sweep 32-100 KB: 74 ms at 32-56, 78 at 72-100); larger
+    // windows work in global (L2) scratch with
     // 4 units per SM in flight
-    if (bytes <= std::min<size_t>(budget, 72 * 1024)) {
+    static const size_t smem_cap = size_t(getenv("PCWD_GENERIC_SMEM_KB") ? atoi(getenv("PCWD_GENERIC_SMEM_KB")) : 48) << 10;
+    if (bytes <= std::min<size_t>(budget, smem_cap)) {
       L.smem = std::max<size_t>(bytes, 16);
       int per_sm = int(std::min<size_t>(8, (228 * 1024) / (L.smem + 2048)));
       per_sm = std::max(per_sm, 1);
