@@ -603,8 +603,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     size_t bytes = size_t(scr) * rb;
     Launch L{u0, u1, 0, 0};
     // shared-memory scratch only up to 48 KB per unit (c4 sweep 32-100 KB: 74 ms at 32-56, 78 at 72-100); larger
-    // windows work in global (L2) scratch with
-    // 4 units per SM in flight
+    // windows work in global (L2) scratch with 4 units per SM in flight
     static const size_t smem_cap = size_t(getenv("PCWD_GENERIC_SMEM_KB") ? atoi(getenv("PCWD_GENERIC_SMEM_KB")) : 48) << 10;
     if (bytes <= std::min<size_t>(budget, smem_cap)) {
       L.smem = std::max<size_t>(bytes, 16);
