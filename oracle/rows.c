@@ -242,3 +242,89 @@ int oracle_rows(const oracle_problem* p, const int64_t* units, int64_t count, do
   free(unz);
   return err;
 }
+
+/* ---- per-unit statistics of the threshold-retained row (all-unit pattern sweeps) ----------------
+ * For each unit: cnt = #{λ : |Θ[μ][λ]| ≥ tau} (the closed inequality of reading R15), hash = FNV-1a
+ * (32 bit) over the little-endian bytes of the retained λ (int32, increasing), ssq = Σ retained θ²,
+ * sketch = Σ retained θ·s(λ) with s(λ) = ±1 from the top bit of splitmix64(λ), rmax = max|Θ[μ][·]|,
+ * near = #{λ : ||θ| − tau| ≤ 1e-12·tau} (decisions an fp64 rounding difference could flip).
+ * These are bookkeeping over the oracle's own fp64 row; nothing here is the method's arithmetic.
+ * A unit whose ‖H*ψ_μ‖₂ < tau retains nothing (Parseval, as in oracle_rows) and skips the cascade. */
+static uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+int oracle_row_stats(const oracle_problem* p, const int64_t* units, int64_t count, double tau,
+                     int64_t* cnt, uint32_t* hash, double* ssq, double* sketch, double* rmax,
+                     int64_t* near, int nthreads) {
+  long N = (p->d == 2) ? (long)p->n * p->n : p->n;
+  int err = 0;
+  nzlist* unz = (nzlist*)calloc(p->m, sizeof(nzlist));
+  if (!unz) return 1;
+  for (int k = 0; k < p->m; ++k) {
+    const double* uk = p->u + (long)k * N;
+    unz[k].zr = (int*)malloc(sizeof(int) * N);
+    unz[k].zc = (int*)malloc(sizeof(int) * N);
+    unz[k].val = (double*)malloc(sizeof(double) * N);
+    if (!unz[k].zr || !unz[k].zc || !unz[k].val) return 1;
+    for (long z = 0; z < N; ++z)
+      if (uk[z] != 0.0) {
+        long c = unz[k].cnt++;
+        unz[k].zr[c] = (p->d == 2) ? (int)(z / p->n) : 0;
+        unz[k].zc[c] = (p->d == 2) ? (int)(z % p->n) : (int)z;
+        unz[k].val[c] = uk[z];
+      }
+  }
+#pragma omp parallel num_threads(nthreads > 0 ? nthreads : 1)
+  {
+    double* buf = (double*)malloc(sizeof(double) * (N * 8 + 2 * (long)p->n + 4 * (long)p->L));
+    if (!buf) {
+#pragma omp atomic write
+      err = 1;
+    } else {
+      double* e = buf;
+      double* psi = buf + N;
+      double* g = buf + 2 * N;
+      double* c = buf + 3 * N;
+      double* work = buf + 4 * N;
+      double* ext = buf + 8 * N;
+#pragma omp for schedule(dynamic, 1)
+      for (int64_t i = 0; i < count; ++i) {
+        memset(e, 0, sizeof(double) * N);
+        e[units[i]] = 1.0;
+        inverse(p, e, psi, work);
+        adjoint_apply(p, unz, psi, g);
+        double s2 = 0.0;
+        for (long j = 0; j < N; ++j) s2 += g[j] * g[j];
+        int64_t nc = 0, nn = 0;
+        uint32_t hh = 2166136261u;
+        double sq = 0.0, sk = 0.0, mx = 0.0;
+        if (sqrt(s2) >= tau * (1.0 - 1e-9)) {
+          forward(p, g, c, work, ext);
+          for (long j = 0; j < N; ++j) {
+            double a = fabs(c[j]);
+            if (a > mx) mx = a;
+            if (fabs(a - tau) <= 1e-12 * tau) ++nn;
+            if (a >= tau) {
+              ++nc;
+              uint32_t col = (uint32_t)j;
+              for (int b = 0; b < 4; ++b) { hh ^= (col >> (8 * b)) & 0xffu; hh *= 16777619u; }
+              sq += c[j] * c[j];
+              sk += (splitmix64((uint64_t)j) >> 63) ? -c[j] : c[j];
+            }
+          }
+        } else {
+          mx = -sqrt(s2);
+        }
+        cnt[i] = nc; hash[i] = hh; ssq[i] = sq; sketch[i] = sk; rmax[i] = mx; near[i] = nn;
+      }
+      free(buf);
+    }
+  }
+  for (int k = 0; k < p->m; ++k) { free(unz[k].zr); free(unz[k].zc); free(unz[k].val); }
+  free(unz);
+  return err;
+}

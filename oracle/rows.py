@@ -69,3 +69,28 @@ def rowmax(p, units, nthreads: int | None = None, bound: float = 0.0) -> np.ndar
     """max_λ |Θ[μ][λ]| per unit; with bound > 0, units that provably hold no entry ≥ bound
     (Parseval) return -‖Θ[μ][·]‖₂ instead (see rows.c)."""
     return _run(p, units, False, nthreads, bound)[1]
+
+
+def row_stats(p, units, tau: float, nthreads: int | None = None) -> dict:
+    """Per-unit statistics of the row retained at the absolute threshold tau (|θ| ≥ tau, reading
+    R15), from the oracle's own fp64 rows (rows.c oracle_row_stats): cnt, hash (FNV-1a 32 over the
+    retained λ as int32 little-endian), ssq (Σ θ²), sketch (Σ θ·s(λ), s = ±1 from splitmix64),
+    rmax (max|Θ[μ][·]|, or −‖H*ψ_μ‖₂ for units skipped by the Parseval bound), near (entries within
+    1e-12·tau of tau)."""
+    lib = _load()
+    lib.oracle_row_stats.restype = ctypes.c_int
+    h = np.ascontiguousarray(p.h, dtype=np.float64)
+    u = np.ascontiguousarray(p.u, dtype=np.float64)
+    v = np.ascontiguousarray(p.v, dtype=np.float64)
+    units = np.ascontiguousarray(np.asarray(units, dtype=np.int64))
+    prob = _Problem(p.d, p.n, p.J, len(h), _ptr(h), p.m, _ptr(u), _ptr(v))
+    c = len(units)
+    out = dict(cnt=np.zeros(c, np.int64), hash=np.zeros(c, np.uint32), ssq=np.zeros(c), sketch=np.zeros(c),
+               rmax=np.zeros(c), near=np.zeros(c, np.int64))
+    P = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    rc = lib.oracle_row_stats(ctypes.byref(prob), P(units), ctypes.c_int64(c), ctypes.c_double(tau),
+                              P(out["cnt"]), P(out["hash"]), P(out["ssq"]), P(out["sketch"]), P(out["rmax"]),
+                              P(out["near"]), ctypes.c_int(nthreads or os.cpu_count() or 1))
+    if rc != 0:
+        raise MemoryError("oracle_row_stats failed")
+    return out
