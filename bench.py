@@ -7,7 +7,8 @@ band gather a2-a4) with u, v already resident in HBM.  L2 is flushed (256 MiB wr
 every timed step, outside the event pair.
 
   python bench.py [--gpus N --steps K --warmup W --config c5 --impl ours|reference]
-  (N > 1: launched by torchrun; units sharded by cost, no collective on the data path)
+  (N > 1: one rank per GPU — launched by torchrun, or re-launched under it by this script when WORLD_SIZE is
+  unset; units sharded by cost, no collective on the data path; per step a barrier, then the max over ranks)
 """
 from __future__ import annotations
 
@@ -106,6 +107,20 @@ def _ncu_traffic(kind: str, level: int):
         i = rows[0].index(name)
         tot += float(rows[2][i].replace(",", "")) * scale.get(rows[1][i], 1.0)
     return tot, os.path.relpath(files[-1], ROOT)
+
+
+def relaunch_under_torchrun(args) -> int | None:
+    """`--gpus N` (N > 1) outside torchrun: re-run this command as N ranks (one process per GPU) under
+    torch.distributed.run on 127.0.0.1 and return its exit code; None when already a rank (or N = 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -225,12 +240,16 @@ def run_ours(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     phase = np.zeros(3)
     lp_acc = []
+    from paper_2005_09870_b200 import pcwd as PW
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     with Clocks(dev) as clk:
         for i in range(args.steps):
             flush.fill_(float(i))                    # L2 flush, outside the timed pair
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()                       # every rank starts the step together
             ev[i][0].record(stream)
             dec.decompose(sp)
             ev[i][1].record(stream)
@@ -241,16 +260,18 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = np.array([a.elapsed_time(b) for a, b in ev])
     info = dec.info()
     nnz = info.nnz
     launches = info.kernel_launches
     if world > 1:
-        from paper_2005_09870_b200 import pcwd as PW
-        t_ms = PW.allreduce_max(t_ms, dev)          # max over ranks
-        nnz_all = int(PW.allreduce_sum(float(nnz), dev))
+        step_ms = PW.allreduce_max_vec(step_ms, dev)   # per step: the slowest rank (device time)
+        offsets = PW.global_row_offsets(nnz, dev)     # C-b: all-gather of the per-rank nnz
+        nnz_all = int(offsets[-1])
     else:
+        offsets = [0, nnz]
         nnz_all = nnz
+    t_ms = float(step_ms.sum())
     ms_per_step = t_ms / args.steps
     value = nnz_all / (ms_per_step * 1e-3)
 
@@ -295,7 +316,7 @@ def run_ours(args):
     # decomposing a sequence of operators of one geometry does.  `with_create_ms`: the same step with
     # pcwd_create (host planning + allocation) inside the timed region, and the unoverlapped copy.
     e2e = None
-    if rank == 0 and not args.no_e2e:
+    if not args.no_e2e:
         u_h = torch.from_numpy(p.u).pin_memory()
         v_h = torch.from_numpy(p.v).pin_memory()
         meta = dec.csr_meta()
@@ -312,16 +333,23 @@ def run_ours(args):
         times = []
         for i in range(max(3, min(args.steps, 10)) + 1):
             torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
             dplan.set_kernels(u_h, v_h, sp)
             dplan.decompose_to_host(rp_h, col_h, val_h, sp)
             torch.cuda.synchronize(dev)
             times.append(time.perf_counter() - t0)
         dplan.close()
-        t_e2e = statistics.median(times[1:])
+        times = np.array(times[1:])
+        if world > 1:
+            times = PW.allreduce_max_vec(times, dev)     # per step: the slowest rank's copy-in + decompose + copy-out
+        t_e2e = float(np.median(times))
         times_c = []
         for i in range(3):
             torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
             d2 = Decomposition(spec_h())
             d2.decompose(sp)
@@ -330,12 +358,18 @@ def run_ours(args):
             torch.cuda.synchronize(dev)
             times_c.append(time.perf_counter() - t0)
             d2.close()
-        e2e = {"value": meta.nnz / t_e2e * (nnz_all / max(nnz, 1)), "unit": "entries/s",
-               "h2d_bytes_per_step": int(p.u.nbytes + p.v.nbytes),
-               "d2h_bytes_per_step": int(rp_h.numel() * 8 + col_h.numel() * 4 + val_h.numel() * val_h.element_size()),
+        times_c = np.array(times_c[1:])
+        if world > 1:
+            times_c = PW.allreduce_max_vec(times_c, dev)
+        h2d = int(p.u.nbytes + p.v.nbytes) * world
+        d2h = int(rp_h.numel() * 8 + col_h.numel() * 4 + val_h.numel() * val_h.element_size())
+        if world > 1:
+            d2h = int(PW.allreduce_sum(float(d2h), dev))
+        e2e = {"value": nnz_all / t_e2e, "unit": "entries/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": t_e2e * 1e3, "calls": "pcwd_set_kernels + pcwd_decompose_to_host (plan built once)",
-               "with_create_ms": statistics.median(times_c[1:]) * 1e3,
-               "timing": "wall clock, synchronize on both sides, median"}
+               "with_create_ms": float(np.median(times_c)) * 1e3,
+               "timing": "wall clock per rank, synchronize on both sides, max over ranks per step, median"}
 
     if rank == 0:
         cb = None
@@ -348,7 +382,8 @@ def run_ours(args):
                 "config": {"workload": WORKLOAD.get(args.config, args.config), "config": args.config,
                            "units": p.N, "retained_per_unit": p.band_L, "nnz": nnz_all,
                            "l2": "flushed (256 MiB write) before every timed step",
-                           "sharding": f"{world} rank(s), cost-balanced contiguous unit ranges"},
+                           "sharding": f"{world} rank(s), cost-balanced contiguous unit ranges",
+                           "row_offsets": [int(x) for x in offsets]},
                 "roofline": roofline, "cpu_baseline": cb, "e2e": e2e,
                 "gpu_launches": launches * args.steps, "clocks": clk.summary(),
                 "decomposition_time_s": ms_per_step * 1e-3}
@@ -369,6 +404,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"], help="compute dtype (the headline is f32)")
     args = ap.parse_args()
+    rc = relaunch_under_torchrun(args)
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
         run_reference(args)
     else:

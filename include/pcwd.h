@@ -46,12 +46,18 @@ typedef enum { PCWD_F32 = 0, PCWD_F64 = 1 } pcwd_dtype;
 typedef enum {
   PCWD_RETAIN_FULL = 0,       /* every (μ, λ): dense rows of length N, exact zeros kept (R14) */
   PCWD_RETAIN_THRESHOLD = 1,  /* |Θ[μ][λ]| ≥ tau_rel · max|Θ|, decided in fp64 (R15)           */
-  PCWD_RETAIN_BAND = 2        /* exactly band_L partners per unit, scale/position key (R16)    */
+  PCWD_RETAIN_BAND = 2,       /* exactly band_L partners per unit, scale/position key (R16)    */
+  PCWD_RETAIN_PATTERN = 3     /* the caller's retained set: pat_rowptr / pat_col, a CSR over units (the
+                                 A_L pattern of Theorem 2's Remark, or any Θ_L of Eq. 7,
+                                 P:858-863); exact zeros kept (R14)                                   */
 } pcwd_retain;
 
 typedef struct {
   int32_t d;            /* dimension, 1 or 2  */
-  int32_t n;            /* side of the torus, power of two; N = n^d  */
+  int32_t n;            /* side of the torus, power of two; N = n^d.  The paper's grid is
+                           N_1 × … × N_d; the method is stated and analysed for
+                           N_1 = … = N_d = 2^J ("to simplify the discussion"), which is
+                           what this library implements: a single side n for every axis      */
   int32_t levels;       /* J = number of analysis steps, 1 ≤ J ≤ log2 n              (R3)    */
   int32_t filter_len;   /* 2δ, even, 2..20  */
   const double* h;      /* HOST, filter_len taps of the low-pass filter; g from P:100        */
@@ -65,6 +71,11 @@ typedef struct {
   int32_t band_L;       /* BAND: partners per unit, 1 ≤ L ≤ N                                 */
   int32_t rank, world;  /* shard of units owned by this handle; world ≥ 1                    */
   int32_t device;       /* CUDA device ordinal used by create                                */
+  const int64_t* pat_rowptr; /* PATTERN: host or device, N + 1 entries over ALL units (Λ order),
+                           pat_rowptr[0] = 0, non-decreasing; a sharded handle reads its rows   */
+  const int32_t* pat_col;    /* PATTERN: host or device, pat_rowptr[N] partner indices λ ∈ [0, N),
+                           strictly increasing within each row (the CSR column order).  Checked
+                           by pcwd_create (PCWD_E_PARAM); copied, the caller keeps ownership    */
 } pcwd_desc;
 
 typedef struct {
@@ -88,7 +99,12 @@ typedef struct {
 
 /* Validate desc and build the handle: plan (sub-band table, windows, band stencil, shard),
  * device buffers, copy of u and v cast to the compute precision.  Caller keeps ownership of
- * every pointer in desc and may free them when this returns.  Synchronous. */
+ * every pointer in desc and may free them when this returns.  Synchronous.
+ * The low-pass filter h must be an orthogonal wavelet filter: ‖h‖₂ = 1, Σ h = √2 and
+ * Σ_n h[n] h[n + 2k] = 0 for k ≠ 0, each to 1e-9; otherwise PCWD_E_CONFIG (Ψ would
+ * not be orthogonal and Θ = Ψ*HΨ would not be the operator's representation).
+ * PATTERN: pat_rowptr / pat_col are checked (monotone, in range, strictly increasing rows) and
+ * copied; a violation is PCWD_E_PARAM. */
 int pcwd_create(const pcwd_desc* desc, void** out_handle);
 
 /* Compute the retained rows of this shard into handle-owned CSR (templates, k-sum, cascade,

@@ -7,6 +7,7 @@ A").  Readings (R14-R16):
   full       every pair (μ, λ) ∈ Λ×Λ, exact zeros included.
   threshold  keep iff |Θ[μ][λ]| ≥ τ_rel · M, M = max over all entries of |Θ| (closed
              inequality), decided on fp64 values.
+  pattern    the caller's CSR over units (any Θ_L of Eq. 7; the A_L of the Remark).
   band (L)   for each unit μ keep exactly the L partners λ that come first in the total
              order of `band_key` (scale proximity Δ = |ℓ-ℓ'|, then position proximity ρ
              measured on the coarser of the two grids — the (i)/(ii) quantities of the
@@ -93,6 +94,8 @@ def retained_row(p, mu: int, row: np.ndarray, M: float | None = None):
     elif p.retain == "threshold":
         assert M is not None
         cols = threshold_keep(row, p.tau_rel * M)
+    elif p.retain == "pattern":     # the caller's retained set, taken as given (index-defined: zeros kept, R14)
+        cols = np.asarray(p.pat_col[p.pat_rowptr[mu]:p.pat_rowptr[mu + 1]], dtype=np.int64)
     else:
         raise ValueError(p.retain)
     return cols, row[cols]

@@ -537,6 +537,26 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     CK(cudaMemcpy(u_host.data(), desc->u, mN * sizeof(double), cudaMemcpyDeviceToHost));
     uh = u_host.data();
   }
+  // PATTERN: the caller's CSR over all units, checked on the host (monotone row pointers, columns in range and
+  // strictly increasing within each row); the handle keeps its shard's rows
+  std::vector<int64_t> pat_rp;
+  std::vector<int32_t> pat_col;
+  if (desc->retain == PCWD_RETAIN_PATTERN) {
+    pat_rp.resize(N + 1);
+    CK(cudaMemcpy(pat_rp.data(), desc->pat_rowptr, (N + 1) * sizeof(int64_t), cudaMemcpyDefault));
+    if (pat_rp[0] != 0) return fail(PCWD_E_PARAM, "pat_rowptr[0] must be 0");
+    for (int64_t i = 0; i < N; ++i)
+      if (pat_rp[i + 1] < pat_rp[i]) return fail(PCWD_E_PARAM, "pat_rowptr must be non-decreasing");
+    if (pat_rp[N] > (int64_t(1) << 40)) return fail(PCWD_E_PARAM, "pattern too large");
+    pat_col.resize(std::max<int64_t>(pat_rp[N], 1));
+    if (pat_rp[N] > 0) CK(cudaMemcpy(pat_col.data(), desc->pat_col, pat_rp[N] * sizeof(int32_t), cudaMemcpyDefault));
+    for (int64_t i = 0; i < N; ++i)
+      for (int64_t j = pat_rp[i]; j < pat_rp[i + 1]; ++j) {
+        if (pat_col[j] < 0 || pat_col[j] >= N) return fail(PCWD_E_PARAM, "pat_col out of range at row " + std::to_string(i));
+        if (j > pat_rp[i] && pat_col[j] <= pat_col[j - 1])
+          return fail(PCWD_E_PARAM, "pat_col not strictly increasing in row " + std::to_string(i));
+      }
+  }
   Handle* h = new Handle();
   h->desc = *desc;
   rc = build_plan(desc, uh, &h->hp, &msg);
@@ -870,7 +890,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       Launch B{u0, u1, 0, 0};
       B.batched = 1;
       int64_t stride = (scr + 31) & ~int64_t(31);
-      // batch so that the per-unit slots stay L2-resident next to v and the templates
+      // units per batch: up to 32 GiB of slots per level (one batch per level at c5 and 2048²); the sum over
+      // the levels is fitted to the free device memory after the plan (below)
       static const size_t cap = size_t(getenv("PCWD_BATCH_MB") ? atol(getenv("PCWD_BATCH_MB")) : 32768) << 20;
       int64_t batch = std::max<int64_t>(1, std::min<int64_t>(u1 - u0, int64_t(cap / (size_t(stride) * rb))));
       batch = std::min<int64_t>(batch, 65535);
@@ -979,7 +1000,29 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     add_generic(u0, u1, scr);
     s = e;
   }
-  if (h->bscratch_bytes) CKB(dalloc(&h->bscratch, h->bscratch_bytes + 1024));   // + vector over-read slack
+  if (h->bscratch_bytes) {
+    // fit the coarse scratch into half of the free device memory (the CSR, candidates and templates need the
+    // rest): concurrent levels share the budget equally, serial levels share one slice; batches shrink to fit
+    size_t freeb = 0, totb = 0;
+    CKB(cudaMemGetInfo(&freeb, &totb));
+    const size_t budget = freeb / 2;
+    if (h->bscratch_bytes > budget) {
+      int nb = 0;
+      for (const Launch& L : h->launches) nb += L.batched;
+      const size_t per = h->conc ? budget / size_t(std::max(nb, 1)) : budget;
+      size_t off = 0, mx = 0;
+      for (Launch& L : h->launches) {
+        if (!L.batched) continue;
+        const size_t ub = size_t(L.ba.stride) * rb;
+        L.ba.batch = std::max<int64_t>(1, std::min<int64_t>(L.ba.batch, int64_t(per / ub)));
+        const size_t bytes = size_t(L.ba.batch) * ub;
+        if (h->conc) { L.bs_off = off; off += (bytes + 1023) & ~size_t(1023); }
+        mx = std::max(mx, bytes);
+      }
+      h->bscratch_bytes = h->conc ? off : mx;
+    }
+    CKB(dalloc(&h->bscratch, h->bscratch_bytes + 1024));   // + vector over-read slack
+  }
   {
     int nb = 0;
     for (const Launch& L : h->launches) nb += L.batched;
@@ -1069,6 +1112,13 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     h->cap = h->nnz = rows * P.band_L;
   } else if (P.retain == PCWD_RETAIN_FULL) {
     h->cap = h->nnz = rows * P.N;
+  } else if (P.retain == PCWD_RETAIN_PATTERN) {
+    // the shard's rows of the caller's pattern: row pointers rebased to the shard, columns copied once
+    const int64_t base = pat_rp[h->hp.row0];
+    h->cap = h->nnz = pat_rp[h->hp.row1] - base;
+    std::vector<int64_t> rp(rows + 1);
+    for (int64_t i = 0; i <= rows; ++i) rp[i] = pat_rp[h->hp.row0 + i] - base;
+    CKB(cudaMemcpy(h->row_ptr, rp.data(), (rows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   } else {
     CKB(dalloc(&h->unitmax, std::max<int64_t>(rows, 1) * sizeof(double)));
     CKB(dalloc(&h->cnt, std::max<int64_t>(rows * P.nsb, 1) * sizeof(int32_t)));
@@ -1091,6 +1141,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     CKB(dalloc(&h->col, h->cap * sizeof(int32_t)));
     CKB(dalloc(&h->val, h->cap * ob));
   }
+  if (P.retain == PCWD_RETAIN_PATTERN && h->nnz > 0)
+    CKB(cudaMemcpy(h->col, pat_col.data() + pat_rp[h->hp.row0], h->nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
   CKB(cudaDeviceSynchronize());
 #undef CKB
   *out_handle = h;
@@ -1143,6 +1195,13 @@ int pcwd_decompose(void* handle, void* stream) {
     CK(launch_fill_band_rowptr(h->row_ptr, rows, P.band_L, st));
     h->nlaunch++;
     rec(3);
+  } else if (P.retain == PCWD_RETAIN_PATTERN) {
+    rec(0);
+    if ((rc = build_templates(h, st))) return rc;
+    rec(1);
+    rec(2);
+    if ((rc = run_units(h, MODE_PATTERN, st, 0.0))) return rc;
+    rec(3);
   } else if (P.retain == PCWD_RETAIN_FULL) {
     rec(0);
     if ((rc = build_templates(h, st))) return rc;
@@ -1178,14 +1237,35 @@ int pcwd_decompose(void* handle, void* stream) {
     CK(cudaMemcpyAsync(&nnz, h->row_ptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (nnz > h->cap) {
-      if (h->col) cudaFree(h->col);
-      if (h->val) cudaFree(h->val);
-      h->col = nullptr;
-      h->val = nullptr;
-      int64_t cap = nnz + nnz / 8 + 1024;
-      CK(dalloc(&h->col, cap * sizeof(int32_t)));
-      CK(dalloc(&h->val, cap * h->hp.out_bytes));
-      h->cap = cap;
+      // free first (room for the larger CSR), with the handle left consistent (no CSR) if the allocation fails
+      if (h->col) { cudaFree(h->col); h->col = nullptr; }
+      if (h->val) { cudaFree(h->val); h->val = nullptr; }
+      h->cap = 0;
+      h->nnz = 0;
+      h->decomposed = false;
+      int32_t* ncol = nullptr;
+      void* nval = nullptr;
+      int64_t got = 0;
+      auto grow = [&](int64_t c) {
+        if (dalloc(&ncol, c * sizeof(int32_t)) != cudaSuccess) { cudaGetLastError(); ncol = nullptr; return false; }
+        if (dalloc(&nval, c * h->hp.out_bytes) != cudaSuccess) {
+          cudaGetLastError(); cudaFree(ncol); ncol = nullptr; nval = nullptr; return false;
+        }
+        got = c;
+        return true;
+      };
+      bool ok = grow(nnz + nnz / 8 + 1024) || grow(nnz);
+      if (!ok && h->cand) {
+        // the store-then-filter buffer starves the CSR: drop it and write the rows by the recompute pass
+        cudaFree(h->cand);
+        h->cand = nullptr;
+        h->cand_valid = false;
+        ok = grow(nnz + nnz / 8 + 1024) || grow(nnz);
+      }
+      if (!ok) return fail(PCWD_E_OOM, "CSR of " + std::to_string(nnz) + " entries does not fit in device memory");
+      h->col = ncol;
+      h->val = nval;
+      h->cap = got;
     }
     h->nnz = nnz;
     if (h->cand_valid) {
@@ -1265,7 +1345,7 @@ int pcwd_decompose_to_host(void* handle, int64_t* row_ptr, int32_t* col, void* v
   if (!h) return fail(PCWD_E_PARAM, "NULL handle");
   CK(cudaSetDevice(h->desc.device));
   const Plan& P = h->hp.P;
-  if (P.retain == PCWD_RETAIN_THRESHOLD) {
+  if (P.retain == PCWD_RETAIN_THRESHOLD || P.retain == PCWD_RETAIN_PATTERN) {   // rows of varying width
     int rc = pcwd_decompose(handle, stream);
     return rc ? rc : pcwd_copy_csr(handle, row_ptr, col, val, stream);
   }
@@ -1428,7 +1508,7 @@ int pcwd_phase_times(void* handle, double* out_ms, double* out_fma) {
     return fail(PCWD_E_STATE, "profiling not enabled (or THRESHOLD: not instrumented)");
   float t[3] = {0, 0, 0};
   CK(cudaEventElapsedTime(&t[0], h->ev[0], h->ev[1]));
-  if (h->hp.P.retain == PCWD_RETAIN_BAND) {
+  if (h->hp.P.retain == PCWD_RETAIN_BAND || h->hp.P.retain == PCWD_RETAIN_PATTERN) {
     CK(cudaEventElapsedTime(&t[1], h->ev[1], h->ev[2]));
     CK(cudaEventElapsedTime(&t[2], h->ev[2], h->ev[3]));
   } else {

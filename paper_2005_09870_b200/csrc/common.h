@@ -25,7 +25,8 @@ constexpr int kMaxJ = 16;
 constexpr int kMaxSB = 1 + 3 * kMaxJ;
 constexpr int kMaxTaps = 20;
 
-enum Mode : int { MODE_FULL = 0, MODE_BAND = 1, MODE_TMAX = 2, MODE_TCOUNT = 3, MODE_TWRITE = 4, MODE_TSTORE = 5 };
+enum Mode : int { MODE_FULL = 0, MODE_BAND = 1, MODE_TMAX = 2, MODE_TCOUNT = 3, MODE_TWRITE = 4, MODE_TSTORE = 5,
+                  MODE_PATTERN = 6 };
 
 struct Range {
   int lo, len, nl;

@@ -12,6 +12,7 @@
 //
 // One CTA processes one unit at a time (grid-stride over units in Λ order, coarse and costly
 // first); its windows live in shared memory when they fit, else in a per-CTA global slice.
+#include <mutex>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -199,6 +200,21 @@ __device__ __forceinline__ int block_reduce_sum(int x, int* red) {
   return red[0];
 }
 
+__device__ __forceinline__ int block_reduce_maxi(int x, int* red) {
+  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int y = threadIdx.x < kBlock / 32 ? red[threadIdx.x] : 0;
+    for (int o = 16; o > 0; o >>= 1) y = max(y, __shfl_xor_sync(0xffffffffu, y, o));
+    if (threadIdx.x == 0) red[0] = y;
+  }
+  __syncthreads();
+  return red[0];
+}
+
 // a / b for a ≥ 0, b ≥ 1: through a float reciprocal below 2^20 (the +0.5 keeps the truncation exact), else integer
 __device__ __forceinline__ int qdiv(int a, int b, float inv_b) {
   return a < (1 << 20) ? __float2int_rz((float(a) + 0.5f) * inv_b) : a / b;
@@ -258,6 +274,13 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
     if (MODE == MODE_BAND) {
       for (int j = tid; j < P.band_Lpad; j += kBlock) { stage_col[j] = INT_MAX; stage_val[j] = Real(0); }
     }
+    // PATTERN: the cascade runs up to the coarsest level among the unit's listed partners
+    int nsteps = S.steps;
+    if (MODE == MODE_PATTERN) {
+      int mx = 0;
+      for (int64_t j = A.row_ptr[row] + tid; j < A.row_ptr[row + 1]; j += kBlock) mx = max(mx, P.sb[find_subband(P, A.col[j])].level);
+      nsteps = block_reduce_maxi(mx, red_i);
+    }
     __syncthreads();
 
     // ---- a3: windowed periodic cascade, steps 1..S.steps, emitting after each step
@@ -268,7 +291,7 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
     int64_t crun = 0;   // TSTORE: candidates of this unit stored so far
     double* cbase = nullptr;
     if (MODE == MODE_TSTORE) cbase = A.cand + S.cand_off + (unit - (S.offset > A.row0 ? S.offset : A.row0)) * S.cand_slot;
-    for (int s = 1; s <= S.steps; ++s) {
+    for (int s = 1; s <= nsteps; ++s) {
       const Range a0 = D == 2 ? step_out(in0, L2, 0) : Range{0, 1, 1};
       const Range d0 = D == 2 ? step_out(in0, L2, 1) : Range{0, 1, 1};
       const Range a1 = step_out(in1, L2, 0);
@@ -413,6 +436,25 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
           }
           stage_val[j] = x;
           stage_col[j] = int(L.offset + int64_t(l0) * L.nl + l1);
+        }
+      } else if (MODE == MODE_PATTERN) {   // the caller's partners of this step's sub-bands (columns given)
+        OutT* outv = reinterpret_cast<OutT*>(A.val);
+        for (int64_t j = A.row_ptr[row] + tid; j < A.row_ptr[row + 1]; j += kBlock) {
+          const int c = A.col[j];
+          const int sb = find_subband(P, c);
+          const SubBand& L = P.sb[sb];
+          if (L.level != s || (sb == 0 && s != P.J)) continue;
+          const OutWin<Real>* W = nullptr;
+          for (int wi = 0; wi < nw; ++wi) if (w[wi].sbi == sb) W = &w[wi];
+          const int64_t lp = c - L.offset;
+          const int l0 = D == 2 ? int(lp / L.nl) : 0;
+          const int l1 = D == 2 ? int(lp - int64_t(l0) * L.nl) : int(lp);
+          Real x = Real(0);
+          if (W) {
+            const int li0 = local_index(W->r0, l0), li1 = local_index(W->r1, l1);
+            if (li0 >= 0 && li1 >= 0) x = W->buf[li0 * W->r1.len + li1];
+          }
+          outv[j] = OutT(x);
         }
       } else if (MODE == MODE_TMAX) {
         for (int wi = 0; wi < nw; ++wi) {
@@ -740,9 +782,25 @@ cudaError_t launch_cast(const double* src, void* dst, int64_t count, int real_by
 template <typename Real, typename OutT, int D, int MODE>
 static cudaError_t launch_one(const Plan& P, const UnitArgs& A, int grid, size_t smem, cudaStream_t st) {
   auto kern = unit_kernel<Real, OutT, D, MODE>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
+  // the kernel has static shared memory too (reductions, scan storage): opt in whenever static + dynamic
+  // exceeds 48 KB; the attribute only ever grows (per instantiation, process-wide), under a lock so that
+  // handles used from several threads never launch between another thread's check and its set
+  static std::mutex mu;
+  static int opted = -1, static_bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (opted < 0) {
+      cudaFuncAttributes fa;
+      cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+      if (e != cudaSuccess) return e;
+      static_bytes = int(fa.sharedSizeBytes);
+      opted = 48 * 1024 - static_bytes;
+    }
+    if (int(smem) > opted) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      opted = int(smem);
+    }
   }
   kern<<<grid, kBlock, smem, st>>>(P, A);
   return cudaGetLastError();
@@ -763,6 +821,9 @@ cudaError_t launch_units(const Plan& P, const UnitArgs& A, int mode, int real_by
     case MODE_BAND:
       return real_bytes == 4 ? launch_d<float, float, MODE_BAND>(P, A, grid, smem, st)
                              : launch_d<double, double, MODE_BAND>(P, A, grid, smem, st);
+    case MODE_PATTERN:
+      return real_bytes == 4 ? launch_d<float, float, MODE_PATTERN>(P, A, grid, smem, st)
+                             : launch_d<double, double, MODE_PATTERN>(P, A, grid, smem, st);
     case MODE_TMAX:
       return launch_d<double, double, MODE_TMAX>(P, A, grid, smem, st);
     case MODE_TSTORE:

@@ -33,6 +33,20 @@ int validate_desc(const pcwd_desc* d, std::string* msg) {
     *msg = "filter_len must be even, 2..20"; return PCWD_E_CONFIG;
   }
   if (!d->h) { *msg = "h is NULL"; return PCWD_E_PARAM; }
+  {  // an orthogonal wavelet filter: ‖h‖₂ = 1, Σ h = √2, Σ_n h[n] h[n+2k] = 0 (k ≠ 0)
+    const int L = d->filter_len;
+    double s1 = 0.0;
+    for (int i = 0; i < L; ++i) s1 += d->h[i];
+    if (std::fabs(s1 - std::sqrt(2.0)) > 1e-9) { *msg = "h: sum must be sqrt(2) (low-pass filter of an orthogonal wavelet)"; return PCWD_E_CONFIG; }
+    for (int k = 0; 2 * k < L; ++k) {
+      double a = 0.0;
+      for (int i = 0; i + 2 * k < L; ++i) a += d->h[i] * d->h[i + 2 * k];
+      if (std::fabs(a - (k == 0 ? 1.0 : 0.0)) > 1e-9) {
+        *msg = k == 0 ? "h: norm must be 1" : "h: not orthogonal to its even shifts (sum h[n]h[n+2k] != 0)";
+        return PCWD_E_CONFIG;
+      }
+    }
+  }
   if (d->m < 1) { *msg = "m must be >= 1"; return PCWD_E_PARAM; }
   if (d->dtype != PCWD_F32 && d->dtype != PCWD_F64) { *msg = "dtype"; return PCWD_E_PARAM; }
   int64_t N = d->d == 2 ? int64_t(d->n) * d->n : d->n;
@@ -41,6 +55,8 @@ int validate_desc(const pcwd_desc* d, std::string* msg) {
   } else if (d->retain == PCWD_RETAIN_BAND) {
     if (d->band_L < 1 || d->band_L > N) { *msg = "band_L must be in [1, N]"; return PCWD_E_PARAM; }
     if (d->band_L > 4096) { *msg = "band_L > 4096 not supported"; return PCWD_E_UNSUPPORTED; }
+  } else if (d->retain == PCWD_RETAIN_PATTERN) {
+    if (!d->pat_rowptr || !d->pat_col) { *msg = "PATTERN needs pat_rowptr and pat_col"; return PCWD_E_PARAM; }
   } else if (d->retain != PCWD_RETAIN_FULL) {
     *msg = "retain"; return PCWD_E_PARAM;
   }

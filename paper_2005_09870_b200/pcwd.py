@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpcwd.so")
 
 PCWD_F32, PCWD_F64 = 0, 1
-RETAIN = {"full": 0, "threshold": 1, "band": 2}
+RETAIN = {"full": 0, "threshold": 1, "band": 2, "pattern": 3}
 STATUS = {0: "OK", 1: "E_SHAPE", 2: "E_CONFIG", 3: "E_PARAM", 4: "E_CUDA", 5: "E_OOM", 6: "E_STATE",
           7: "E_UNSUPPORTED"}
 
@@ -33,7 +33,8 @@ class Desc(ctypes.Structure):
                 ("filter_len", ctypes.c_int32), ("h", ctypes.c_void_p), ("m", ctypes.c_int32),
                 ("u", ctypes.c_void_p), ("v", ctypes.c_void_p), ("dtype", ctypes.c_int32),
                 ("retain", ctypes.c_int32), ("tau_rel", ctypes.c_double), ("band_L", ctypes.c_int32),
-                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("pat_rowptr", ctypes.c_void_p), ("pat_col", ctypes.c_void_p)]
 
 
 class Csr(ctypes.Structure):
@@ -128,17 +129,24 @@ class Spec:
     rank: int = 0
     world: int = 1
     device: int = 0
+    pat_rowptr: object = None   # PATTERN: int64 (N+1) and int32 (nnz) CSR over all units (numpy or CUDA tensor)
+    pat_col: object = None
 
 
 def make_desc(s: Spec, keep: list) -> Desc:
     h = np.ascontiguousarray(np.asarray(s.h, dtype=np.float64))
     keep.append(h)
-    for a in (s.u, s.v):
+    rp, pc = s.pat_rowptr, s.pat_col
+    if isinstance(rp, np.ndarray):
+        rp = np.ascontiguousarray(rp, dtype=np.int64)
+    if isinstance(pc, np.ndarray):
+        pc = np.ascontiguousarray(pc, dtype=np.int32)
+    for a in (s.u, s.v, rp, pc):
         keep.append(a)
     m = int(s.u.shape[0])
     return Desc(s.d, s.n, s.levels, len(h), _ptr(h), m, _ptr(s.u), _ptr(s.v),
                 PCWD_F64 if s.dtype == "f64" else PCWD_F32, RETAIN[s.retain], float(s.tau_rel),
-                int(s.band_L), s.rank, s.world, s.device)
+                int(s.band_L), s.rank, s.world, s.device, _ptr(rp), _ptr(pc))
 
 
 class Decomposition:
@@ -146,8 +154,8 @@ class Decomposition:
 
     def __init__(self, spec: Spec):
         self.spec = spec
-        keep = []
-        self._desc = make_desc(spec, keep)
+        self._keep = []
+        self._desc = make_desc(spec, self._keep)
         h = ctypes.c_void_p()
         _check(lib().pcwd_create(ctypes.byref(self._desc), ctypes.byref(h)), "pcwd_create")
         self._h = h
@@ -294,6 +302,97 @@ def allreduce_sum(x: float, device: int = 0) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def _coll_device(device: int = 0):
+    import torch
+    import torch.distributed as dist
+    return torch.device("cuda", device) if dist.get_backend() == "nccl" else torch.device("cpu")
+
+
+def allreduce_max_vec(x, device: int = 0) -> np.ndarray:
+    """Element-wise MAX over ranks of a small fp64 vector (per-step times: the slowest rank of every step)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(np.asarray(x, dtype=np.float64), device=_coll_device(device))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.cpu().numpy()
+
+
+def global_row_offsets(nnz: int, device: int = 0) -> list:
+    """C-b: all-gather of the per-rank nnz; returns the exclusive prefix [0, nnz_0, nnz_0+nnz_1, …,
+    total] — rank r's entries start at offsets[r] of the global CSR (its rows at the handle's row0)."""
+    import torch
+    import torch.distributed as dist
+    dev = _coll_device(device)
+    w = dist.get_world_size()
+    t = torch.tensor([int(nnz)], dtype=torch.int64, device=dev)
+    out = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(w)]
+    dist.all_gather(out, t)
+    counts = [int(o.item()) for o in out]
+    return [0] + list(np.cumsum(counts).tolist())
+
+
+def gather_csr(row_ptr, col, val, row0: int, n_rows_all: int, dst: int = 0):
+    """C-c: assemble the ranks' CSR shards (contiguous unit ranges, Λ order) into one CSR on rank
+    `dst` — per-rank sizes by all-gather, then point-to-point transfers (NCCL over NVLink on GPUs, gloo on CPU).
+    row_ptr (int64, shard-local, starting at 0), col (int32), val: this rank's shard as torch tensors on the
+    collective's device.  Returns (row_ptr, col, val) of the whole Θ on `dst`, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    r, w = dist.get_rank(), dist.get_world_size()
+    dev = row_ptr.device
+    meta = torch.tensor([int(row0), int(row_ptr.numel() - 1), int(col.numel())], dtype=torch.int64, device=dev)
+    metas = [torch.zeros(3, dtype=torch.int64, device=dev) for _ in range(w)]
+    dist.all_gather(metas, meta)
+    metas = [[int(x) for x in m.tolist()] for m in metas]
+    if r != dst:
+        for t in (row_ptr, col, val):
+            if t.numel():
+                dist.send(t.contiguous(), dst)
+        return None
+    nnz_all = sum(m[2] for m in metas)
+    rp_all = torch.zeros(n_rows_all + 1, dtype=torch.int64, device=dev)
+    col_all = torch.empty(nnz_all, dtype=col.dtype, device=dev)
+    val_all = torch.empty(nnz_all, dtype=val.dtype, device=dev)
+    off = 0
+    for q, (q_row0, q_rows, q_nnz) in enumerate(metas):
+        if q == dst:
+            parts = (row_ptr, col, val)
+        else:
+            parts = (torch.empty(q_rows + 1, dtype=torch.int64, device=dev), torch.empty(q_nnz, dtype=col.dtype, device=dev),
+                     torch.empty(q_nnz, dtype=val.dtype, device=dev))
+            for t in parts:
+                if t.numel():
+                    dist.recv(t, q)
+        rp_all[q_row0 + 1:q_row0 + q_rows + 1] = parts[0][1:] + off
+        col_all[off:off + q_nnz] = parts[1]
+        val_all[off:off + q_nnz] = parts[2]
+        off += q_nnz
+    return rp_all, col_all, val_all
+
+
+def apply_distributed(dec: "Decomposition", x, transpose: bool = False):
+    """C-d: Θ_ret x over a sharded Θ.  transpose = 0: x is the full Λ-vector (replicated), each rank
+    multiplies its rows (pcwd_apply) and the row blocks are all-gathered into the full y.  transpose = 1: x is the
+    full vector too; each rank applies its rows' transpose to its slice x[row0:row1] (a full-length partial) and
+    the partials are summed by an all-reduce — Θᵀx = Σ_r Θ_rᵀ x_r (the FISTA gradient Θ_L*(…))."""
+    import torch
+    import torch.distributed as dist
+    info = dec.info()
+    if not transpose:
+        y_loc = dec.apply(x)
+        sizes = [torch.zeros(1, dtype=torch.int64, device=x.device) for _ in range(dist.get_world_size())]
+        dist.all_gather(sizes, torch.tensor([y_loc.numel()], dtype=torch.int64, device=x.device))
+        mx = max(int(t.item()) for t in sizes)
+        buf = torch.zeros(mx, dtype=x.dtype, device=x.device)
+        buf[:y_loc.numel()] = y_loc
+        outs = [torch.empty(mx, dtype=x.dtype, device=x.device) for _ in sizes]
+        dist.all_gather(outs, buf)
+        return torch.cat([o[:int(n.item())] for o, n in zip(outs, sizes)])
+    y = dec.apply(x[info.row0:info.row1].contiguous(), transpose=True)
+    dist.all_reduce(y, op=dist.ReduceOp.SUM)
+    return y
 
 
 # ---- host-only plan queries (no GPU) ---------------------------------------------------------

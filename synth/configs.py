@@ -43,6 +43,8 @@ class Problem:
     band_L: int = 0
     dtypes: tuple = ("f64",)
     meta: dict = field(default_factory=dict)
+    pat_rowptr: np.ndarray | None = None   # retain == "pattern": CSR over units (int64 N+1, int32 columns)
+    pat_col: np.ndarray | None = None
 
     def __post_init__(self):
         self.u = np.ascontiguousarray(self.u, dtype=np.float64)
@@ -62,6 +64,9 @@ class Problem:
         for a in (self.h, self.u, self.v):
             s.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
         s.update(repr((self.d, self.n, self.J, self.retain, self.tau_rel, self.band_L)).encode())
+        if self.pat_rowptr is not None:
+            s.update(np.ascontiguousarray(self.pat_rowptr, dtype=np.int64).tobytes())
+            s.update(np.ascontiguousarray(self.pat_col, dtype=np.int32).tobytes())
         return s.hexdigest()
 
 
@@ -288,3 +293,22 @@ def micro(n: int, d: int, M: int, J: int, m: int, R: int, seed: int, retain: str
     return Problem(f"micro_n{n}_d{d}_M{M}_J{J}_m{m}_R{R}_s{seed}_{retain}", d, n, J,
                    daubechies(M), u, v, retain, tau_rel=tau_rel, band_L=band_L,
                    dtypes=("f64", "f32"))
+
+
+def random_pattern(N: int, max_per_row: int, seed: int, empty_every: int = 7):
+    """A seeded retained pattern for PATTERN tests: row μ keeps μ itself plus k − 1 other random units
+    (k uniform in 1..max_per_row), except every `empty_every`-th row, which is empty.  Returns the CSR
+    (rowptr int64 N+1, col int32, columns increasing within a row)."""
+    rng = np.random.default_rng(seed)
+    rp, cols = [0], []
+    for mu in range(N):
+        if empty_every and mu % empty_every == 3:
+            c = np.zeros(0, np.int64)
+        else:
+            k = int(rng.integers(1, min(max_per_row, N) + 1))
+            others = rng.choice(N - 1, size=k - 1, replace=False)
+            others = others + (others >= mu)            # skip μ itself
+            c = np.sort(np.concatenate([[mu], others]))
+        cols.append(c.astype(np.int32))
+        rp.append(rp[-1] + len(c))
+    return np.array(rp, dtype=np.int64), np.concatenate(cols).astype(np.int32)

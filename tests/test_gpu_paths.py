@@ -71,6 +71,17 @@ def test_threshold_recompute_matches_store_then_filter(tmp_path):
             assert np.array_equal(got[k], ref[k])
 
 
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_threshold_generic_smem_cap(tmp_path, dtype):
+    """The threshold rule runs the generic unit kernel on every level: a 200 KB shared-memory cap moves the
+    coarser levels of c2 from the global (L2) scratch into shared memory — the same fp64 arithmetic, so the
+    same CSR bit for bit."""
+    ref = _run(tmp_path, "c2", dtype, {})
+    got = _run(tmp_path, "c2", dtype, {"PCWD_GENERIC_SMEM_KB": "200"})
+    for k in ("rp", "col", "val"):
+        assert np.array_equal(got[k], ref[k])
+
+
 @pytest.mark.parametrize("case", [("c3", "f32"), ("micro128", "f64")], ids=["c3-f32", "128-f64"])
 @pytest.mark.parametrize("env", SWITCHES, ids=["+".join(f"{k}={v}" for k, v in s.items()) for s in SWITCHES])
 def test_switch_matches_default_path(tmp_path, case, env):

@@ -43,6 +43,10 @@ def _spec(**kw):
     ({"levels": 0}, 2), ({"levels": 5}, 2), ({"h": np.ones(3)}, 2),
     ({"retain": "threshold", "tau_rel": 0.0}, 3), ({"band_L": 0}, 3), ({"band_L": 257}, 3),
     ({"rank": 2, "world": 2}, 3), ({"world": 0}, 3),
+    # not an orthogonal wavelet filter: wrong sum, wrong norm, not orthogonal to even shifts
+    ({"h": np.array([1.0, 1.0]) / np.sqrt(2) * 1.001}, 2), ({"h": np.array([0.5, 0.5, 0.5, 0.5]) * np.sqrt(2) / 2}, 2),
+    ({"h": np.array([0.6, 0.2, 0.3, 0.5]) * np.sqrt(2) / 1.6}, 2),
+    ({"retain": "pattern"}, 3),
 ])
 def test_validation_codes(kw, code):
     assert P.validate(_spec(**kw)) == code
@@ -138,3 +142,13 @@ def test_c5_shard_plan_aligned_and_time_balanced(world):
         assert a[1] == b[0] and b[0] % 16 == 0
     sizes = [b - a for a, b in rs]
     assert sizes[0] < sizes[-1]          # rank 0 holds the coarse (expensive) units
+
+
+def test_corrupted_filter_rejected():
+    """SPEC's fault-injection example (S:540): one tap of a valid DB4 filter perturbed by 1e-6 → E_CONFIG;
+    the valid filter passes."""
+    h = C.daubechies(4).copy()
+    assert P.validate(_spec(h=h)) == 0
+    h[3] += 1e-6
+    assert P.validate(_spec(h=h)) == 2
+    assert "h:" in P.lib().pcwd_last_error().decode()

@@ -65,3 +65,69 @@ def test_gloo_world2_shards_and_threshold_exchange(world):
         assert r[2] == r[5]               # all-reduced max = global max of Θ
         assert r[3] == r[6]               # summed shard counts = global retained count
         assert r[4] == float(world)       # max over ranks
+
+
+def _worker_shards(rank, world, port, out):
+    """C-b offsets, C-c shard gather and C-d transposed-apply reduction over the shards of an oracle Θ (the GPU
+    computes the shards in the real run; here the exchanges are what is tested)."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        from oracle import operator as op
+        from paper_2005_09870_b200 import pcwd as P
+        from synth import configs as C
+        p = C.micro(16, 2, 4, 3, 2, 2, 32, retain="threshold", tau_rel=1e-3)
+        T = op.theta_dense(p)
+        M = float(np.abs(T).max())
+        spec = P.Spec(p.d, p.n, p.J, p.h, p.u, p.v, dtype="f64", retain="threshold", tau_rel=1e-3,
+                      rank=rank, world=world)
+        r0, r1 = P.plan_shard(spec)
+        keep = np.abs(T[r0:r1]) >= 1e-3 * M
+        rp = np.concatenate([[0], np.cumsum(keep.sum(axis=1))]).astype(np.int64)
+        col = np.nonzero(keep)[1].astype(np.int32)
+        val = T[r0:r1][keep]
+        offs = P.global_row_offsets(len(col))
+        g = P.gather_csr(torch.from_numpy(rp), torch.from_numpy(col), torch.from_numpy(val), r0, p.N)
+        # Θᵀ x as the sum of the shards' partials Θ_rᵀ x[r0:r1]
+        x = np.random.default_rng(0).standard_normal(p.N)
+        part = np.zeros(p.N)
+        dense = np.zeros((r1 - r0, p.N))
+        dense[keep] = val
+        part += dense.T @ x[r0:r1]
+        y = torch.from_numpy(part)
+        dist.all_reduce(y, op=dist.ReduceOp.SUM)
+        steps = P.allreduce_max_vec(np.array([rank + 1.0, 5.0 - rank]))
+        out[rank] = (offs, None if g is None else tuple(t.numpy() for t in g), y.numpy(), steps, len(col), r0)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_offsets_gather_apply():
+    from oracle import operator as op
+    from synth import configs as C
+    from paper_2005_09870_b200 import _build
+    _build.build()
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_shards, args=(world, port, out), nprocs=world, join=True)
+    res = [out[r] for r in range(world)]
+    p = C.micro(16, 2, 4, 3, 2, 2, 32, retain="threshold", tau_rel=1e-3)
+    T = op.theta_dense(p)
+    keep = np.abs(T) >= 1e-3 * np.abs(T).max()
+    nnz = [r[4] for r in res]
+    assert res[0][0] == res[1][0] == [0, nnz[0], nnz[0] + nnz[1]]          # C-b: identical on every rank
+    rp, col, val = res[0][1]                                                # C-c: the whole Θ on rank 0
+    assert res[1][1] is None
+    assert np.array_equal(rp, np.concatenate([[0], np.cumsum(keep.sum(axis=1))]))
+    assert np.array_equal(col, np.nonzero(keep)[1]) and np.array_equal(val, T[keep])
+    x = np.random.default_rng(0).standard_normal(p.N)
+    dense = np.where(keep, T, 0.0)
+    for r in res:                                                           # C-d: Σ_r Θ_rᵀ x_r = Θᵀ x
+        assert np.allclose(r[2], dense.T @ x, rtol=1e-13, atol=1e-13)
+        assert list(r[3]) == [2.0, 5.0]                                     # per-step max over ranks
