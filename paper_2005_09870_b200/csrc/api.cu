@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -1470,6 +1471,136 @@ int pcwd_apply(void* handle, const void* x, void* y, int transpose, void* stream
     CK(launch_spmv(h->row_ptr, h->col, h->val, x, y, h->rows(), h->hp.P.N, 0, h->hp.out_bytes,
                    static_cast<cudaStream_t>(stream)));
   }
+  return PCWD_OK;
+}
+
+int pcwd_operator_apply(void* handle, const void* x, void* y, int adjoint, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !x || !y) return fail(PCWD_E_PARAM, "NULL argument");
+  if (x == y) return fail(PCWD_E_PARAM, "x and y must not alias");
+  CK(cudaSetDevice(h->desc.device));
+  CK(launch_operator(h->hp.P, h->u_d, h->v_d, x, y, adjoint, h->hp.real_bytes, static_cast<cudaStream_t>(stream)));
+  return PCWD_OK;
+}
+
+int pcwd_approx(void* handle, double eta, void* stream, pcwd_approx_info* out) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h) return fail(PCWD_E_PARAM, "NULL handle");
+  if (!(eta > 0.0)) return fail(PCWD_E_PARAM, "eta must be > 0");
+  const Plan& P = h->hp.P;
+  if (h->hp.real_bytes != 8) return fail(PCWD_E_UNSUPPORTED, "pcwd_approx computes in fp64: create the handle with dtype F64");
+  if (h->desc.world != 1) return fail(PCWD_E_STATE, "pcwd_approx needs world = 1");
+  if (P.m > 64) return fail(PCWD_E_UNSUPPORTED, "pcwd_approx supports m <= 64");
+  CK(cudaSetDevice(h->desc.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t N = P.N;
+  const int bins = approx_bins();
+  // classes: (sub-band, position mod 2^{J-ℓ}) in sub-band order
+  ApproxArgs A{};
+  int64_t nc = 0;
+  for (int s = 0; s < P.nsb; ++s) {
+    A.clsbase[s] = nc;
+    const int64_t M = int64_t(1) << (P.J - P.sb[s].level);
+    nc += P.d == 2 ? M * M : M;
+  }
+  A.clsbase[P.nsb] = nc;
+  A.ncls = nc;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->desc.device);
+  const int grid = int(std::min<int64_t>(nc, int64_t(nsm) * 2));
+  A.cstride = (5 + int64_t(P.m)) * N;
+  struct Bufs {
+    double *scratch = nullptr, *rowh = nullptr, *colh = nullptr;
+    int64_t* cnt = nullptr;
+    ~Bufs() { cudaFree(scratch); cudaFree(rowh); cudaFree(colh); cudaFree(cnt); }
+  } B;
+  CK(dalloc(&B.scratch, size_t(grid) * A.cstride * sizeof(double)));
+  CK(dalloc(&B.rowh, size_t(nc) * P.m * bins * sizeof(double)));
+  CK(dalloc(&B.colh, size_t(nc) * P.m * bins * sizeof(double)));
+  CK(dalloc(&B.cnt, size_t(N) * sizeof(int64_t)));
+  CK(cudaMemsetAsync(B.colh, 0, size_t(nc) * P.m * bins * sizeof(double), st));
+  if (int rc = build_templates(h, st)) return rc;
+  A.T = static_cast<const double*>(h->T_d);
+  A.v = static_cast<const double*>(h->v_d);
+  A.scratch = B.scratch;
+  A.rowhist = B.rowh;
+  A.colhist = B.colh;
+  A.cnt = B.cnt;
+  // pass 0: |A_k| by truncation index (row and column sums of every class)
+  CK(launch_approx_stats(P, A, grid, st));
+  std::vector<double> rowh(size_t(nc) * P.m * bins), colh(size_t(nc) * P.m * bins), vh(size_t(P.m) * N);
+  CK(cudaMemcpyAsync(rowh.data(), B.rowh, rowh.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(colh.data(), B.colh, colh.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(vh.data(), h->v_d, vh.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  pcwd_approx_info info{};
+  info.eta = eta;
+  info.m = P.m;
+  for (int k = 0; k < P.m; ++k) {
+    double vinf = 0.0;
+    for (int64_t i = 0; i < N; ++i) vinf = std::max(vinf, std::fabs(vh[size_t(k) * N + i]));
+    const double eps = vinf > 0.0 ? eta / (P.m * vinf) : HUGE_VAL;
+    // dropped part at index S: entries with S_keep > S; its max row / column abs sums over the classes
+    int smax = -1;
+    for (int64_t c = 0; c < nc; ++c)
+      for (int b = 0; b < bins; ++b)
+        if (rowh[(size_t(c) * P.m + k) * bins + b] > 0.0) smax = std::max(smax, b);
+    int Sk = smax;
+    double bk = 0.0;
+    for (int S = -1; S <= smax; ++S) {
+      double mr = 0.0, mc = 0.0;
+      for (int64_t c = 0; c < nc; ++c) {
+        double r = 0.0, q = 0.0;
+        for (int b = S + 1; b < bins; ++b) {
+          r += rowh[(size_t(c) * P.m + k) * bins + b];
+          q += colh[(size_t(c) * P.m + k) * bins + b];
+        }
+        mr = std::max(mr, r);
+        mc = std::max(mc, q);
+      }
+      const double bound = std::sqrt(mr * mc);
+      if (bound <= eps) { Sk = S; bk = bound; break; }
+    }
+    A.S[k] = Sk;
+    info.S[k] = Sk;
+    info.eps[k] = eps;
+    info.bound[k] = bk;
+  }
+  // pass 1: nonzeros per row of Θ̃; host scan; pass 2: write
+  CK(launch_approx_rows(P, A, 0, 8, grid, st));
+  std::vector<int64_t> cnt(N), rp(N + 1, 0);
+  CK(cudaMemcpyAsync(cnt.data(), B.cnt, N * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < N; ++i) rp[i + 1] = rp[i] + cnt[i];
+  const int64_t nnz = rp[N];
+  if (nnz > h->cap) {
+    if (h->col) { cudaFree(h->col); h->col = nullptr; }
+    if (h->val) { cudaFree(h->val); h->val = nullptr; }
+    h->cap = 0;
+    h->nnz = 0;
+    h->decomposed = false;
+    CK(dalloc(&h->col, std::max<int64_t>(nnz, 1) * sizeof(int32_t)));
+    if (dalloc(&h->val, std::max<int64_t>(nnz, 1) * h->hp.out_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(h->col);
+      h->col = nullptr;
+      return fail(PCWD_E_OOM, "CSR of Θ̃ does not fit in device memory");
+    }
+    h->cap = nnz;
+  }
+  CK(cudaMemcpyAsync(h->row_ptr, rp.data(), (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  A.row_ptr = h->row_ptr;
+  A.col = h->col;
+  A.val = h->val;
+  CK(launch_approx_rows(P, A, 1, h->hp.out_bytes, grid, st));
+  CK(cudaStreamSynchronize(st));
+  h->nnz = nnz;
+  h->decomposed = true;
+  h->tvalid = false;
+  h->M_set = false;
+  h->cand_valid = false;
+  info.nnz = nnz;
+  if (out) *out = info;
   return PCWD_OK;
 }
 

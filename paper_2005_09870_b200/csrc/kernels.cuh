@@ -170,6 +170,31 @@ cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t
 cudaError_t launch_wavelet_transform(const Plan& P, const void* in, void* out, void* work0, void* work1, int inverse,
                                      int rb, cudaStream_t st);
 
+// Algorithm 1 (approx.cu): classes = (sub-band, position mod 2^{J−ℓ}), ordered by sub-band (clsbase[s] = first
+// class of sub-band s).  Scratch per CTA: (5 + m) N doubles.
+struct ApproxArgs {
+  const double* T;          // templates (fp64)
+  const double* v;          // m × N (fp64)
+  double* scratch;
+  int64_t cstride;          // doubles per CTA
+  int64_t ncls;
+  int64_t clsbase[kMaxSB + 1];
+  int S[64];                // truncation index per k (−1: Ã_k = 0)
+  double* rowhist;          // stats: ncls × m × bins
+  double* colhist;          // stats: ncls × m × bins (zeroed by the caller)
+  int64_t* cnt;             // count pass: per unit
+  const int64_t* row_ptr;   // write pass
+  int32_t* col;
+  void* val;
+};
+int approx_block();
+int approx_bins();
+cudaError_t launch_approx_stats(const Plan& P, const ApproxArgs& A, int grid, cudaStream_t st);
+cudaError_t launch_approx_rows(const Plan& P, const ApproxArgs& A, int write, int out_bytes, int grid, cudaStream_t st);
+// y = H f or H* f on the plan's grid (direct sums over the planned box of supp u_k); f, out: N of the compute type.
+cudaError_t launch_operator(const Plan& P, const double* u, const void* v, const void* f, void* out, int adjoint,
+                            int real_bytes, cudaStream_t st);
+
 cudaError_t launch_band_batched(const Plan& P, const BatchArgs& A, int real_bytes, int64_t maxX0, const int64_t* workA,
                                 const int64_t* workB, const int64_t* appr0, const int64_t* appr1, int steps,
                                 cudaStream_t st, int* launches);

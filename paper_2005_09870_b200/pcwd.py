@@ -50,11 +50,17 @@ class Info(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int32), ("compute_dtype", ctypes.c_int32)]
 
 
+class ApproxInfo(ctypes.Structure):
+    _fields_ = [("eta", ctypes.c_double), ("m", ctypes.c_int32), ("S", ctypes.c_int32 * 64),
+                ("eps", ctypes.c_double * 64), ("bound", ctypes.c_double * 64), ("nnz", ctypes.c_int64)]
+
+
 EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_max", "pcwd_get_csr",
            "pcwd_copy_csr", "pcwd_apply", "pcwd_info", "pcwd_destroy", "pcwd_error_string",
            "pcwd_last_error", "pcwd_validate", "pcwd_plan_shard", "pcwd_plan_stencil",
            "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile",
-           "pcwd_set_kernels", "pcwd_decompose_to_host", "pcwd_wavelet_transform", "pcwd_fista"]
+           "pcwd_set_kernels", "pcwd_decompose_to_host", "pcwd_wavelet_transform", "pcwd_fista",
+           "pcwd_approx", "pcwd_operator_apply"]
 
 _lib = None
 
@@ -91,6 +97,8 @@ def lib():
         L.pcwd_decompose_to_host.argtypes = [vp, vp, vp, vp, vp]
         L.pcwd_wavelet_transform.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         L.pcwd_fista.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), vp, vp]
+        L.pcwd_approx.argtypes = [vp, ctypes.c_double, vp, ctypes.POINTER(ApproxInfo)]
+        L.pcwd_operator_apply.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         for f in EXPORTS:
             getattr(L, f)  # every declared symbol must exist
         _lib = L
@@ -194,6 +202,22 @@ class Decomposition:
         _check(lib().pcwd_fista(self._h, ctypes.c_void_p(_ptr(z0)), ctypes.c_void_p(_ptr(w)), int(iters), int(precond),
                                 ctypes.byref(t), ctypes.c_void_p(_ptr(z)), ctypes.c_void_p(stream)), "pcwd_fista")
         return z, t.value
+
+    def approx(self, eta: float, stream: int = 0) -> dict:
+        """Algorithm 1's η-approximation Θ̃ into this handle's CSR (pcwd_approx); returns the per-k truncation."""
+        inf = ApproxInfo()
+        _check(lib().pcwd_approx(self._h, ctypes.c_double(eta), ctypes.c_void_p(stream), ctypes.byref(inf)), "pcwd_approx")
+        m = inf.m
+        return {"eta": inf.eta, "S": list(inf.S[:m]), "eps": list(inf.eps[:m]), "bound": list(inf.bound[:m]),
+                "nnz": inf.nnz}
+
+    def operator_apply(self, x, adjoint: bool = False, stream: int = 0):
+        """H x (or H* x) on the device (pcwd_operator_apply): x a CUDA tensor of N values of the handle's dtype."""
+        import torch
+        y = torch.empty_like(x)
+        _check(lib().pcwd_operator_apply(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(y)), int(adjoint),
+                                         ctypes.c_void_p(stream)), "pcwd_operator_apply")
+        return y
 
     def local_max(self, stream: int = 0) -> float:
         out = ctypes.c_double()
