@@ -198,6 +198,27 @@ int pcwd_approx(void* handle, double eta, void* stream, pcwd_approx_info* out);
  * Enqueued on stream. */
 int pcwd_operator_apply(void* handle, const void* x, void* y, int adjoint, void* stream);
 
+/* ---- constructing the product-convolution expansion (§3.3) ------------------
+ * Both factor impulse responses given on the window [−R, R]^d around the origin (W = (2R+1)^d values per response,
+ * row-major over the offsets (z0, z1) = (a − R, b − R); 2R + 1 ≤ n): u_k = the m leading left singular vectors of
+ * the W × s matrix of responses (uncentred PCA, R10; sign: largest-|entry| positive), found on the GPU by
+ * subspace iteration from a seeded Gaussian block with CholeskyQR2 re-orthonormalisation and a Rayleigh–Ritz step
+ * (Jacobi).  Outputs: u (m × N, u_k(z) stored at index z mod n, taps that wrap accumulate) and v (m × N), both
+ * DEVICE arrays allocated by the caller — they can be passed straight to pcwd_create / pcwd_set_kernels — and
+ * sigma (HOST, m singular values).  Inputs host or device.  m + oversample ≤ 32.  Synchronous. */
+
+/* §3.3.2: responses sampled at the g^d cell centres y_i = (n/g)(i + ½) (reading R11), irs = g^d × W
+ * (sample-major, row-major grid); v_k = periodic bilinear interpolation of the projections <S(·, y_i), u_k>
+ * between the cell centres (R12); g = n: one response per pixel, v_k(y) = the projection itself. */
+int pcwd_pc_from_samples(int32_t d, int32_t n, int32_t R, int32_t g, int32_t m, const double* irs, double* u,
+                         double* v, double* sigma, void* stream);
+/* §3.3.3: randomized SVD of the space-varying impulse response S given at every pixel: svir = N × W
+ * (row y = S(·, y) on the window), `oversample` extra columns, `power_iters` subspace iterations, `seed` of the
+ * counter-based Gaussian start; v_k(y) = <S(·, y), u_k> (so Σ_k u_k v_kᵀ is the rank-m truncated SVD, the
+ * Frobenius-optimal product-convolution expansion of P:241). */
+int pcwd_pc_from_svir(int32_t d, int32_t n, int32_t R, int32_t m, const double* svir, int32_t oversample,
+                      int32_t power_iters, uint64_t seed, double* u, double* v, double* sigma, void* stream);
+
 int pcwd_info(void* handle, pcwd_info_t* out);
 
 /* Phase timing with CUDA events recorded on the decompose stream around each phase

@@ -1483,6 +1483,49 @@ int pcwd_operator_apply(void* handle, const void* x, void* y, int adjoint, void*
   return PCWD_OK;
 }
 
+// ---- constructing the product-convolution expansion (pca.cu) ---------------------------------------------------
+static int pc_common(int d, int n, int R, int m, int64_t s, const double* X, int g, int oversample, int power_iters,
+                     uint64_t seed, double* u, double* v, double* sigma, cudaStream_t st) {
+  if (!X || !u || !v || !sigma) return fail(PCWD_E_PARAM, "NULL argument");
+  if (d != 1 && d != 2) return fail(PCWD_E_SHAPE, "d must be 1 or 2");
+  if (n < 2 || (n & (n - 1))) return fail(PCWD_E_SHAPE, "n must be a power of two >= 2");
+  if (R < 0 || 2 * R + 1 > n) return fail(PCWD_E_PARAM, "window 2R+1 must fit the torus");
+  const int W = d == 2 ? (2 * R + 1) * (2 * R + 1) : 2 * R + 1;
+  if (m < 1 || m > W || m > s || m + std::max(oversample, 0) > 32)
+    return fail(PCWD_E_PARAM, "need 1 <= m <= min(W, samples) and m + oversample <= 32");
+  if (power_iters < 1) return fail(PCWD_E_PARAM, "power_iters must be >= 1");
+  const bool dev = is_device_ptr(X);
+  double *Xd = nullptr, *U = nullptr, *c = nullptr;
+  struct F { double** p[3]; bool own; ~F() { if (own && *p[0]) cudaFree(*p[0]); cudaFree(*p[1]); cudaFree(*p[2]); } } fr{{&Xd, &U, &c}, !dev};
+  if (dev) Xd = const_cast<double*>(X);
+  else {
+    CK(dalloc(&Xd, sizeof(double) * s * W));
+    CK(cudaMemcpyAsync(Xd, X, sizeof(double) * s * W, cudaMemcpyHostToDevice, st));
+  }
+  CK(dalloc(&U, sizeof(double) * W * m));
+  CK(dalloc(&c, sizeof(double) * s * m));
+  int rc = pcwd_pca::factor(Xd, s, W, m, oversample, power_iters, seed, U, c, sigma, st);
+  if (rc) return fail(rc, "factorisation failed");
+  rc = pcwd_pca::finish(U, c, d, n, R, g, m, u, v, st);
+  if (rc) return fail(rc, "embedding / interpolation failed");
+  CK(cudaStreamSynchronize(st));
+  return PCWD_OK;
+}
+
+int pcwd_pc_from_samples(int32_t d, int32_t n, int32_t R, int32_t g, int32_t m, const double* irs, double* u,
+                         double* v, double* sigma, void* stream) {
+  if (g < 1 || g > n) return fail(PCWD_E_PARAM, "g must be in [1, n]");
+  const int64_t s = d == 2 ? int64_t(g) * g : g;
+  return pc_common(d, n, R, m, s, irs, g, 8, 24, 0x5eed5eedULL, u, v, sigma, static_cast<cudaStream_t>(stream));
+}
+
+int pcwd_pc_from_svir(int32_t d, int32_t n, int32_t R, int32_t m, const double* svir, int32_t oversample,
+                      int32_t power_iters, uint64_t seed, double* u, double* v, double* sigma, void* stream) {
+  const int64_t s = d == 2 ? int64_t(n) * n : n;
+  return pc_common(d, n, R, m, s, svir, n, oversample, power_iters, seed, u, v, sigma,
+                   static_cast<cudaStream_t>(stream));
+}
+
 int pcwd_approx(void* handle, double eta, void* stream, pcwd_approx_info* out) {
   Handle* h = static_cast<Handle*>(handle);
   if (!h) return fail(PCWD_E_PARAM, "NULL handle");

@@ -248,3 +248,10 @@ cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void*
                                cudaStream_t st);
 
 }  // namespace pcwd
+
+// pca.cu: factorisation of impulse-response rows X (s × W, device) — see the file header.
+namespace pcwd_pca {
+int factor(const double* X, int64_t s, int W, int m, int oversample, int power_iters, uint64_t seed, double* U,
+           double* c, double* sigma, cudaStream_t st);
+int finish(const double* U, const double* c, int d, int n, int R, int g, int m, double* u, double* v, cudaStream_t st);
+}  // namespace pcwd_pca

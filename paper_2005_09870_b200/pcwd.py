@@ -60,7 +60,7 @@ EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_m
            "pcwd_last_error", "pcwd_validate", "pcwd_plan_shard", "pcwd_plan_stencil",
            "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile",
            "pcwd_set_kernels", "pcwd_decompose_to_host", "pcwd_wavelet_transform", "pcwd_fista",
-           "pcwd_approx", "pcwd_operator_apply"]
+           "pcwd_approx", "pcwd_operator_apply", "pcwd_pc_from_samples", "pcwd_pc_from_svir"]
 
 _lib = None
 
@@ -99,6 +99,8 @@ def lib():
         L.pcwd_fista.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), vp, vp]
         L.pcwd_approx.argtypes = [vp, ctypes.c_double, vp, ctypes.POINTER(ApproxInfo)]
         L.pcwd_operator_apply.argtypes = [vp, vp, vp, ctypes.c_int, vp]
+        L.pcwd_pc_from_samples.argtypes = [i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]
+        L.pcwd_pc_from_svir.argtypes = [i32, i32, i32, i32, vp, i32, i32, ctypes.c_uint64, vp, vp, vp, vp]
         for f in EXPORTS:
             getattr(L, f)  # every declared symbol must exist
         _lib = L
@@ -326,6 +328,34 @@ def allreduce_sum(x: float, device: int = 0) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def _pc_out(m: int, N: int, device: int):
+    import torch
+    dev = torch.device("cuda", device)
+    return (torch.empty((m, N), dtype=torch.float64, device=dev), torch.empty((m, N), dtype=torch.float64, device=dev),
+            np.zeros(m))
+
+
+def pc_from_samples(d: int, n: int, R: int, g: int, m: int, irs, device: int = 0, stream: int = 0):
+    """§3.3.2 on the GPU (pcwd_pc_from_samples): (u, v) as (m, N) fp64 CUDA tensors and the singular values."""
+    irs = np.ascontiguousarray(irs, dtype=np.float64) if isinstance(irs, np.ndarray) else irs
+    u, v, sig = _pc_out(m, n ** d, device)
+    _check(lib().pcwd_pc_from_samples(d, n, R, g, m, ctypes.c_void_p(_ptr(irs)), ctypes.c_void_p(_ptr(u)),
+                                      ctypes.c_void_p(_ptr(v)), sig.ctypes.data_as(ctypes.c_void_p),
+                                      ctypes.c_void_p(stream)), "pcwd_pc_from_samples")
+    return u, v, sig
+
+
+def pc_from_svir(d: int, n: int, R: int, m: int, svir, oversample: int = 8, power_iters: int = 16, seed: int = 1,
+                 device: int = 0, stream: int = 0):
+    """§3.3.3 on the GPU (pcwd_pc_from_svir): randomized SVD of the SVIR given at every pixel (N × W)."""
+    svir = np.ascontiguousarray(svir, dtype=np.float64) if isinstance(svir, np.ndarray) else svir
+    u, v, sig = _pc_out(m, n ** d, device)
+    _check(lib().pcwd_pc_from_svir(d, n, R, m, ctypes.c_void_p(_ptr(svir)), oversample, power_iters,
+                                   ctypes.c_uint64(seed), ctypes.c_void_p(_ptr(u)), ctypes.c_void_p(_ptr(v)),
+                                   sig.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(stream)), "pcwd_pc_from_svir")
+    return u, v, sig
 
 
 def _coll_device(device: int = 0):

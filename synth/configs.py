@@ -69,6 +69,26 @@ class Problem:
             s.update(np.ascontiguousarray(self.pat_col, dtype=np.int32).tobytes())
         return s.hexdigest()
 
+    def fingerprint(self) -> list:
+        """Rounding-robust summary of the inputs (sums, sums of squares, weighted sums, 16 sampled entries of h, u, v):
+        the PCA and FFT steps of the recipes go through LAPACK / BLAS / pocketfft, whose last bits differ between
+        CPUs, so the sha256 of the fp64 inputs is machine-dependent while these agree to ~1e-15 relative."""
+        out = []
+        rng = np.random.default_rng(12345)
+        for a in (self.h, self.u, self.v):
+            x = np.ascontiguousarray(a, dtype=np.float64).ravel()
+            w = rng.uniform(-1.0, 1.0, size=x.size)
+            idx = rng.integers(0, x.size, size=16)
+            out += [float(x.sum()), float(np.dot(x, x)), float(np.dot(w, x))] + [float(v) for v in x[idx]]
+        return out
+
+    def fingerprint_matches(self, fp, rtol: float = 1e-10) -> bool:
+        mine = self.fingerprint()
+        if len(mine) != len(fp):
+            return False
+        scale = max(abs(v) for v in mine) or 1.0
+        return all(abs(a - b) <= rtol * max(abs(a), abs(b), 1e-6 * scale) for a, b in zip(mine, fp))
+
 
 # ----------------------------------------------------------------------------- helpers
 
@@ -293,6 +313,34 @@ def micro(n: int, d: int, M: int, J: int, m: int, R: int, seed: int, retain: str
     return Problem(f"micro_n{n}_d{d}_M{M}_J{J}_m{m}_R{R}_s{seed}_{retain}", d, n, J,
                    daubechies(M), u, v, retain, tau_rel=tau_rel, band_L=band_L,
                    dtypes=("f64", "f32"))
+
+
+def c2_samples():
+    """The sampled impulse responses config 2 is built from (8 × 8 cell centres, R = 9): (irs (64, 361), n, R, g, m)."""
+    n, m, R, g = 64, 5, 9, 8
+    dy, dx = _offsets(R, 2)
+
+    def ir(y0, x0):
+        sig = 1.0 + 2.0 * (x0 + y0) / 128.0
+        return np.exp(-(dx ** 2 + dy ** 2) / (2 * sig * sig)).ravel()
+
+    cs = (n // g) * np.arange(g) + (n // g) // 2
+    return _normalise(np.stack([ir(a, b) for a in cs for b in cs])), n, R, g, m
+
+
+def svir_anisotropic(n: int, R: int) -> np.ndarray:
+    """The space-varying impulse response of config 3's recipe (anisotropic rotated Gaussian, σx = 1 + 3x/n,
+    σy = 1 + 3y/n, angle πx/n) at EVERY pixel of an n × n torus: (N, (2R+1)²), rows normalised to unit sum."""
+    dy, dx = _offsets(R, 2)
+    out = np.zeros((n * n, (2 * R + 1) ** 2))
+    for y0 in range(n):
+        for x0 in range(n):
+            sx, sy, th = 1 + 3.0 * x0 / n, 1 + 3.0 * y0 / n, math.pi * x0 / n
+            c, s = math.cos(th), math.sin(th)
+            a = c * dx + s * dy
+            b = -s * dx + c * dy
+            out[y0 * n + x0] = np.exp(-0.5 * ((a / sx) ** 2 + (b / sy) ** 2)).ravel()
+    return _normalise(out)
 
 
 def random_pattern(N: int, max_per_row: int, seed: int, empty_every: int = 7):

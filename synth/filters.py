@@ -50,6 +50,71 @@ def daubechies(M: int) -> np.ndarray:
     return h
 
 
+def _phase_nonlinearity(h: np.ndarray, grid: int = 512) -> float:
+    """Mean squared deviation of the unwrapped phase of H(e^{iω}) = Σ h[n] e^{-iωn} from its best linear fit on
+    ω ∈ (0, π) (the least-asymmetric criterion)."""
+    w = np.linspace(1e-3, math.pi - 1e-3, grid)
+    H = np.exp(-1j * np.outer(w, np.arange(len(h)))) @ h
+    ph = np.unwrap(np.angle(H))
+    A = np.stack([w, np.ones_like(w)], axis=1)
+    coef, *_ = np.linalg.lstsq(A, ph, rcond=None)
+    return float(np.mean((ph - A @ coef) ** 2))
+
+
+def symlet(M: int) -> np.ndarray:
+    """Least-asymmetric Daubechies ("Symmlet") low-pass filter with M vanishing moments (2M taps) — the paper's
+    basis is the Symmlet of order 6.
+
+    Same spectral factorisation as `daubechies` (so |m0(ω)| is identical), but instead of taking every root inside
+    the unit circle, one root of each reciprocal pair {z, 1/z} is chosen so that the phase of m0 is closest to
+    linear (reading R4b).  Conjugate y-roots are chosen together (h stays real).  Of the two mirror-image
+    optima (h and its reversal) the one with the later energy centre Σ n h[n]² is returned.
+    """
+    if M < 1:
+        raise ValueError("M must be >= 1")
+    if M == 1:
+        return daubechies(1)
+    coeffs = [math.comb(M - 1 + k, k) for k in range(M)]
+    yroots = np.roots(coeffs[::-1])
+    groups, used = [], [False] * len(yroots)
+    for i, yr in enumerate(yroots):
+        if used[i]:
+            continue
+        used[i] = True
+        g = [i]
+        if abs(yr.imag) > 1e-12:
+            j = min((j for j in range(len(yroots)) if not used[j]), key=lambda j: abs(yroots[j] - np.conj(yr)))
+            used[j] = True
+            g.append(j)
+        groups.append(g)
+
+    def zpair(yr):
+        b = 2.0 - 4.0 * yr
+        disc = np.sqrt(b * b - 4.0 + 0j)
+        z1, z2 = (b + disc) / 2.0, (b - disc) / 2.0
+        return (z1, z2) if abs(z1) < 1.0 else (z2, z1)   # (inside, outside)
+
+    best = None
+    for mask in range(1 << len(groups)):
+        poly = np.array([1.0 + 0j])
+        for _ in range(M):
+            poly = np.convolve(poly, [1.0, 1.0])
+        for gi, g in enumerate(groups):
+            for i in g:
+                z = zpair(yroots[i])[(mask >> gi) & 1]
+                poly = np.convolve(poly, [1.0, -z])
+        h = np.real(poly)
+        h = h * (math.sqrt(2.0) / h.sum())          # any factor of |m0|² with m0(0) = √2 has ‖h‖₂ = 1
+        score = _phase_nonlinearity(h)
+        if best is None or score < best[0] - 1e-12:
+            best = (score, h)
+    h = best[1]
+    n = np.arange(len(h))
+    if np.dot(n, h ** 2) < np.dot(n, h[::-1] ** 2):
+        h = h[::-1].copy()
+    return h
+
+
 def haar() -> np.ndarray:
     return daubechies(1)
 

@@ -14,6 +14,7 @@ torch = pytest.importorskip("torch")
 from oracle import operator as op, retention as ret, rows as R  # noqa: E402
 from paper_2005_09870_b200 import Decomposition, Spec  # noqa: E402
 from synth import configs as C  # noqa: E402
+from conftest import record_parity  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -53,6 +54,27 @@ def compare(p, g, units, rows_ref, dtype, M=None):
         num += float(np.sum((v - ref) ** 2))
         den += float(np.sum(ref ** 2))
     err = (num / den) ** 0.5 if den > 0 else num ** 0.5
+    record_parity(p.name, dtype, err, len(units))
+    assert err <= TOL[dtype], f"relative Frobenius error {err:.3e} > {TOL[dtype]}"
+    return err
+
+
+def compare_cached(p, g, cache, dtype, name):
+    """Like compare, against cached oracle rows (tests/golden/cache, written by tools/oracle_cache.py from oracle/
+    only): columns bit-exact, relative Frobenius error over all cached units."""
+    assert p.fingerprint_matches(list(cache["inputs_fingerprint"])), "cache computed from other inputs"
+    units, crp, ccol, cval = cache["units"], cache["row_ptr"], cache["col"], cache["val"]
+    num = den = 0.0
+    for i, mu in enumerate(units):
+        r = int(mu) - g["row0"]
+        c = g["col"][g["rp"][r]:g["rp"][r + 1]]
+        v = g["val"][g["rp"][r]:g["rp"][r + 1]]
+        ref_c, ref_v = ccol[crp[i]:crp[i + 1]], cval[crp[i]:crp[i + 1]]
+        assert np.array_equal(c, ref_c), f"pattern mismatch, unit {mu}"
+        num += float(np.sum((v - ref_v) ** 2))
+        den += float(np.sum(ref_v ** 2))
+    err = (num / den) ** 0.5
+    record_parity(name, dtype, err, len(units))
     assert err <= TOL[dtype], f"relative Frobenius error {err:.3e} > {TOL[dtype]}"
     return err
 
@@ -204,23 +226,6 @@ def test_host_inputs_equal_device_inputs():
     assert np.array_equal(a["val"], b["val"]) and np.array_equal(a["col"], b["col"])
 
 
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_apply_matches_csr(dtype):
-    p = C.micro(16, 2, 4, 3, 2, 2, 24, retain="band", band_L=32)
-    g = run(p, dtype)
-    rng = np.random.default_rng(0)
-    x = rng.standard_normal(p.N)
-    tdt = torch.float64 if dtype == "f64" else torch.float32
-    y = g["dec"].apply(torch.tensor(x, dtype=tdt, device="cuda")).cpu().numpy()
-    dense = np.zeros((p.N, p.N))
-    for r in range(p.N):
-        dense[r, g["col"][g["rp"][r]:g["rp"][r + 1]]] = g["val"][g["rp"][r]:g["rp"][r + 1]]
-    tol = 1e-12 if dtype == "f64" else 1e-5
-    assert np.max(np.abs(y - dense @ x)) <= tol * np.max(np.abs(dense @ x))
-    yt = g["dec"].apply(torch.tensor(x, dtype=tdt, device="cuda"), transpose=True).cpu().numpy()
-    assert np.max(np.abs(yt - dense.T @ x)) <= tol * np.max(np.abs(dense.T @ x))
-
-
 # ----------------------------------------------------------------------------- kernel-path coverage
 
 def _kinds(p, dtype):
@@ -348,3 +353,138 @@ def test_zero_filter_gives_exact_zeros(retain):
         ref = ret.band_pattern_dense(p, 24)
         for mu in (0, 5, p.N - 1):
             assert np.array_equal(g["col"][g["rp"][mu]:g["rp"][mu + 1]], ref[mu])
+
+
+# ----------------------------------------------------------------------------- exhaustive coverage (round 2)
+
+CACHE = os.path.join(HERE, "golden", "cache")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_c5_every_fine_class_and_seam(dtype):
+    """c5 against cached oracle rows (tools/oracle_cache.py): for every level-1..3 sub-band one unit of each of the
+    16 position classes (p0 mod 4, p1 mod 4) of the fine kernel's geometry, plus units on row 0, row n_ℓ−1, column
+    0 and the last 8-unit round of a row for every class of the other axis; for every coarse sub-band its seam units
+    (corners, edge midpoints) and two interior units (all units when ≤ 16)."""
+    path = os.path.join(CACHE, "c5_band_rows.npz")
+    if not os.path.exists(path):
+        pytest.skip("c5 oracle cache not computed (tools/oracle_cache.py --config c5)")
+    p = C.get("c5")
+    g = run(p, dtype)
+    compare_cached(p, g, np.load(path), dtype, "c5_classes")
+
+
+def test_c3_every_fine_class_and_seam():
+    path = os.path.join(CACHE, "c3_band_rows.npz")
+    if not os.path.exists(path):
+        pytest.skip("c3 oracle cache not computed (tools/oracle_cache.py --config c3)")
+    p = C.get("c3")
+    g = run(p, "f32")
+    compare_cached(p, g, np.load(path), "f32", "c3_classes")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_all_units_128_L128(dtype):
+    """128², DB4, J = 5, band L = 128 (the c5 rule: class modulus M = 4 on the fine levels): every one of the 16,384
+    units against the oracle rows; levels 1-2 on the fine kernel."""
+    p = C.micro(128, 2, 4, 5, 3, 4, 61, retain="band", band_L=128)
+    kinds = _kinds(p, dtype)
+    assert ("fine", 1) in kinds and ("fine", 2) in kinds
+    g = run(p, dtype)
+    num = den = 0.0
+    for u0 in range(0, p.N, 2048):
+        units = list(range(u0, min(p.N, u0 + 2048)))
+        rows = R.rows(p, units)
+        for i, mu in enumerate(units):
+            cols = ret.band_partners(p, mu, 128)
+            c = g["col"][g["rp"][mu]:g["rp"][mu + 1]]
+            assert np.array_equal(c, cols), f"pattern mismatch, unit {mu}"
+            num += float(np.sum((g["val"][g["rp"][mu]:g["rp"][mu + 1]] - rows[i][cols]) ** 2))
+            den += float(np.sum(rows[i][cols] ** 2))
+    err = (num / den) ** 0.5
+    record_parity("micro128_L128_all_units", dtype, err, p.N)
+    assert err <= TOL[dtype]
+
+
+def test_c4_all_units_pattern():
+    """c4 (512², DB6, J = 7, |θ| ≥ 1e-5·max): every GPU row against the all-unit oracle sweep
+    (tools/c4_pattern_stats.py, oracle only): retained count and column hash of all 262,144 rows (bit-exact
+    pattern), the total, and the ±1 sketch Σθ·s(λ) per row — an unbiased estimate of the squared Frobenius error
+    summed over all rows (E[(Σ_i s_i e_i)²] = Σ_i e_i²)."""
+    path = os.path.join(HERE, "golden", "c4_pattern_stats.npz")
+    meta = os.path.join(HERE, "golden", "c4_pattern_stats.json")
+    if not os.path.exists(path):
+        pytest.skip("c4 all-unit statistics not computed (tools/c4_pattern_stats.py)")
+    from rowstats import row_stats
+    gold = np.load(path)
+    summ = json.load(open(meta))
+    p = C.get("c4")
+    assert p.fingerprint_matches(summ["inputs_fingerprint"])   # (sha256 is machine-dependent, see synth)
+    g = run(p, "f32")
+    assert abs(g["M"] - summ["M"]) <= 1e-12 * summ["M"]
+    assert g["nnz"] == summ["nnz"] == int(gold["cnt"].sum())
+    cnt, h, sk = row_stats(g["rp"], g["col"], g["val"])
+    bad = np.nonzero((cnt != gold["cnt"]) | (h != gold["hash"]))[0]
+    assert len(bad) == 0, f"{len(bad)} rows differ from the oracle pattern, first {bad[:10]}"
+    est = float(np.sqrt(np.sum((sk - gold["sketch"]) ** 2) / np.sum(gold["ssq"])))
+    record_parity("c4_all_units_sketch", "f32", est, p.N, nnz=int(g["nnz"]))
+    assert est <= TOL["f32"], est
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_apply_matches_oracle_theta_L(dtype):
+    """pcwd_apply (y = Θ_L x and Θ_Lᵀ x, the products of Eq. 7 / FISTA) against Θ_L built from the
+    oracle's dense Θ and its band pattern."""
+    p = C.micro(16, 2, 4, 3, 2, 2, 24, retain="band", band_L=32)
+    T = op.theta_dense(p)
+    TL = np.zeros_like(T)
+    for mu in range(p.N):
+        cols = ret.band_partners(p, mu, 32)
+        TL[mu, cols] = T[mu, cols]
+    g = run(p, dtype)
+    x = np.random.default_rng(0).standard_normal(p.N)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    y = g["dec"].apply(torch.tensor(x, dtype=tdt, device="cuda")).cpu().numpy()
+    yt = g["dec"].apply(torch.tensor(x, dtype=tdt, device="cuda"), transpose=True).cpu().numpy()
+    for got, ref in ((y, TL @ x), (yt, TL.T @ x)):
+        err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        record_parity("apply_theta_L", dtype, err, p.N)
+        assert err <= TOL[dtype]
+
+
+def test_apply_transpose_sums_over_shards():
+    """C-d: Θᵀx of a sharded Θ is the sum of the shards' partials Θ_rᵀ x[r0:r1] (pcwd_apply transpose = 1 per
+    shard handle), equal to the whole handle's Θᵀx."""
+    p = C.micro(16, 2, 4, 3, 2, 2, 25, retain="band", band_L=32)
+    x = np.random.default_rng(1).standard_normal(p.N)
+    full = run(p, "f64")
+    yt = full["dec"].apply(torch.tensor(x, device="cuda"), transpose=True).cpu().numpy()
+    acc = np.zeros(p.N)
+    for r in range(3):
+        g = run(p, "f64", world=3, rank=r)
+        xs = torch.tensor(x[g["row0"]:g["row1"]], device="cuda")
+        acc += g["dec"].apply(xs, transpose=True).cpu().numpy()
+    assert np.max(np.abs(acc - yt)) <= 1e-13 * np.max(np.abs(yt))
+
+
+@pytest.mark.parametrize("retain,L", [("full", 0), ("band", 96), ("threshold", 0)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_symlet6_parity(retain, L, dtype):
+    """The paper's own basis, the Symmlet of order 6 (12 taps): 32², J = 3, every unit."""
+    from synth.filters import symlet
+    p = C.micro(32, 2, 6, 3, 3, 3, 71, retain=retain, tau_rel=1e-4 if retain == "threshold" else 0.0, band_L=L)
+    p.h = symlet(6)
+    T = op.theta_dense(p)
+    g = run(p, dtype)
+    compare(p, g, list(range(p.N)), T, dtype, float(np.abs(T).max()))
+
+
+def test_symlet6_c5_geometry_band_fp32():
+    """The c5 operator (1024², J = 8, L = 128) on the Symmlet-6 basis (12 taps) through the band kernels: sampled
+    units of every sub-band against the oracle rows."""
+    from synth.filters import symlet
+    p = C.get("c5")
+    q = C.Problem("c5_sym6", p.d, p.n, p.J, symlet(6), p.u, p.v, "band", band_L=128)
+    g = run(q, "f32")
+    units = _sample_units(q, 2, 1, 3, seed=7)
+    compare(q, g, units, R.rows(q, units), "f32")

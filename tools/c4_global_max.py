@@ -48,6 +48,7 @@ def main():
         json.dump(state, open(ck, "w"))
         print(f"{hi}/{p.N} M={state['M']:.17g} arg={state['arg']} t={time.time()-t0:.0f}s", flush=True)
     out = {"config": a.config, "M": state["M"], "argmax_unit": state["arg"], "inputs_sha256": sha,
+           "inputs_fingerprint": p.fingerprint(),
            "how": "oracle/rows.c over all units, Parseval-pruned (tools/c4_global_max.py)"}
     here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     json.dump(out, open(os.path.join(here, "tests", "golden", f"{a.config}_global_max.json"), "w"), indent=1)

@@ -61,7 +61,7 @@ def main():
     out = os.path.join(ROOT, "tests", "golden", f"{a.config}_pattern_stats.npz")
     np.savez_compressed(out, cnt=st["cnt"].astype(np.int32), hash=st["hash"], sketch=st["sketch"],
                         ssq=st["ssq"], rmax=st["rmax"].astype(np.float64))
-    summ = {"config": a.config, "inputs_sha256": sha, "M": M, "tau": tau, "nnz": int(st["cnt"].sum()),
+    summ = {"config": a.config, "inputs_sha256": sha, "inputs_fingerprint": p.fingerprint(), "M": M, "tau": tau, "nnz": int(st["cnt"].sum()),
             "max_per_unit": int(st["cnt"].max()), "near_tau": int(st["near"].sum()),
             "max_rowmax": float(st["rmax"].max()), "argmax_unit": int(np.argmax(st["rmax"])),
             "how": "oracle/rows.c oracle_row_stats over all units (tools/c4_pattern_stats.py)"}

@@ -82,6 +82,7 @@ def main():
     out = os.path.join(ROOT, "tests", "golden", "cache", f"{a.config}_band_rows.npz")
     np.savez_compressed(out, units=units, row_ptr=np.array(rp, dtype=np.int64), col=np.concatenate(cols),
                         val=np.concatenate(vals), inputs_sha256=np.array(p.sha256()),
+                        inputs_fingerprint=np.array(p.fingerprint()),
                         how=np.array("oracle/rows.c + oracle/retention.py (tools/oracle_cache.py)"))
     print("wrote", out)
 
