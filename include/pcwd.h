@@ -198,6 +198,13 @@ int pcwd_approx(void* handle, double eta, void* stream, pcwd_approx_info* out);
  * Enqueued on stream. */
 int pcwd_operator_apply(void* handle, const void* x, void* y, int adjoint, void* stream);
 
+/* Algorithm 2's column orientation (ledger C1): for each λ of `lambdas` (host or
+ * device, count Λ indices) the whole column Θ[·][λ] = Ψ*(H ψ_λ), w_λ = H ψ_λ = Σ_k u_k ⋆ (v_k ⊙ ψ_λ) by direct
+ * sums over supp ψ_λ ⊕ supp u, then the whole-torus cascade.  out: DEVICE, count × N fp64 (row i = column λ_i).
+ * About m·|supp u| / (window) times the row path's work per unit (SURVEY §0 finding 2); meant for columns on
+ * demand and the C1 cross-check.  Synchronous. */
+int pcwd_columns(void* handle, const int64_t* lambdas, int64_t count, double* out, void* stream);
+
 /* ---- constructing the product-convolution expansion (§3.3) ------------------
  * Both factor impulse responses given on the window [−R, R]^d around the origin (W = (2R+1)^d values per response,
  * row-major over the offsets (z0, z1) = (a − R, b − R); 2R + 1 ≤ n): u_k = the m leading left singular vectors of
@@ -222,7 +229,9 @@ int pcwd_pc_from_svir(int32_t d, int32_t n, int32_t R, int32_t m, const double* 
 int pcwd_info(void* handle, pcwd_info_t* out);
 
 /* Phase timing with CUDA events recorded on the decompose stream around each phase
- * (enable = 1 before pcwd_decompose; read after the stream is synchronised).
+ * (enable = 1 before pcwd_decompose; read after the stream is synchronised).  enable = 2 also serialises the
+ * unit-kernel launches (no concurrent coarse streams) so that pcwd_launch_profile reports each kernel's own
+ * duration rather than overlapping stream spans.
  * Phases: 0 = templates (a1), 1 = unit kernels (a2+a3+a4), 2 = everything else (fills, scans,
  * threshold max/count passes).  out_ms[3] receives milliseconds of the last decompose;
  * out_fma[3] the algorithmic FMAs of phases 0 and 1 (phase 2: 0). */

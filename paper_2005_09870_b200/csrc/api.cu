@@ -82,6 +82,7 @@ struct Handle {
   bool M_set = false, tmpl_fresh = false, decomposed = false;
   int nlaunch = 0;
   bool profile = false;
+  bool profile_serial = false;      // pcwd_profile(h, 2): launches serialised (per-kernel times, no overlap)
   cudaEvent_t ev[8] = {};
   std::vector<cudaEvent_t> lev;     // profile: one event pair per unit launch (run_units)
   cudaStream_t cs = nullptr;        // decompose_to_host: copy stream
@@ -261,8 +262,8 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
   };
   // coarse (batched) levels are independent: each runs on its own stream with its own scratch slice,
   // forked from `st` after the templates and joined back before the next non-batched launch
-  const bool conc = h->conc && mode == MODE_BAND;
-  const bool conc_t = h->conc_t && (mode == MODE_TSTORE || mode == MODE_TMAX);
+  const bool conc = h->conc && mode == MODE_BAND && !h->profile_serial;
+  const bool conc_t = h->conc_t && (mode == MODE_TSTORE || mode == MODE_TMAX) && !h->profile_serial;
   // the fine kernels (on `st`) may also run beside the coarse streams: they share no data (all but the first,
   // largest one, which runs alone)
   static const bool overlap = getenv("PCWD_COARSE_OVERLAP") ? atoi(getenv("PCWD_COARSE_OVERLAP")) != 0 : true;
@@ -1483,6 +1484,32 @@ int pcwd_operator_apply(void* handle, const void* x, void* y, int adjoint, void*
   return PCWD_OK;
 }
 
+int pcwd_columns(void* handle, const int64_t* lambdas, int64_t count, double* out, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || (count > 0 && (!lambdas || !out))) return fail(PCWD_E_PARAM, "NULL argument");
+  if (count < 0) return fail(PCWD_E_PARAM, "count < 0");
+  if (count == 0) return PCWD_OK;
+  CK(cudaSetDevice(h->desc.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Plan& P = h->hp.P;
+  std::vector<int64_t> lh(count);
+  CK(cudaMemcpy(lh.data(), lambdas, count * sizeof(int64_t), cudaMemcpyDefault));
+  for (int64_t i = 0; i < count; ++i)
+    if (lh[i] < 0 || lh[i] >= P.N) return fail(PCWD_E_PARAM, "lambda index out of range");
+  const int64_t cstride = (3 + int64_t(P.m)) * P.N;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->desc.device);
+  const int64_t budget = int64_t(4) << 30;   // scratch: at most 4 GiB of CTA slices
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>({count, int64_t(nsm) * 2, budget / (cstride * 8)})));
+  struct B { double* s = nullptr; int64_t* l = nullptr; ~B() { cudaFree(s); cudaFree(l); } } b;
+  CK(dalloc(&b.s, size_t(grid) * cstride * sizeof(double)));
+  CK(dalloc(&b.l, count * sizeof(int64_t)));
+  CK(cudaMemcpyAsync(b.l, lh.data(), count * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CK(launch_columns(P, h->u_d, h->v_d, b.l, count, b.s, cstride, grid, out, h->hp.real_bytes, st));
+  CK(cudaStreamSynchronize(st));
+  return PCWD_OK;
+}
+
 // ---- constructing the product-convolution expansion (pca.cu) ---------------------------------------------------
 static int pc_common(int d, int n, int R, int m, int64_t s, const double* X, int g, int oversample, int power_iters,
                      uint64_t seed, double* u, double* v, double* sigma, cudaStream_t st) {
@@ -1672,6 +1699,7 @@ int pcwd_profile(void* handle, int enable) {
   if (enable && !h->ev[0])
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
   h->profile = enable != 0;
+  h->profile_serial = enable == 2;
   return PCWD_OK;
 }
 

@@ -365,6 +365,91 @@ __global__ void __launch_bounds__(kAB) approx_rows_kernel(const __grid_constant_
   }
 }
 
+// Algorithm 2's column orientation, fixed λ: w_λ = H ψ_λ = Σ_k u_k ⋆ (v_k ⊙ ψ_λ), then Θ[·][λ] = Ψ* w_λ.
+// One CTA per requested λ: ψ_λ = Ψ e_λ (whole-torus inverse cascade); q_k = v_k ⊙ ψ_λ on supp ψ_λ; w_λ(x) =
+// Σ_{y ∈ supp ψ_λ} Σ_k q_k(y) u_k(x − y) over the box supp ψ_λ ⊕ box(u) (zero elsewhere); Ψ* w_λ by the whole-torus
+// forward cascade.  Scratch per CTA: (3 + m) N doubles.
+template <typename Real>
+__global__ void __launch_bounds__(kAB) column_kernel(const __grid_constant__ Plan P, const double* __restrict__ u,
+                                                     const Real* __restrict__ v, const int64_t* __restrict__ lam,
+                                                     int64_t count, double* __restrict__ scratch, int64_t cstride,
+                                                     double* __restrict__ out) {
+  const int64_t N = P.N;
+  const int n = P.n;
+  double* psi = scratch + int64_t(blockIdx.x) * cstride;
+  double* w = psi + N;
+  double* y = w + N;
+  double* q = y + N;   // m × (box of supp ψ_λ)
+  for (int64_t it = blockIdx.x; it < count; it += gridDim.x) {
+    const int64_t l = lam[it];
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) w[i] = i == l ? 1.0 : 0.0;
+    __syncthreads();
+    inverse_full(P, w, psi, y);
+    int s, p0, p1;
+    locate(P, l, &s, &p0, &p1);
+    int st[2] = {0, 0}, ln[2] = {1, 1};
+    for (int a = (P.d == 2 ? 0 : 1); a < 2; ++a) supp_box(P, P.sb[s], a, a == 0 ? p0 : p1, &st[a], &ln[a]);
+    const int B = ln[0] * ln[1];
+    for (int t = threadIdx.x; t < B * P.m; t += blockDim.x) {
+      const int k = t / B, b = t - k * B;
+      const int b0 = b / ln[1], b1 = b - b0 * ln[1];
+      const int64_t yi = P.d == 2 ? int64_t(wrap(st[0] + b0, n)) * n + wrap(st[1] + b1, n) : wrap(st[1] + b1, n);
+      q[t] = double(v[int64_t(k) * N + yi]) * psi[yi];
+    }
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) w[i] = 0.0;
+    __syncthreads();
+    // output box: supp ψ_λ ⊕ [zlo, zhi] per axis (the whole line when it covers it)
+    int xs[2], xl[2];
+    for (int a = 0; a < 2; ++a) {
+      if (a == 0 && P.d == 1) { xs[0] = 0; xl[0] = 1; continue; }
+      const int wz = P.zhi[a] - P.zlo[a] + 1;
+      xl[a] = min(n, ln[a] + wz - 1);
+      xs[a] = xl[a] >= n ? 0 : wrap(st[a] + P.zlo[a], n);
+    }
+    for (int t = threadIdx.x; t < xl[0] * xl[1]; t += blockDim.x) {
+      const int i0 = t / xl[1], i1 = t - i0 * xl[1];
+      const int x0 = P.d == 2 ? wrap(xs[0] + i0, n) : 0, x1 = wrap(xs[1] + i1, n);
+      double acc = 0.0;
+      const int wu0 = P.d == 2 ? P.zhi[0] - P.zlo[0] + 1 : 1, wu1 = P.zhi[1] - P.zlo[1] + 1;
+      if (B <= wu0 * wu1) {   // gather over y ∈ supp ψ_λ
+        for (int b0 = 0; b0 < ln[0]; ++b0) {
+          const int y0 = P.d == 2 ? wrap(st[0] + b0, n) : 0;
+          const int z0 = P.d == 2 ? wrap(x0 - y0, n) : 0;
+          for (int b1 = 0; b1 < ln[1]; ++b1) {
+            const int y1 = wrap(st[1] + b1, n);
+            const int64_t zi = int64_t(z0) * n + wrap(x1 - y1, n);
+            const int b = b0 * ln[1] + b1;
+            for (int k = 0; k < P.m; ++k) {
+              const double uz = u[int64_t(k) * N + zi];
+              if (uz != 0.0) acc = fma(q[int64_t(k) * B + b], uz, acc);
+            }
+          }
+        }
+      } else {                // gather over z ∈ box(u): y = x − z must fall in supp ψ_λ
+        for (int a0 = 0; a0 < wu0; ++a0) {
+          const int z0 = P.d == 2 ? wrap(P.zlo[0] + a0, n) : 0;
+          const int b0 = P.d == 2 ? wrap(x0 - z0 - st[0], n) : 0;
+          if (b0 >= ln[0]) continue;
+          for (int a1 = 0; a1 < wu1; ++a1) {
+            const int z1 = wrap(P.zlo[1] + a1, n);
+            const int b1 = wrap(x1 - z1 - st[1], n);
+            if (b1 >= ln[1]) continue;
+            const int64_t zi = int64_t(z0) * n + z1;
+            const int b = b0 * ln[1] + b1;
+            for (int k = 0; k < P.m; ++k) {
+              const double uz = u[int64_t(k) * N + zi];
+              if (uz != 0.0) acc = fma(q[int64_t(k) * B + b], uz, acc);
+            }
+          }
+        }
+      }
+      w[P.d == 2 ? int64_t(x0) * n + x1 : x1] = acc;
+    }
+    __syncthreads();
+    forward_full(P, w, out + it * N, y);
+  }
+}
+
 // y = H f (adjoint = 0) or H* f (adjoint = 1), direct sums over the planned box of supp u_k:
 //   H f (x) = Σ_k Σ_z u_k(z) v_k(x − z) f(x − z),   H* g (y) = Σ_k v_k(y) Σ_z u_k(z) g(y + z).
 template <typename Real>
@@ -416,6 +501,15 @@ cudaError_t launch_approx_rows(const Plan& P, const ApproxArgs& A, int write, in
   if (!write) approx_rows_kernel<false, double><<<grid, kAB, 0, st>>>(P, A);
   else if (out_bytes == 8) approx_rows_kernel<true, double><<<grid, kAB, 0, st>>>(P, A);
   else approx_rows_kernel<true, float><<<grid, kAB, 0, st>>>(P, A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_columns(const Plan& P, const double* u, const void* v, const int64_t* lam, int64_t count,
+                           double* scratch, int64_t cstride, int grid, double* out, int real_bytes, cudaStream_t st) {
+  if (real_bytes == 8)
+    column_kernel<double><<<grid, kAB, 0, st>>>(P, u, static_cast<const double*>(v), lam, count, scratch, cstride, out);
+  else
+    column_kernel<float><<<grid, kAB, 0, st>>>(P, u, static_cast<const float*>(v), lam, count, scratch, cstride, out);
   return cudaGetLastError();
 }
 

@@ -191,6 +191,10 @@ int approx_block();
 int approx_bins();
 cudaError_t launch_approx_stats(const Plan& P, const ApproxArgs& A, int grid, cudaStream_t st);
 cudaError_t launch_approx_rows(const Plan& P, const ApproxArgs& A, int write, int out_bytes, int grid, cudaStream_t st);
+// Algorithm 2's columns Θ[·][λ] = Ψ*(H ψ_λ) for count indices lam (device), out: count × N fp64; scratch per CTA
+// cstride ≥ (3 + m) N doubles.
+cudaError_t launch_columns(const Plan& P, const double* u, const void* v, const int64_t* lam, int64_t count,
+                           double* scratch, int64_t cstride, int grid, double* out, int real_bytes, cudaStream_t st);
 // y = H f or H* f on the plan's grid (direct sums over the planned box of supp u_k); f, out: N of the compute type.
 cudaError_t launch_operator(const Plan& P, const double* u, const void* v, const void* f, void* out, int adjoint,
                             int real_bytes, cudaStream_t st);

@@ -7,8 +7,8 @@
 //
 // Both factor a matrix X (s × W): row i is one impulse response on the window [−R, R]^d (W = (2R+1)^d values).
 // u_k = the m leading right singular vectors of X (uncentred PCA, reading R10), found by subspace iteration on XᵀX
-// started from a seeded Gaussian block (counter-based generator), re-orthonormalised by CholeskyQR2 after every
-// product, then a Rayleigh–Ritz step (cyclic Jacobi on the r × r projected matrix).  Sign: the largest-|entry| of
+// started from a seeded Gaussian block (counter-based generator), re-orthonormalised (modified Gram–Schmidt, twice)
+// after every product, then a Rayleigh–Ritz step (cyclic Jacobi on the r × r projected matrix).  Sign: the largest-|entry| of
 // each u_k is positive.  c = X u (the projections).  All of it runs in these kernels; the host only sequences them.
 #include <algorithm>
 #include <cmath>
@@ -177,6 +177,56 @@ __global__ void small_kernel(const double* __restrict__ part, int nb, int r, int
   }
 }
 
+__device__ double block_sum(double x, double* red) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < int(blockDim.x >> 5); ++i) s += red[i];
+  return s;
+}
+
+// One CTA: Y (W × r) ← an orthonormal basis of its column span by modified Gram–Schmidt, each column orthogonalised
+// twice; a column that (numerically) lies in the span of the previous ones — the null space of a rank-deficient X —
+// is replaced by a fresh seeded Gaussian column and orthogonalised again.
+__global__ void mgs_kernel(double* Y, int W, int r, uint64_t seed) {
+  __shared__ double red[32];
+  for (int j = 0; j < r; ++j) {
+    for (int attempt = 0; attempt < 8; ++attempt) {
+      double n0 = 0.0;
+      for (int w = threadIdx.x; w < W; w += blockDim.x) n0 += Y[int64_t(w) * r + j] * Y[int64_t(w) * r + j];
+      n0 = sqrt(block_sum(n0, red));
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i = 0; i < j; ++i) {
+          double dp = 0.0;
+          for (int w = threadIdx.x; w < W; w += blockDim.x) dp += Y[int64_t(w) * r + i] * Y[int64_t(w) * r + j];
+          dp = block_sum(dp, red);
+          for (int w = threadIdx.x; w < W; w += blockDim.x) Y[int64_t(w) * r + j] -= dp * Y[int64_t(w) * r + i];
+          __syncthreads();
+        }
+      double nj = 0.0;
+      for (int w = threadIdx.x; w < W; w += blockDim.x) nj += Y[int64_t(w) * r + j] * Y[int64_t(w) * r + j];
+      nj = sqrt(block_sum(nj, red));
+      if (nj > 1e-12 * n0 && nj > 1e-300) {
+        for (int w = threadIdx.x; w < W; w += blockDim.x) Y[int64_t(w) * r + j] /= nj;
+        __syncthreads();
+        break;
+      }
+      for (int w = threadIdx.x; w < W; w += blockDim.x) {   // dependent column: restart it from noise
+        const uint64_t a = splitmix64(seed ^ (0xABCDULL + uint64_t(attempt) * 1000003ULL + uint64_t(j) * 7919ULL +
+                                              uint64_t(w) * 104729ULL));
+        const uint64_t b = splitmix64(a + 0x9E3779B97F4A7C15ULL);
+        const double u1 = (double(a >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+        const double u2 = double(b >> 11) * (1.0 / 9007199254740992.0);
+        Y[int64_t(w) * r + j] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // U (W × m) = Y (W × r) · V[:, :m], then the sign rule: the largest-|entry| of each column positive (first on ties).
 __global__ void ritz_kernel(const double* __restrict__ Y, const double* __restrict__ V, int W, int r, int m,
                             double* __restrict__ U) {
@@ -285,12 +335,10 @@ int factor(const double* X, int64_t s, int W, int m, int oversample, int power_i
     return PCWD_E_OOM;
   const int gw = int(std::min<int64_t>((s * 32 + kT - 1) / kT, 148 * 16));
   const int gt = int(std::min<int64_t>((int64_t(W) * r + kT - 1) / kT, 148 * 16));
-  auto orth = [&]() {   // CholeskyQR2 of Y (W × r)
-    for (int rep = 0; rep < 2; ++rep) {
-      gram_part_kernel<<<nbW, kT, 0, st>>>(Y, W, r, chunk, part);
-      small_kernel<<<1, kT, 0, st>>>(part, nbW, r, 0, Y, W, nullptr, nullptr);
-    }
-  };
+  // (CholeskyQR squares the condition number of Y, which the power iterations drive to ~(σ_1/σ_r)^2: modified
+  // Gram–Schmidt with re-orthogonalisation instead)
+  auto orth = [&]() { mgs_kernel<<<1, kT, 0, st>>>(Y, W, r, seed); };
+  (void)nbW;
   gauss_kernel<<<gt, kT, 0, st>>>(Y, W, r, seed);
   orth();
   for (int it = 0; it < power_iters; ++it) {   // Y ← orth(Xᵀ X Y)

@@ -60,7 +60,7 @@ EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_m
            "pcwd_last_error", "pcwd_validate", "pcwd_plan_shard", "pcwd_plan_stencil",
            "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile",
            "pcwd_set_kernels", "pcwd_decompose_to_host", "pcwd_wavelet_transform", "pcwd_fista",
-           "pcwd_approx", "pcwd_operator_apply", "pcwd_pc_from_samples", "pcwd_pc_from_svir"]
+           "pcwd_approx", "pcwd_operator_apply", "pcwd_pc_from_samples", "pcwd_pc_from_svir", "pcwd_columns"]
 
 _lib = None
 
@@ -100,6 +100,7 @@ def lib():
         L.pcwd_approx.argtypes = [vp, ctypes.c_double, vp, ctypes.POINTER(ApproxInfo)]
         L.pcwd_operator_apply.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         L.pcwd_pc_from_samples.argtypes = [i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]
+        L.pcwd_columns.argtypes = [vp, vp, ctypes.c_int64, vp, vp]
         L.pcwd_pc_from_svir.argtypes = [i32, i32, i32, i32, vp, i32, i32, ctypes.c_uint64, vp, vp, vp, vp]
         for f in EXPORTS:
             getattr(L, f)  # every declared symbol must exist
@@ -212,6 +213,16 @@ class Decomposition:
         m = inf.m
         return {"eta": inf.eta, "S": list(inf.S[:m]), "eps": list(inf.eps[:m]), "bound": list(inf.bound[:m]),
                 "nnz": inf.nnz}
+
+    def columns(self, lambdas, stream: int = 0):
+        """Algorithm 2's columns Θ[·][λ] (pcwd_columns) for the given Λ indices: a (count, N) fp64 CUDA tensor."""
+        import torch
+        lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.int64))
+        out = torch.empty((len(lam), int(self.info().N)), dtype=torch.float64,
+                          device=torch.device("cuda", self.spec.device))
+        _check(lib().pcwd_columns(self._h, ctypes.c_void_p(_ptr(lam)), ctypes.c_int64(len(lam)),
+                                  ctypes.c_void_p(_ptr(out)), ctypes.c_void_p(stream)), "pcwd_columns")
+        return out
 
     def operator_apply(self, x, adjoint: bool = False, stream: int = 0):
         """H x (or H* x) on the device (pcwd_operator_apply): x a CUDA tensor of N values of the handle's dtype."""
