@@ -173,24 +173,30 @@ int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int preco
 
 /* ---- Algorithm 1 proper: the η-approximation --------------------------------------- */
 
+typedef enum {
+  PCWD_TRUNC_INDEX = 0,     /* Theorem 2's Remark: drop |ℓ_λ − ℓ_μ| > S or ϑ(λ,μ) > 2^S (Definition 1)   */
+  PCWD_TRUNC_MAGNITUDE = 1  /* "simply threshold A": keep |A_k[μ][ν]| ≥ 2^{−(S+1)} (power-of-two steps)  */
+} pcwd_trunc_rule;
+
 typedef struct {
   double eta;             /* the requested precision η                                                    */
   int32_t m;
-  int32_t S[64];          /* per k: truncation index S_k of Ã_k (−1: Ã_k = 0)                              */
+  int32_t S[64];          /* per k: truncation index S_k of Ã_k (−1: Ã_k = 0); the rule's parameter        */
   double eps[64];         /* per k: ε_k = η / (m ‖v_k‖∞)    */
   double bound[64];       /* per k: Schur bound sqrt(‖E‖₁‖E‖_∞) ≥ ‖A_k − Ã_k‖₂ of the dropped part E       */
   int64_t nnz;            /* nonzeros of Θ̃                                                                 */
 } pcwd_approx_info;
 
 /* Algorithm 1: Θ̃ = Σ_k Ã_k B_k, an η-approximation of Θ (‖Θ − Θ̃‖₂ ≤ η), into the
- * handle's CSR (all nonzeros of Θ̃, columns increasing; replaces the last decompose — pcwd_get_csr, pcwd_apply and
- * pcwd_fista then work on Θ̃).  A_k = Ψ*U_kΨ, B_k = Ψ*V_kΨ; Ã_k zeroes the entries with |ℓ_λ − ℓ_μ| > S_k or
- * ϑ(λ,μ) > 2^{S_k} (Theorem 2's Remark P:1178, ϑ of Definition 1), S_k the smallest index whose dropped
- * part has Schur bound ≤ ε_k = η/(m‖v_k‖∞) (DESIGN.md R-A1..R-A3).  η > 0 (PCWD_E_PARAM).  Needs dtype F64 (the
+ * handle's CSR (Θ̃ on its predicted support, columns increasing; replaces the last decompose — pcwd_get_csr,
+ * pcwd_apply and pcwd_fista then work on Θ̃).  A_k = Ψ*U_kΨ, B_k = Ψ*V_kΨ; Ã_k is A_k truncated by `rule`
+ * (pcwd_trunc_rule: the Remark's index rule, or power-of-two magnitude thresholds) with the smallest index S_k
+ * whose dropped part has Schur bound sqrt(‖E‖₁‖E‖_∞) ≤ ε_k = η/(m‖v_k‖∞) (DESIGN.md R-A1..R-A4), so that
+ * ‖A_k − Ã_k‖₂ ≤ ε_k.  η > 0 and rule ∈ {0, 1} (PCWD_E_PARAM).  Needs dtype F64 (the
  * paper's precision; PCWD_E_UNSUPPORTED otherwise), world = 1 and m ≤ 64 (PCWD_E_STATE /
  * PCWD_E_UNSUPPORTED); whole-torus transforms per class of units, so meant for N ≤ 512² (the paper's η sweep is
  * at 256²).  out (may be NULL) receives the per-k truncation.  Synchronous. */
-int pcwd_approx(void* handle, double eta, void* stream, pcwd_approx_info* out);
+int pcwd_approx(void* handle, double eta, int rule, void* stream, pcwd_approx_info* out);
 
 /* y = H x (adjoint = 0) or y = H* x (adjoint = 1) on the handle's grid: H f = Σ_k u_k ⋆ (v_k ⊙ f) (Eq. 2,
  * P:29-32) by direct sums over the support box of the u_k.  x, y: DEVICE arrays of N values of the handle's dtype,

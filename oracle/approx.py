@@ -120,13 +120,20 @@ def choose_S(A: np.ndarray, Sk: np.ndarray, eps: float):
     return smax, 0.0
 
 
-def theta_tilde(p, eta: float, W: np.ndarray | None = None):
+def magnitude_bins(A: np.ndarray) -> np.ndarray:
+    """The magnitude rule's index ("simply threshold A"; reading R-A4): b with |a| ∈ [2^{-b-1}, 2^{-b}), from
+    the binary exponent, clamped to [0, 62]; index S keeps b ≤ S, i.e. |a| ≥ 2^{-(S+1)}."""
+    _, e = np.frexp(np.abs(A))
+    return np.clip(-e, 0, 62)
+
+
+def theta_tilde(p, eta: float, W: np.ndarray | None = None, rule: str = "index"):
     """Θ̃ of Algorithm 1, its bookkeeping {eps, S, bound} per k, and its predicted support (Lemma 9,
     P:1452): 𝒮 = supp(F·I) with F[μ][ν] = [Ã_k[μ][ν] ≠ 0 for some k] and I[ν][λ] = [supp ψ_ν ∩ supp ψ_λ ≠ ∅]
     (the set ℐ of P:1187, which contains supp B_k)."""
     if W is None:
         W = basis.analysis_matrix(p.d, p.n, p.J, p.h)
-    Sk = s_keep_matrix(p)
+    Sidx = s_keep_matrix(p) if rule == "index" else None
     T = np.zeros((p.N, p.N))
     F = np.zeros((p.N, p.N), dtype=bool)
     info = []
@@ -134,6 +141,7 @@ def theta_tilde(p, eta: float, W: np.ndarray | None = None):
         vinf = float(np.abs(p.v[k]).max())
         eps = eta / (p.m * vinf) if vinf > 0 else np.inf
         A = conv_rep(p, k, W)
+        Sk = Sidx if rule == "index" else magnitude_bins(A)
         S, b = choose_S(A, Sk, eps)
         At = np.where(Sk <= S, A, 0.0)
         T += At @ mult_rep(p, k, W)

@@ -1390,20 +1390,28 @@ int ensure_transpose(Handle* h, cudaStream_t st) {
   const int64_t N = h->hp.P.N, nnz = h->nnz;
   const int vb = h->hp.out_bytes;
   if (nnz > h->tcap) {
-    void* ptrs[] = {h->rpT, h->rowT, h->valT, h->twork};
+    void* ptrs[] = {h->rpT, h->rowT, h->valT};
     for (void* p : ptrs)
       if (p) cudaFree(p);
-    h->rpT = nullptr; h->rowT = nullptr; h->valT = nullptr; h->twork = nullptr;
+    h->rpT = nullptr; h->rowT = nullptr; h->valT = nullptr;
+    h->tcap = -1;   // consistent if an allocation below fails
     const int64_t cap = std::max<int64_t>(nnz, 1);
     CK(dalloc(&h->rpT, (N + 1) * sizeof(int64_t)));
     CK(dalloc(&h->rowT, cap * sizeof(int32_t)));
     CK(dalloc(&h->valT, cap * vb));
-    h->twork_bytes = csr_transpose_bytes(cap, N, vb) + ((N + 1) * 8 + 255) + (cap * 4 + 255) + (cap * vb + 255);
-    CK(dalloc(&h->twork, h->twork_bytes));
     h->tcap = cap;
   }
-  CK(csr_transpose(h->row_ptr, h->col, h->val, h->rows(), nnz, N, vb, h->rpT, h->rowT, h->valT, h->twork,
-                   h->twork_bytes, st));
+  // the sort's work space only lives while the transpose is built (Θ̃ of pcwd_approx can have billions of entries)
+  h->twork_bytes = csr_transpose_bytes(std::max<int64_t>(nnz, 1), N, vb) + ((N + 1) * 8 + 255);
+  CK(dalloc(&h->twork, h->twork_bytes));
+  const cudaError_t e = csr_transpose(h->row_ptr, h->col, h->val, h->rows(), nnz, N, vb, h->rpT, h->rowT, h->valT,
+                                      h->twork, h->twork_bytes, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaFree(h->twork);
+  h->twork = nullptr;
+  h->twork_bytes = 0;
+  CK(e);
+  CK(e2);
   h->tvalid = true;
   return PCWD_OK;
 }
@@ -1553,10 +1561,11 @@ int pcwd_pc_from_svir(int32_t d, int32_t n, int32_t R, int32_t m, const double* 
                    static_cast<cudaStream_t>(stream));
 }
 
-int pcwd_approx(void* handle, double eta, void* stream, pcwd_approx_info* out) {
+int pcwd_approx(void* handle, double eta, int rule, void* stream, pcwd_approx_info* out) {
   Handle* h = static_cast<Handle*>(handle);
   if (!h) return fail(PCWD_E_PARAM, "NULL handle");
   if (!(eta > 0.0)) return fail(PCWD_E_PARAM, "eta must be > 0");
+  if (rule != PCWD_TRUNC_INDEX && rule != PCWD_TRUNC_MAGNITUDE) return fail(PCWD_E_PARAM, "rule");
   const Plan& P = h->hp.P;
   if (h->hp.real_bytes != 8) return fail(PCWD_E_UNSUPPORTED, "pcwd_approx computes in fp64: create the handle with dtype F64");
   if (h->desc.world != 1) return fail(PCWD_E_STATE, "pcwd_approx needs world = 1");
@@ -1575,6 +1584,7 @@ int pcwd_approx(void* handle, double eta, void* stream, pcwd_approx_info* out) {
   }
   A.clsbase[P.nsb] = nc;
   A.ncls = nc;
+  A.rule = rule;
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->desc.device);
   const int grid = int(std::min<int64_t>(nc, int64_t(nsm) * 2));

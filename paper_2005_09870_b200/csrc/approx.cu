@@ -187,6 +187,15 @@ __device__ int s_keep(const Plan& P, int sm, int pm0, int pm1, int sn, int pn0, 
   return S;
 }
 
+// Magnitude rule ("simply threshold A", the Remark's alternative): bin b of |a| ∈ [2^{-b-1}, 2^{-b}) (exact,
+// from the binary exponent), clamped to [0, 62]; index S keeps the bins b ≤ S, i.e. |a| ≥ 2^{-(S+1)} (S = −1: none).
+// Power-of-two thresholds keep the decision away from rounding (a GPU/oracle flip needs |a| within an ulp of 2^-e).
+__device__ __forceinline__ int mag_bin(double a) {
+  int x;
+  frexp(fabs(a), &x);   // |a| = f·2^x, f ∈ [½, 1)
+  return min(max(-x, 0), 62);
+}
+
 // Λ index → (sub-band, p0, p1)
 __device__ __forceinline__ void locate(const Plan& P, int64_t idx, int* s, int* p0, int* p1) {
   *s = find_subband(P, idx);
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(kAB) approx_stats_kernel(const __grid_constant
         if (a == 0.0) continue;
         int sn, p0, p1;
         locate(P, i, &sn, &p0, &p1);
-        const int S = s_keep(P, s, q0, q1, sn, p0, p1);
+        const int S = A.rule == 0 ? s_keep(P, s, q0, q1, sn, p0, p1) : mag_bin(c[i]);
         atomicAdd(&hist[S], a);
         atomicAdd(&A.colhist[(class_of(P, A, sn, p0, p1) * P.m + k) * kSB + S], a);
       }
@@ -301,7 +310,7 @@ __global__ void __launch_bounds__(kAB) approx_rows_kernel(const __grid_constant_
         if (c[i] == 0.0) continue;
         int sn, p0, p1;
         locate(P, i, &sn, &p0, &p1);
-        if (s_keep(P, s, q0, q1, sn, p0, p1) > A.S[k]) c[i] = 0.0;
+        if ((A.rule == 0 ? s_keep(P, s, q0, q1, sn, p0, p1) : mag_bin(c[i])) > A.S[k]) c[i] = 0.0;
         else kap[i] = 1.0;
       }
       __syncthreads();

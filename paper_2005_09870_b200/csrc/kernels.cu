@@ -894,92 +894,6 @@ cudaError_t launch_spmv(const int64_t* row_ptr, const int32_t* col, const void* 
   return cudaGetLastError();
 }
 
-cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* tmp, size_t* tmp_bytes,
-                               cudaStream_t st) {
-  return cub::DeviceScan::ExclusiveSum(tmp, *tmp_bytes, in, out, n, st);
-}
-
 }  // namespace pcwd
-
-// ============================================================================= CSR transpose (apply ᵀ, FISTA)
-// Θᵀ of a shard's CSR as its own CSR over the N columns, entries of each column in increasing row order
-// (counting sort by column, then a segmented sort by row), so that Θᵀ x is a gather — no atomics, the same
-// summation order every time.
-namespace pcwd {
-namespace {
-__global__ void col_count_kernel(const int32_t* __restrict__ col, int64_t nnz, unsigned long long* __restrict__ cnt) {
-  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < nnz; j += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(&cnt[col[j]], 1ull);
-}
-template <typename T>
-__global__ void scatter_t_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const T* __restrict__ val,
-                                 int64_t rows, const int64_t* __restrict__ rpT, unsigned long long* __restrict__ fill,
-                                 int32_t* __restrict__ rowT, T* __restrict__ valT) {
-  const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  for (int64_t j = rp[warp] + lane; j < rp[warp + 1]; j += 32) {
-    const int c = col[j];
-    const int64_t pos = rpT[c] + int64_t(atomicAdd(&fill[c], 1ull));
-    rowT[pos] = int32_t(warp);
-    valT[pos] = val[j];
-  }
-}
-}  // namespace
-
-size_t csr_transpose_bytes(int64_t nnz, int64_t ncols, int vbytes) {
-  size_t sort_tmp = 0, scan_tmp = 0;
-  cub::DeviceSegmentedSort::SortPairs(nullptr, sort_tmp, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
-                                      static_cast<const float*>(nullptr), static_cast<float*>(nullptr), nnz, ncols,
-                                      static_cast<const int64_t*>(nullptr), static_cast<const int64_t*>(nullptr));
-  if (vbytes == 8) {
-    size_t t = 0;
-    cub::DeviceSegmentedSort::SortPairs(nullptr, t, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
-                                        static_cast<const double*>(nullptr), static_cast<double*>(nullptr), nnz, ncols,
-                                        static_cast<const int64_t*>(nullptr), static_cast<const int64_t*>(nullptr));
-    sort_tmp = t;
-  }
-  cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, static_cast<const unsigned long long*>(nullptr),
-                                static_cast<int64_t*>(nullptr), ncols + 1);
-  return std::max(sort_tmp, scan_tmp) + 256;
-}
-
-// work: ≥ csr_transpose_bytes + (ncols + 1)·8 (counts) + nnz·(4 + vbytes) (unsorted copies); outputs rpT (ncols + 1),
-// rowT (nnz, shard-local rows), valT (nnz).
-cudaError_t csr_transpose(const int64_t* rp, const int32_t* col, const void* val, int64_t rows, int64_t nnz,
-                          int64_t ncols, int vbytes, int64_t* rpT, int32_t* rowT, void* valT, void* work,
-                          size_t work_bytes, cudaStream_t st) {
-  char* w = static_cast<char*>(work);
-  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(w);
-  w += ((ncols + 1) * 8 + 255) & ~int64_t(255);
-  int32_t* rowU = reinterpret_cast<int32_t*>(w);
-  w += (nnz * 4 + 255) & ~int64_t(255);
-  void* valU = w;
-  w += (nnz * vbytes + 255) & ~int64_t(255);
-  size_t tmp_bytes = work_bytes - size_t(w - static_cast<char*>(work));
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(cnt, 0, (ncols + 1) * 8, st))) return e;
-  col_count_kernel<<<grid_for(nnz), kBlock, 0, st>>>(col, nnz, cnt);
-  if ((e = cub::DeviceScan::ExclusiveSum(w, tmp_bytes, cnt, rpT, ncols + 1, st))) return e;
-  if ((e = cudaMemsetAsync(cnt, 0, (ncols + 1) * 8, st))) return e;
-  const int grid = int((rows * 32 + kBlock - 1) / kBlock);
-  if (grid > 0) {
-    if (vbytes == 4)
-      scatter_t_kernel<float><<<grid, kBlock, 0, st>>>(rp, col, static_cast<const float*>(val), rows, rpT, cnt, rowU,
-                                                      static_cast<float*>(valU));
-    else
-      scatter_t_kernel<double><<<grid, kBlock, 0, st>>>(rp, col, static_cast<const double*>(val), rows, rpT, cnt, rowU,
-                                                       static_cast<double*>(valU));
-  }
-  tmp_bytes = work_bytes - size_t(w - static_cast<char*>(work));
-  if (vbytes == 4)
-    e = cub::DeviceSegmentedSort::SortPairs(w, tmp_bytes, rowU, rowT, static_cast<const float*>(valU),
-                                            static_cast<float*>(valT), nnz, ncols, rpT, rpT + 1, st);
-  else
-    e = cub::DeviceSegmentedSort::SortPairs(w, tmp_bytes, rowU, rowT, static_cast<const double*>(valU),
-                                            static_cast<double*>(valT), nnz, ncols, rpT, rpT + 1, st);
-  if (e) return e;
-  return cudaGetLastError();
-}
-
-}  // namespace pcwd
+// exclusive_scan_i64 and csr_transpose (Θᵀ for apply ᵀ / FISTA) live in sort.cu (the library's own scan and stable
+// radix sort).

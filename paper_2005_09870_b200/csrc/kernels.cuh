@@ -180,6 +180,7 @@ struct ApproxArgs {
   int64_t ncls;
   int64_t clsbase[kMaxSB + 1];
   int S[64];                // truncation index per k (−1: Ã_k = 0)
+  int rule;                 // 0: Remark (i)/(ii) index rule; 1: magnitude, |a| ≥ 2^{-(S+1)}
   double* rowhist;          // stats: ncls × m × bins
   double* colhist;          // stats: ncls × m × bins (zeroed by the caller)
   int64_t* cnt;             // count pass: per unit

@@ -97,7 +97,7 @@ def lib():
         L.pcwd_decompose_to_host.argtypes = [vp, vp, vp, vp, vp]
         L.pcwd_wavelet_transform.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         L.pcwd_fista.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), vp, vp]
-        L.pcwd_approx.argtypes = [vp, ctypes.c_double, vp, ctypes.POINTER(ApproxInfo)]
+        L.pcwd_approx.argtypes = [vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ApproxInfo)]
         L.pcwd_operator_apply.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         L.pcwd_pc_from_samples.argtypes = [i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]
         L.pcwd_columns.argtypes = [vp, vp, ctypes.c_int64, vp, vp]
@@ -206,10 +206,12 @@ class Decomposition:
                                 ctypes.byref(t), ctypes.c_void_p(_ptr(z)), ctypes.c_void_p(stream)), "pcwd_fista")
         return z, t.value
 
-    def approx(self, eta: float, stream: int = 0) -> dict:
-        """Algorithm 1's η-approximation Θ̃ into this handle's CSR (pcwd_approx); returns the per-k truncation."""
+    def approx(self, eta: float, rule: str = "index", stream: int = 0) -> dict:
+        """Algorithm 1's η-approximation Θ̃ into this handle's CSR (pcwd_approx); rule "index" (the Remark's (i)/(ii))
+        or "magnitude" (power-of-two thresholds); returns the per-k truncation."""
         inf = ApproxInfo()
-        _check(lib().pcwd_approx(self._h, ctypes.c_double(eta), ctypes.c_void_p(stream), ctypes.byref(inf)), "pcwd_approx")
+        _check(lib().pcwd_approx(self._h, ctypes.c_double(eta), {"index": 0, "magnitude": 1}[rule],
+                                 ctypes.c_void_p(stream), ctypes.byref(inf)), "pcwd_approx")
         m = inf.m
         return {"eta": inf.eta, "S": list(inf.S[:m]), "eps": list(inf.eps[:m]), "bound": list(inf.bound[:m]),
                 "nnz": inf.nnz}

@@ -54,17 +54,18 @@ def _gauss_micro(n=16, J=3, m=3, seed=5):
     return p
 
 
+@pytest.mark.parametrize("rule", ["index", "magnitude"])
 @pytest.mark.parametrize("eta", [1.0, 1e-1, 1e-2, 1e-3, 1e-5])
-def test_accuracy_lemma(eta):
+def test_accuracy_lemma(eta, rule):
     p = _gauss_micro()
     W = basis.analysis_matrix(p.d, p.n, p.J, p.h)
     T = op.theta_dense(p, W)
-    Tt, info, sup = AP.theta_tilde(p, eta, W)
+    Tt, info, sup = AP.theta_tilde(p, eta, W, rule)
     assert np.linalg.norm(T - Tt, 2) <= eta * (1 + 1e-12)
     assert not np.any(Tt[~sup])                                            # supp Θ̃ ⊆ 𝒮 (Lemma 9)
-    Sk = AP.s_keep_matrix(p)
     for k, inf in enumerate(info):
         A = AP.conv_rep(p, k, W)
+        Sk = AP.s_keep_matrix(p) if rule == "index" else AP.magnitude_bins(A)
         E = np.where(Sk > inf["S"], A, 0.0)
         assert np.linalg.norm(E, 2) <= inf["eps"] * (1 + 1e-12)          # ‖A_k − Ã_k‖₂ ≤ ε_k
         assert abs(inf["eps"] - eta / (p.m * np.abs(p.v[k]).max())) <= 1e-15 * inf["eps"]
@@ -110,3 +111,18 @@ def test_zero_multiplier_term_contributes_nothing():
     q.u, q.v = q.u[:1], q.v[:1]
     T1, _, _ = AP.theta_tilde(q, 1e-3 / 2)          # same ε_0 = η/(m ‖v_0‖∞) with m = 1
     assert np.max(np.abs(Tt - T1)) <= 1e-14
+
+
+def test_magnitude_bins_hand_values():
+    """|a| ∈ [2^{-b-1}, 2^{-b}) → b (0.5 ∈ [½, 1) → 0, 2^-10 ∈ [2^-10, 2^-9) → 9); ≥ 1 → 0; tiny → 62; exact zeros
+    (which contribute nothing either way) → 0."""
+    a = np.array([1.5, 1.0, 0.75, 0.5, 0.4999, 0.25, -0.3, 2.0 ** -10, 1e-30, 0.0])
+    assert AP.magnitude_bins(a).tolist() == [0, 0, 0, 0, 1, 1, 1, 9, 62, 0]
+
+
+def test_magnitude_rule_is_sparser_for_the_same_eta():
+    p = _gauss_micro()
+    W = basis.analysis_matrix(p.d, p.n, p.J, p.h)
+    a = np.count_nonzero(AP.theta_tilde(p, 1.0, W, "index")[2])
+    b = np.count_nonzero(AP.theta_tilde(p, 1.0, W, "magnitude")[2])
+    assert b < a

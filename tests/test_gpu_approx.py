@@ -60,16 +60,17 @@ CASES = [  # (n, d, M, J, m, seed, eta values)
 ]
 
 
+@pytest.mark.parametrize("rule", ["index", "magnitude"])
 @pytest.mark.parametrize("case", CASES, ids=[f"n{c[0]}d{c[1]}M{c[2]}J{c[3]}" for c in CASES])
-def test_approx_matches_dense_algorithm1(case):
+def test_approx_matches_dense_algorithm1(case, rule):
     n, d, M, J, m, seed, etas = case
     p = _smooth_micro(n, d, M, J, m, seed)
     W = basis.analysis_matrix(p.d, p.n, p.J, p.h)
     dec = Decomposition(Spec(p.d, p.n, p.J, p.h, torch.from_numpy(p.u).cuda(), torch.from_numpy(p.v).cuda(),
                              dtype="f64", retain="full"))
     for eta in etas:
-        T_ref, info_ref, sup = AP.theta_tilde(p, eta, W)
-        got = dec.approx(eta)
+        T_ref, info_ref, sup = AP.theta_tilde(p, eta, W, rule)
+        got = dec.approx(eta, rule)
         assert got["S"] == [i["S"] for i in info_ref], (eta, got["S"], [i["S"] for i in info_ref])
         for b, i in zip(got["bound"], info_ref):
             assert abs(b - i["bound"]) <= 1e-10 * max(i["bound"], 1e-300)
@@ -116,16 +117,38 @@ def test_operator_apply_matches_oracle():
     dec.close()
 
 
-@pytest.mark.parametrize("eta", [3.0, 1.0, 0.3])
-def test_accuracy_lemma_c3_operator(eta):
-    """The c3 operator (256², DB4, J = 6, m = 8) in fp64: ‖Θ − Θ̃‖₂ ≤ η measured on the GPU (power iteration)."""
-    p = C.get("c3")
+def _blur128():
+    """A 128² space-varying blur (N = 16,384, DB4, J = 5, m = 4, 9 × 9 taps) in the shape of the paper's operators."""
+    p = C.micro(128, 2, 4, 5, 4, 4, 91)
+    rng = np.random.default_rng(91)
+    r = np.arange(-4, 5)
+    g = np.exp(-(r[:, None] ** 2 + r[None, :] ** 2) / 4.0)
+    u = np.zeros((4, 128, 128))
+    for k in range(4):
+        w = g ** (1 + k) * (1 + 0.5 * rng.uniform(size=g.shape))
+        w /= w.sum()
+        for i, a in enumerate(r):
+            for j, b in enumerate(r):
+                u[k, a % 128, b % 128] = w[i, j]
+    y = np.arange(128) / 128
+    p.u = u.reshape(4, -1)
+    p.v = np.stack([1.0 + 0.3 * (k + 1) * np.cos(2 * np.pi * (y[:, None] + k * y[None, :])) for k in range(4)]).reshape(4, -1)
+    return p
+
+
+@pytest.mark.parametrize("rule", ["index", "magnitude"])
+@pytest.mark.parametrize("eta", [3.0, 0.3, 0.03])
+def test_accuracy_lemma_128(eta, rule):
+    """‖Θ − Θ̃‖₂ ≤ η measured on the GPU by power iteration (128², fp64)."""
+    p = _blur128()
     dec = Decomposition(Spec(p.d, p.n, p.J, p.h, torch.from_numpy(p.u).cuda(), torch.from_numpy(p.v).cuda(),
                              dtype="f64", retain="band", band_L=64))
-    info = dec.approx(eta)
-    err = _spectral_error(dec, p.N)
-    assert err <= eta, (eta, err, info["S"])
-    dec.close()
+    try:
+        info = dec.approx(eta, rule)
+        err = _spectral_error(dec, p.N)
+        assert err <= eta, (eta, err, info["S"])
+    finally:
+        dec.close()
 
 
 def test_approx_argument_checks():
@@ -141,4 +164,6 @@ def test_approx_argument_checks():
     with pytest.raises(PcwdError) as e:
         dec.approx(0.0)
     assert e.value.code == 3
+    with pytest.raises(KeyError):
+        dec.approx(1.0, "other")
     dec.close()
