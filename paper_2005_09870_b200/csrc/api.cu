@@ -435,6 +435,8 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     A.tau = tau;
     A.use_smem = L.smem > 0;
     A.cand = h->cand;
+    static const int unit_dbg = getenv("PCWD_UNIT_DBG") ? atoi(getenv("PCWD_UNIT_DBG")) : 0;
+    A.dbg = unit_dbg;
     CK(launch_units(P, A, mode, h->hp.real_bytes, h->hp.out_bytes, L.grid, L.smem, ls));
     h->nlaunch++;
     if (mode == MODE_BAND || mode == MODE_FULL)

@@ -220,8 +220,109 @@ __device__ __forceinline__ int qdiv(int a, int b, float inv_b) {
   return a < (1 << 20) ? __float2int_rz((float(a) + 0.5f) * inv_b) : a / b;
 }
 
+// ---- register-blocked cascade passes of the generic kernel (2-D, windows that do not wrap or cover the line) ----
+// A task computes 8 consecutive outputs of one filter from one run of 14 + 2δ inputs held in registers (the
+// outputs at 2j + t share all but two inputs): 14 + 2δ loads and one bounds test each for 8·2δ FMAs, instead of
+// 2δ loads, tests and index computations per output.  TL2 = 2δ is a compile-time constant (taps from the
+// kernel-parameter bank by compile-time index).  mode 0: window clear of wrapping (signed offset, zero outside);
+// mode 1: whole periodic line (index mod the line).
+constexpr int kNQ = 4;   // outputs per task (4: the kernel keeps ≤ 80 registers, 3 CTAs per SM)
+
+template <typename Real, int TL2>
+__device__ __forceinline__ void run_load(const Real* __restrict__ base, int64_t stride, int q0, const Range& in, int mode,
+                                         Real x[2 * kNQ - 2 + TL2]) {
+  if (mode == 0) {
+    int dq = (q0 - in.lo) & (in.nl - 1);
+    if (dq >= in.nl - 2 * TL2) dq -= in.nl;
+#pragma unroll
+    for (int i = 0; i < 2 * kNQ - 2 + TL2; ++i)
+      x[i] = unsigned(dq + i) < unsigned(in.len) ? base[int64_t(dq + i) * stride] : Real(0);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 2 * kNQ - 2 + TL2; ++i) x[i] = base[int64_t((q0 + i - in.lo) & (in.nl - 1)) * stride];
+  }
+}
+
+template <typename Real, int TL2>
+__device__ void pass_a_blk(const Plan& P, const Real* __restrict__ cur, Real* __restrict__ Y, const Range& in0,
+                           const Range& in1, const Range& a1, const Range& d1, int mode) {
+  const int ycols = a1.len + d1.len;
+  const int ga = (a1.len + kNQ - 1) / kNQ, gd = (d1.len + kNQ - 1) / kNQ;
+  const int tot = in0.len * (ga + gd);
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    const int g = idx / in0.len, i0 = idx - g * in0.len;   // consecutive threads: consecutive rows
+    const int e1 = g >= ga;
+    const int j0 = kNQ * (e1 ? g - ga : g);
+    const Range& R = e1 ? d1 : a1;
+    Real x[2 * kNQ - 2 + TL2];
+    run_load<Real, TL2>(cur + int64_t(i0) * in1.len, 1, 2 * (R.lo + j0) + P.to[e1], in1, mode, x);
+    Real* out = Y + int64_t(i0) * ycols + (e1 ? a1.len : 0);
+#pragma unroll
+    for (int q = 0; q < kNQ; ++q) {
+      Real acc = Real(0);
+#pragma unroll
+      for (int t = 0; t < TL2; ++t) acc = fmaT(TapsOf<Real>::get(P, e1, t), x[2 * q + t], acc);
+      if (j0 + q < R.len) out[j0 + q] = acc;
+    }
+  }
+}
+
+template <typename Real, int TL2>
+__device__ void pass_b_blk(const Plan& P, const Real* __restrict__ Y, Real* __restrict__ nxt, Real* __restrict__ Dd,
+                           const Range& in0, const Range& a0, const Range& d0, const Range& a1, const Range& d1,
+                           int mode) {
+  const int ycols = a1.len + d1.len;
+  const int s01 = a0.len * d1.len, s10 = d0.len * a1.len;
+  const int ga = (a0.len + kNQ - 1) / kNQ, gd = (d0.len + kNQ - 1) / kNQ;
+  const int tot = ycols * (ga + gd);
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
+    const int g = idx / ycols, colY = idx - g * ycols;     // consecutive threads: consecutive columns
+    const int e0 = g >= ga;
+    const int j0 = kNQ * (e0 ? g - ga : g);
+    const Range& R = e0 ? d0 : a0;
+    Real x[2 * kNQ - 2 + TL2];
+    run_load<Real, TL2>(Y + colY, ycols, 2 * (R.lo + j0) + P.to[e0], in0, mode, x);
+    const int e1 = colY >= a1.len;
+    const int j1 = e1 ? colY - a1.len : colY;
+    const int w1 = e1 ? d1.len : a1.len;
+    Real* out = e0 == 0 ? (e1 ? Dd : nxt) : (e1 ? Dd + s01 + s10 : Dd + s01);
+#pragma unroll
+    for (int q = 0; q < kNQ; ++q) {
+      Real acc = Real(0);
+#pragma unroll
+      for (int t = 0; t < TL2; ++t) acc = fmaT(TapsOf<Real>::get(P, e0, t), x[2 * q + t], acc);
+      if (j0 + q < R.len) out[(j0 + q) * w1 + j1] = acc;
+    }
+  }
+}
+
+// dispatch on 2δ (the Daubechies / Symmlet lengths of the configurations); false: use the per-output loops
+template <typename Real>
+__device__ __forceinline__ bool pass_a_dispatch(const Plan& P, const Real* cur, Real* Y, const Range& in0, const Range& in1,
+                                                const Range& a1, const Range& d1, int mode) {
+  switch (P.L2) {
+    case 2: pass_a_blk<Real, 2>(P, cur, Y, in0, in1, a1, d1, mode); return true;
+    case 4: pass_a_blk<Real, 4>(P, cur, Y, in0, in1, a1, d1, mode); return true;
+    case 8: pass_a_blk<Real, 8>(P, cur, Y, in0, in1, a1, d1, mode); return true;
+    case 12: pass_a_blk<Real, 12>(P, cur, Y, in0, in1, a1, d1, mode); return true;
+  }
+  return false;
+}
+template <typename Real>
+__device__ __forceinline__ bool pass_b_dispatch(const Plan& P, const Real* Y, Real* nxt, Real* Dd, const Range& in0,
+                                                const Range& a0, const Range& d0, const Range& a1, const Range& d1,
+                                                int mode) {
+  switch (P.L2) {
+    case 2: pass_b_blk<Real, 2>(P, Y, nxt, Dd, in0, a0, d0, a1, d1, mode); return true;
+    case 4: pass_b_blk<Real, 4>(P, Y, nxt, Dd, in0, a0, d0, a1, d1, mode); return true;
+    case 8: pass_b_blk<Real, 8>(P, Y, nxt, Dd, in0, a0, d0, a1, d1, mode); return true;
+    case 12: pass_b_blk<Real, 12>(P, Y, nxt, Dd, in0, a0, d0, a1, d1, mode); return true;
+  }
+  return false;
+}
+
 template <typename Real, typename OutT, int D, int MODE>
-__global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Plan P,
+__global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__ Plan P,
                                                       const __grid_constant__ UnitArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red_d[kBlock / 32];
@@ -267,7 +368,8 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
         const int64_t vy = int64_t(y0) * n + y1;
         const int64_t ti = int64_t(t0) * tw1 + t1;
         Real acc = Real(0);
-        for (int k = 0; k < P.m; ++k) acc = fmaT(v[k * P.N + vy], T[k * S.tstride + ti], acc);
+        if (!(A.dbg & 1))
+          for (int k = 0; k < P.m; ++k) acc = fmaT(v[k * P.N + vy], T[k * S.tstride + ti], acc);
         X0[idx] = acc;
       }
     }
@@ -309,7 +411,8 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
         const int totA = in0.len * ycols;
         const float inv_y = 1.0f / float(ycols), inv_a1 = 1.0f / float(a1.len), inv_d1 = 1.0f / float(d1.len);
         const int k1 = kind(in1);
-        for (int idx = tid; idx < totA; idx += kBlock) {       // pass A: axis 1
+        const bool blkA = k1 <= 1 && pass_a_dispatch<Real>(P, cur, Y, in0, in1, a1, d1, k1);
+        for (int idx = blkA ? totA : tid; idx < totA; idx += kBlock) {       // pass A: axis 1
           const int i0 = qdiv(idx, ycols, inv_y), j = idx - i0 * ycols;
           const int e1 = j >= a1.len;
           const int jj = e1 ? j - a1.len : j;
@@ -342,7 +445,8 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
         s10 = d0.len * a1.len;
         const int s11 = d0.len * d1.len;
         const int totB = s00 + s01 + s10 + s11;
-        for (int idx = tid; idx < totB; idx += kBlock) {       // pass B: axis 0
+        const bool blkB = k0 <= 1 && pass_b_dispatch<Real>(P, Y, nxt, Dd, in0, a0, d0, a1, d1, k0);
+        for (int idx = blkB ? totB : tid; idx < totB; idx += kBlock) {       // pass B: axis 0
           int e0, e1, j0, j1, rem;
           Real* dst;
           if (idx < s00) { e0 = 0; e1 = 0; rem = idx; j0 = qdiv(rem, a1.len, inv_a1); j1 = rem - j0 * a1.len; dst = nxt + rem; }
@@ -470,7 +574,7 @@ __global__ void __launch_bounds__(kBlock) unit_kernel(const __grid_constant__ Pl
             const int ks0 = qdiv(k, W.r1.len, inv_w), ks1 = k - ks0 * W.r1.len;
             const double x = double(W.buf[sorted_to_local(W.r0, ks0) * W.r1.len + sorted_to_local(W.r1, ks1)]);
             tmax = fmax(tmax, fabs(x));
-            cbase[crun + k] = x;
+            if (!(A.dbg & 2)) cbase[crun + k] = x;
           }
           crun += tot;
         }
@@ -802,6 +906,12 @@ static cudaError_t launch_one(const Plan& P, const UnitArgs& A, int grid, size_t
       opted = int(smem);
     }
   }
+  // the kernel strides over units: a grid larger than the CTAs that can be resident at once only adds a partial
+  // second wave (each CTA has the same share of units), so clamp it to one full wave
+  int per_sm = 0, dev = 0, nsm = 148;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem) == cudaSuccess && per_sm > 0 &&
+      cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+    grid = std::min(grid, per_sm * nsm);
   kern<<<grid, kBlock, smem, st>>>(P, A);
   return cudaGetLastError();
 }

@@ -24,6 +24,7 @@ struct UnitArgs {
   double tau;               // threshold (fp64)
   int use_smem;
   double* cand;             // TSTORE: every structural partner value of the unit, window by window in column order
+  int dbg;                  // timing experiments only (PCWD_UNIT_DBG, results invalid): 1 = no k-sum, 2 = no candidate stores
 };
 
 struct TileArgs {
