@@ -303,7 +303,9 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     const int li = (sk || (conc && overlap)) ? nL - 1 - it : it;
     const Launch& L = h->launches[li];
     ls = st;
-    static const bool overlap_all = getenv("PCWD_OVERLAP_ALL") != nullptr;   // level 1 beside the coarse streams too
+    // level 1 beside the coarse streams too (default: the shorter step, c5 r01 15.36 vs 15.74 ms); PCWD_OVERLAP_ALL=0
+    // runs the first (largest) level alone
+    static const bool overlap_all = !(getenv("PCWD_OVERLAP_ALL") && atoi(getenv("PCWD_OVERLAP_ALL")) == 0);
     if (conc && overlap && it == (overlap_all ? 0 : 1))
       if (int rc = fork()) return rc;   // after the first launch: coarse streams wait for it only
     if (conc_t) {   // threshold rule's cascade pass: every level on its own stream (own scratch slices)

@@ -35,7 +35,7 @@ SWITCHES = [
     {"PCWD_NO_TAIL": "1"},
     {"PCWD_COARSE_SERIAL": "1"},
     {"PCWD_COARSE_OVERLAP": "0"},
-    {"PCWD_OVERLAP_ALL": "1"},
+    {"PCWD_OVERLAP_ALL": "0"},
     {"PCWD_GENERIC_SMEM_KB": "200"},
     {"PCWD_NO_FINE": "1"},
     {"PCWD_NO_DIRECT": "1"},
