@@ -220,6 +220,8 @@ def run_ours(args):
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")            # communicator set-up lines on stderr (evidence)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
@@ -291,6 +293,7 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     serial = dec.launch_profile()
     PW._check(PW.lib().pcwd_profile(dec._h, 1), "pcwd_profile")
+    alone_ms = next((m for (m, f, k, lv) in serial if (k, lv) == (dom[2], dom[3])), None)   # the dominant kernel alone
     ms_units = phase[1] / args.steps
     ms_tmpl = phase[0] / args.steps
     peaks = _peaks()
@@ -306,6 +309,8 @@ def run_ours(args):
                 if traffic_src else None,
                 "kernel": f"{dom[2]} unit kernel, level {dom[3]} (a2 k-sum + a3 cascade + a4 gather)",
                 "kernel_ms": dom[0], "kernel_share_of_step": dom[0] / ms_per_step,
+                "kernel_ms_alone": alone_ms, "frac_alone": (2.0 * dom[1] / (alone_ms * 1e-3) / 1e12 / fp32_peak
+                                                            if alone_ms else None),
                 "fma_per_launch": dom[1],
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz of MEASURED_PEAKS.json"
                 + (" / 2 (FP64)" if args.dtype == "f64" else ""),

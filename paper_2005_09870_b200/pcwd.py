@@ -248,6 +248,11 @@ class Decomposition:
         if self.spec.retain == "threshold" and self.spec.world > 1:
             self.set_global_max(allreduce_max(self.local_max(stream), self.spec.device))
         self.decompose(stream)
+        if self.spec.world > 1:   # C-b: where this shard's entries start in the global CSR
+            self.row_offsets = global_row_offsets(self.info().nnz, self.spec.device)
+        else:
+            self.row_offsets = [0, self.info().nnz]
+        return self.row_offsets
 
     # -- results ------------------------------------------------------------------------
     def info(self) -> Info:
