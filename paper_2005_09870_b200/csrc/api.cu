@@ -638,7 +638,7 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       per_sm = std::max(per_sm, 1);
       L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * per_sm));
     } else {   // its own slice of the global scratch (launches may run concurrently)
-      L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * 4));
+      L.grid = int(std::min<int64_t>(u1 - u0, int64_t(nsm) * 8));   // 128-thread CTAs, up to 6-8 per SM
       L.gs_stride = (scr + 31) & ~int64_t(31);
       L.gs_off = gmax;
       gmax += L.gs_stride * L.grid;

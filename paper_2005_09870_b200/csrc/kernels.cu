@@ -24,6 +24,7 @@
 namespace pcwd {
 
 constexpr int kBlock = 256;
+constexpr int kUB = 128;   // threads per CTA of the generic unit kernel (one unit per CTA; more CTAs per SM hide its barrier chain)
 
 __device__ __forceinline__ float fmaT(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fmaT(double a, double b, double c) { return fma(a, b, c); }
@@ -170,6 +171,7 @@ struct OutWin {
   int sbi;
 };
 
+template <int NT = kUB>   // NT: threads of the calling CTA (the unit kernel's kUB, or kBlock)
 __device__ __forceinline__ double block_reduce_max(double x, double* red) {
   for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -177,7 +179,7 @@ __device__ __forceinline__ double block_reduce_max(double x, double* red) {
   if (l == 0) red[w] = x;
   __syncthreads();
   if (threadIdx.x < 32) {
-    double y = threadIdx.x < kBlock / 32 ? red[threadIdx.x] : 0.0;
+    double y = threadIdx.x < NT / 32 ? red[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) y = fmax(y, __shfl_xor_sync(0xffffffffu, y, o));
     if (threadIdx.x == 0) red[0] = y;
   }
@@ -185,6 +187,7 @@ __device__ __forceinline__ double block_reduce_max(double x, double* red) {
   return red[0];
 }
 
+template <int NT = kUB>
 __device__ __forceinline__ int block_reduce_sum(int x, int* red) {
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -192,7 +195,7 @@ __device__ __forceinline__ int block_reduce_sum(int x, int* red) {
   if (l == 0) red[w] = x;
   __syncthreads();
   if (threadIdx.x < 32) {
-    int y = threadIdx.x < kBlock / 32 ? red[threadIdx.x] : 0;
+    int y = threadIdx.x < NT / 32 ? red[threadIdx.x] : 0;
     for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
     if (threadIdx.x == 0) red[0] = y;
   }
@@ -200,6 +203,7 @@ __device__ __forceinline__ int block_reduce_sum(int x, int* red) {
   return red[0];
 }
 
+template <int NT = kUB>
 __device__ __forceinline__ int block_reduce_maxi(int x, int* red) {
   for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -207,7 +211,7 @@ __device__ __forceinline__ int block_reduce_maxi(int x, int* red) {
   if (l == 0) red[w] = x;
   __syncthreads();
   if (threadIdx.x < 32) {
-    int y = threadIdx.x < kBlock / 32 ? red[threadIdx.x] : 0;
+    int y = threadIdx.x < NT / 32 ? red[threadIdx.x] : 0;
     for (int o = 16; o > 0; o >>= 1) y = max(y, __shfl_xor_sync(0xffffffffu, y, o));
     if (threadIdx.x == 0) red[0] = y;
   }
@@ -321,13 +325,13 @@ __device__ __forceinline__ bool pass_b_dispatch(const Plan& P, const Real* Y, Re
   return false;
 }
 
-template <typename Real, typename OutT, int D, int MODE>
-__global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__ Plan P,
+template <typename Real, typename OutT, int D, int MODE, int NT>
+__global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) unit_kernel(const __grid_constant__ Plan P,
                                                       const __grid_constant__ UnitArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double red_d[kBlock / 32];
-  __shared__ int red_i[kBlock / 32];
-  using BlockScan = cub::BlockScan<int, kBlock>;
+  __shared__ double red_d[NT / 32];
+  __shared__ int red_i[NT / 32];
+  using BlockScan = cub::BlockScan<int, NT>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
 
   Real* scratch = A.use_smem ? reinterpret_cast<Real*>(smem_raw)
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
       const bool f1 = S.tW[1] >= n;
       const int tw1 = S.tRS;
       const int total = r0.len * r1.len;
-      for (int idx = tid; idx < total; idx += kBlock) {
+      for (int idx = tid; idx < total; idx += NT) {
         const int i0 = idx / r1.len, i1 = idx - i0 * r1.len;
         const int y0 = D == 2 ? ((r0.lo + i0) & mask) : 0;
         const int y1 = (r1.lo + i1) & mask;
@@ -374,14 +378,14 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
       }
     }
     if (MODE == MODE_BAND) {
-      for (int j = tid; j < P.band_Lpad; j += kBlock) { stage_col[j] = INT_MAX; stage_val[j] = Real(0); }
+      for (int j = tid; j < P.band_Lpad; j += NT) { stage_col[j] = INT_MAX; stage_val[j] = Real(0); }
     }
     // PATTERN: the cascade runs up to the coarsest level among the unit's listed partners
     int nsteps = S.steps;
     if (MODE == MODE_PATTERN) {
       int mx = 0;
-      for (int64_t j = A.row_ptr[row] + tid; j < A.row_ptr[row + 1]; j += kBlock) mx = max(mx, P.sb[find_subband(P, A.col[j])].level);
-      nsteps = block_reduce_maxi(mx, red_i);
+      for (int64_t j = A.row_ptr[row] + tid; j < A.row_ptr[row + 1]; j += NT) mx = max(mx, P.sb[find_subband(P, A.col[j])].level);
+      nsteps = block_reduce_maxi<NT>(mx, red_i);
     }
     __syncthreads();
 
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
         const float inv_y = 1.0f / float(ycols), inv_a1 = 1.0f / float(a1.len), inv_d1 = 1.0f / float(d1.len);
         const int k1 = kind(in1);
         const bool blkA = k1 <= 1 && pass_a_dispatch<Real>(P, cur, Y, in0, in1, a1, d1, k1);
-        for (int idx = blkA ? totA : tid; idx < totA; idx += kBlock) {       // pass A: axis 1
+        for (int idx = blkA ? totA : tid; idx < totA; idx += NT) {       // pass A: axis 1
           const int i0 = qdiv(idx, ycols, inv_y), j = idx - i0 * ycols;
           const int e1 = j >= a1.len;
           const int jj = e1 ? j - a1.len : j;
@@ -446,7 +450,7 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
         const int s11 = d0.len * d1.len;
         const int totB = s00 + s01 + s10 + s11;
         const bool blkB = k0 <= 1 && pass_b_dispatch<Real>(P, Y, nxt, Dd, in0, a0, d0, a1, d1, k0);
-        for (int idx = blkB ? totB : tid; idx < totB; idx += kBlock) {       // pass B: axis 0
+        for (int idx = blkB ? totB : tid; idx < totB; idx += NT) {       // pass B: axis 0
           int e0, e1, j0, j1, rem;
           Real* dst;
           if (idx < s00) { e0 = 0; e1 = 0; rem = idx; j0 = qdiv(rem, a1.len, inv_a1); j1 = rem - j0 * a1.len; dst = nxt + rem; }
@@ -477,7 +481,7 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
         }
       } else {
         const int tot = a1.len + d1.len;
-        for (int idx = tid; idx < tot; idx += kBlock) {
+        for (int idx = tid; idx < tot; idx += NT) {
           const int e1 = idx >= a1.len;
           const int jj = e1 ? idx - a1.len : idx;
           const Range& R = e1 ? d1 : a1;
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
           const OutWin<Real>& W = w[wi];
           const SubBand& L = P.sb[W.sbi];
           const int tot = W.r0.len * W.r1.len;
-          for (int idx = tid; idx < tot; idx += kBlock) {
+          for (int idx = tid; idx < tot; idx += NT) {
             const int i0 = idx / W.r1.len, i1 = idx - i0 * W.r1.len;
             const int g0 = (W.r0.lo + i0) & (W.r0.nl - 1);
             const int g1 = (W.r1.lo + i1) & (W.r1.nl - 1);
@@ -520,7 +524,7 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
         }
       } else if (MODE == MODE_BAND) {
         const int4* st = A.stencil + S.stencil_off;
-        for (int j = tid; j < P.band_L; j += kBlock) {
+        for (int j = tid; j < P.band_L; j += NT) {
           const int4 e = st[j];
           const SubBand& L = P.sb[e.x];
           if (L.level != s || (e.x == 0 && s != P.J)) continue;
@@ -543,7 +547,7 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
         }
       } else if (MODE == MODE_PATTERN) {   // the caller's partners of this step's sub-bands (columns given)
         OutT* outv = reinterpret_cast<OutT*>(A.val);
-        for (int64_t j = A.row_ptr[row] + tid; j < A.row_ptr[row + 1]; j += kBlock) {
+        for (int64_t j = A.row_ptr[row] + tid; j < A.row_ptr[row + 1]; j += NT) {
           const int c = A.col[j];
           const int sb = find_subband(P, c);
           const SubBand& L = P.sb[sb];
@@ -563,14 +567,14 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
       } else if (MODE == MODE_TMAX) {
         for (int wi = 0; wi < nw; ++wi) {
           const int tot = w[wi].r0.len * w[wi].r1.len;
-          for (int idx = tid; idx < tot; idx += kBlock) tmax = fmax(tmax, fabs(double(w[wi].buf[idx])));
+          for (int idx = tid; idx < tot; idx += NT) tmax = fmax(tmax, fabs(double(w[wi].buf[idx])));
         }
       } else if (MODE == MODE_TSTORE) {   // TMAX + every value stored in column (sorted) order
         for (int wi = 0; wi < nw; ++wi) {
           const OutWin<Real>& W = w[wi];
           const int tot = W.r0.len * W.r1.len;
           const float inv_w = 1.0f / float(W.r1.len);
-          for (int k = tid; k < tot; k += kBlock) {
+          for (int k = tid; k < tot; k += NT) {
             const int ks0 = qdiv(k, W.r1.len, inv_w), ks1 = k - ks0 * W.r1.len;
             const double x = double(W.buf[sorted_to_local(W.r0, ks0) * W.r1.len + sorted_to_local(W.r1, ks1)]);
             tmax = fmax(tmax, fabs(x));
@@ -582,8 +586,8 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
         for (int wi = 0; wi < nw; ++wi) {
           int c = 0;
           const int tot = w[wi].r0.len * w[wi].r1.len;
-          for (int idx = tid; idx < tot; idx += kBlock) c += fabs(double(w[wi].buf[idx])) >= A.tau;
-          c = block_reduce_sum(c, red_i);
+          for (int idx = tid; idx < tot; idx += NT) c += fabs(double(w[wi].buf[idx])) >= A.tau;
+          c = block_reduce_sum<NT>(c, red_i);
           if (tid == 0) A.cnt[row * P.nsb + w[wi].sbi] = c;
         }
       } else if (MODE == MODE_TWRITE) {
@@ -595,7 +599,7 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
           for (int q = 0; q < W.sbi; ++q) base += A.cnt[row * P.nsb + q];
           const int tot = W.r0.len * W.r1.len;
           int running = 0;
-          for (int k0 = 0; k0 < tot; k0 += kBlock) {
+          for (int k0 = 0; k0 < tot; k0 += NT) {
             const int k = k0 + tid;
             int keep = 0, colv = 0;
             Real x = Real(0);
@@ -630,7 +634,7 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
       const int Lp = P.band_Lpad;
       for (int k = 2; k <= Lp; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int i = tid; i < Lp; i += kBlock) {
+          for (int i = tid; i < Lp; i += NT) {
             const int ixj = i ^ j;
             if (ixj > i) {
               const bool up = (i & k) == 0;
@@ -646,12 +650,12 @@ __global__ void __launch_bounds__(kBlock, 3) unit_kernel(const __grid_constant__
       }
       OutT* outv = reinterpret_cast<OutT*>(A.val);
       const int64_t base = row * P.band_L;
-      for (int j = tid; j < P.band_L; j += kBlock) {
+      for (int j = tid; j < P.band_L; j += NT) {
         A.col[base + j] = stage_col[j];
         outv[base + j] = OutT(stage_val[j]);
       }
     } else if (MODE == MODE_TMAX || MODE == MODE_TSTORE) {
-      const double mx = block_reduce_max(tmax, red_d);
+      const double mx = block_reduce_max<NT>(tmax, red_d);
       if (tid == 0) A.unitmax[row] = mx;
     }
     __syncthreads();
@@ -768,7 +772,7 @@ __global__ void max_reduce_kernel(const double* x, int64_t n, unsigned long long
   double m = 0.0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     m = fmax(m, x[i]);
-  m = block_reduce_max(m, red);
+  m = block_reduce_max<kBlock>(m, red);
   if (threadIdx.x == 0) atomicMax(out, __double_as_longlong(m));   // m ≥ 0: bit order = value order
 }
 
@@ -883,9 +887,9 @@ cudaError_t launch_cast(const double* src, void* dst, int64_t count, int real_by
   return cudaGetLastError();
 }
 
-template <typename Real, typename OutT, int D, int MODE>
+template <typename Real, typename OutT, int D, int MODE, int NT>
 static cudaError_t launch_one(const Plan& P, const UnitArgs& A, int grid, size_t smem, cudaStream_t st) {
-  auto kern = unit_kernel<Real, OutT, D, MODE>;
+  auto kern = unit_kernel<Real, OutT, D, MODE, NT>;
   // the kernel has static shared memory too (reductions, scan storage): opt in whenever static + dynamic
   // exceeds 48 KB; the attribute only ever grows (per instantiation, process-wide), under a lock so that
   // handles used from several threads never launch between another thread's check and its set
@@ -909,17 +913,23 @@ static cudaError_t launch_one(const Plan& P, const UnitArgs& A, int grid, size_t
   // the kernel strides over units: a grid larger than the CTAs that can be resident at once only adds a partial
   // second wave (each CTA has the same share of units), so clamp it to one full wave
   int per_sm = 0, dev = 0, nsm = 148;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem) == cudaSuccess && per_sm > 0 &&
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) == cudaSuccess && per_sm > 0 &&
       cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
     grid = std::min(grid, per_sm * nsm);
-  kern<<<grid, kBlock, smem, st>>>(P, A);
+  kern<<<grid, NT, smem, st>>>(P, A);
   return cudaGetLastError();
 }
 
+// 128 threads per unit when the launch has many units (more units in flight per SM), 256 when it has few (the
+// coarse levels: big windows, too few units to fill the GPU one per 128-thread CTA)
 template <typename Real, typename OutT, int MODE>
 static cudaError_t launch_d(const Plan& P, const UnitArgs& A, int grid, size_t smem, cudaStream_t st) {
-  return P.d == 2 ? launch_one<Real, OutT, 2, MODE>(P, A, grid, smem, st)
-                  : launch_one<Real, OutT, 1, MODE>(P, A, grid, smem, st);
+  const bool few = A.u1 - A.u0 < 148 * 6;
+  if (few)
+    return P.d == 2 ? launch_one<Real, OutT, 2, MODE, 256>(P, A, grid, smem, st)
+                    : launch_one<Real, OutT, 1, MODE, 256>(P, A, grid, smem, st);
+  return P.d == 2 ? launch_one<Real, OutT, 2, MODE, 128>(P, A, grid, smem, st)
+                  : launch_one<Real, OutT, 1, MODE, 128>(P, A, grid, smem, st);
 }
 
 cudaError_t launch_units(const Plan& P, const UnitArgs& A, int mode, int real_bytes, int out_bytes, int grid,
