@@ -711,27 +711,26 @@ __global__ void __launch_bounds__(kBlock) cand_filter_kernel(const __grid_consta
           c = __reduce_add_sync(0xffffffffu, c);
           if (lane == 0) cnt[row * P.nsb + wsb[wi]] = c;
         } else {
+          // the count pass gave this window's kept entries: skip windows with none, stop once all are written,
+          // and compute the column index only for the kept lanes
+          const int want = cnt[row * P.nsb + wsb[wi]];
           const SubBand& L = P.sb[wsb[wi]];
           int64_t b = base;
-          for (int q = 0; q < wsb[wi]; ++q) b += cnt[row * P.nsb + q];
+          if (want > 0)
+            for (int q = 0; q < wsb[wi]; ++q) b += cnt[row * P.nsb + q];
           int running = 0;
-          for (int k0 = 0; k0 < tot; k0 += 32) {
+          for (int k0 = 0; k0 < tot && running < want; k0 += 32) {
             const int k = k0 + lane;
-            int keep = 0, colv = 0;
-            double x = 0.0;
-            if (k < tot) {
-              x = cw[k];
-              keep = fabs(x) >= tau;
+            const double x = k < tot ? cw[k] : 0.0;
+            const int keep = k < tot && fabs(x) >= tau;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
               const int ks0 = k / wr1[wi].len, ks1 = k - ks0 * wr1[wi].len;
               const int i0 = sorted_to_local(wr0[wi], ks0), i1 = sorted_to_local(wr1[wi], ks1);
               const int g0 = (wr0[wi].lo + i0) & (wr0[wi].nl - 1);
               const int g1 = (wr1[wi].lo + i1) & (wr1[wi].nl - 1);
-              colv = int(L.offset + int64_t(g0) * L.nl + g1);
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
               const int posn = __popc(m & lt);
-              col[b + running + posn] = colv;
+              col[b + running + posn] = int(L.offset + int64_t(g0) * L.nl + g1);
               val[b + running + posn] = OutT(x);
             }
             running += __popc(m);
