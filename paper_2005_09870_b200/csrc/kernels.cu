@@ -573,12 +573,21 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) unit_kernel(const __gri
         for (int wi = 0; wi < nw; ++wi) {
           const OutWin<Real>& W = w[wi];
           const int tot = W.r0.len * W.r1.len;
-          const float inv_w = 1.0f / float(W.r1.len);
-          for (int k = tid; k < tot; k += NT) {
-            const int ks0 = qdiv(k, W.r1.len, inv_w), ks1 = k - ks0 * W.r1.len;
-            const double x = double(W.buf[sorted_to_local(W.r0, ks0) * W.r1.len + sorted_to_local(W.r1, ks1)]);
-            tmax = fmax(tmax, fabs(x));
-            if (!(A.dbg & 2)) cbase[crun + k] = x;
+          auto ident = [](const Range& r) { return r.len >= r.nl || (r.lo & (r.nl - 1)) + r.len <= r.nl; };
+          if (ident(W.r0) && ident(W.r1)) {   // no wrap: the window's row-major order is the column order
+            for (int k = tid; k < tot; k += NT) {
+              const double x = double(W.buf[k]);
+              tmax = fmax(tmax, fabs(x));
+              if (!(A.dbg & 2)) cbase[crun + k] = x;
+            }
+          } else {
+            const float inv_w = 1.0f / float(W.r1.len);
+            for (int k = tid; k < tot; k += NT) {
+              const int ks0 = qdiv(k, W.r1.len, inv_w), ks1 = k - ks0 * W.r1.len;
+              const double x = double(W.buf[sorted_to_local(W.r0, ks0) * W.r1.len + sorted_to_local(W.r1, ks1)]);
+              tmax = fmax(tmax, fabs(x));
+              if (!(A.dbg & 2)) cbase[crun + k] = x;
+            }
           }
           crun += tot;
         }
