@@ -163,13 +163,26 @@ int pcwd_wavelet_transform(void* handle, const void* in, void* out, int inverse,
  *   z^(i) = Prox^Σ_{‖·‖_{1,w}}(y^(i) − τ Σ Θ_Lᵀ(Θ_L y^(i) − z0)),  y^(i+1) = z^(i) + (i−1)/(i+2)(z^(i) − z^(i−1)),
  * z^(0) = y^(1) = 0, for i = 1..iters.  precond = 0: Σ = I (FISTA-W); 1: Σ = diag(Θ_LᵀΘ_L)⁻¹ (FISTA-WP, Jacobi;
  * reading R-F1 of DESIGN.md).  Prox^Σ is the soft threshold at τ Σ_λλ w[λ].  *tau > 0 is used as the step;
- * *tau ≤ 0 computes τ = 0.99 / ‖Σ^½ Θ_LᵀΘ_L Σ^½‖₂ (power iteration until ‖M v‖ changes by < 1e-6 over 8 steps, at most 100) and returns it in *tau (this
- * synchronises the stream once).  z0 (= Ψ* f0), w (weights ≥ 0), z_out (= z^(iters)): DEVICE arrays of N values
- * of the handle's dtype.  Needs a decompose first and world = 1 (the whole Θ on this handle).  Θᵀ products are
- * gathers over a transposed copy of the CSR (built once per decompose, as for pcwd_apply with transpose = 1); the
- * Jacobi diagonal and the power-iteration norms accumulate in fp64 with atomics. */
+ * *tau ≤ 0 computes τ = 0.99 / ‖Σ^½ Θ_LᵀΘ_L Σ^½‖₂ (power iteration until ‖M v‖ changes by < 1e-6 over 8
+ * steps, at most 100) and returns it in *tau (this synchronises the stream every 8 power steps).  z0 (= Ψ* f0),
+ * w (weights ≥ 0), z_out (= z^(iters)): DEVICE arrays of N values of the handle's dtype.  Needs a decompose first
+ * and the whole Θ on this handle (a sharded Θ: pcwd_fista_sharded).  Θᵀ products are gathers over a transposed
+ * copy of the CSR (built once per decompose, as for pcwd_apply with transpose = 1); the Jacobi diagonal and the
+ * power-iteration norms accumulate in fp64 in a fixed order (the same bits on every run). */
 int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int precond, double* tau, void* z_out,
                void* stream);
+
+/* FISTA over a row-sharded Θ_L (one handle per rank): the same iteration as pcwd_fista,
+ * with Θ_L y computed on the handle's rows only and the gradient Θ_Lᵀ r = Σ_ranks Θ_rᵀ r_r summed by the caller:
+ * after writing its partial into xg (DEVICE, N values of the handle's dtype) the library calls reduce(0, ctx),
+ * which must replace xg by the sum over the ranks, ordered on `stream` (e.g. an NCCL all-reduce on that stream),
+ * and return 0; with precond = 1 the Jacobi diagonal's partial column sums (DEVICE, N fp64 in xd) are summed the
+ * same way once, by reduce(1, ctx).  z0 and w are the whole N-vectors (replicated); every rank computes the same
+ * z_out and τ (the norms of the power iteration are summed in a fixed order, so all ranks stop it together).
+ * A nonzero return of reduce stops the call with PCWD_E_PARAM.  The callback runs on the calling thread. */
+typedef int (*pcwd_reduce_fn)(int which, void* ctx);
+int pcwd_fista_sharded(void* handle, const void* z0, const void* w, int iters, int precond, double* tau, void* z_out,
+                       pcwd_reduce_fn reduce, void* ctx, void* xg, double* xd, void* stream);
 
 /* ---- Algorithm 1 proper: the η-approximation --------------------------------------- */
 

@@ -1375,7 +1375,7 @@ int pcwd_decompose_to_host(void* handle, int64_t* row_ptr, int32_t* col, void* v
 int fista_scratch(Handle* h, char** base, size_t* slice) {
   const int64_t N = h->hp.P.N;
   const size_t sl = (size_t(N) * h->hp.out_bytes + 255) & ~size_t(255);
-  const size_t need = 8 * sl + ((size_t(N + 1) * 8 + 255) & ~size_t(255));
+  const size_t need = 8 * sl + ((size_t(N + 1 + kFistaParts) * 8 + 255) & ~size_t(255));
   if (h->fbuf_bytes < need) {
     if (h->fbuf) cudaFree(h->fbuf);
     h->fbuf = nullptr;
@@ -1433,12 +1433,9 @@ int pcwd_wavelet_transform(void* handle, const void* in, void* out, int inverse,
   return PCWD_OK;
 }
 
-int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int precond, double* tau, void* z_out,
-               void* stream) {
-  Handle* h = static_cast<Handle*>(handle);
-  if (!h || !z0 || !w || !z_out || !tau) return fail(PCWD_E_PARAM, "NULL argument");
+static int fista_common(Handle* h, const void* z0, const void* w, int iters, int precond, double* tau, void* z_out,
+                        int (*reduce)(int, void*), void* ctx, void* xg, double* xd, void* stream) {
   if (!h->decomposed) return fail(PCWD_E_STATE, "decompose first");
-  if (h->rows() != h->hp.P.N) return fail(PCWD_E_STATE, "FISTA needs the whole Θ on one handle (world = 1)");
   if (iters < 0) return fail(PCWD_E_PARAM, "iters < 0");
   CK(cudaSetDevice(h->desc.device));
   char* base;
@@ -1455,10 +1452,11 @@ int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int preco
   F.y = base;
   F.zprev = base + sl;
   F.r = base + 2 * sl;
-  F.g = base + 3 * sl;
+  F.g = xg ? xg : base + 3 * sl;
   F.sigma = base + 4 * sl;
   F.sqrt_sigma = base + 5 * sl;
-  F.dbuf = reinterpret_cast<double*>(base + 8 * sl);
+  F.D = xd ? xd : reinterpret_cast<double*>(base + 8 * sl);
+  F.dbuf = reinterpret_cast<double*>(base + 8 * sl) + F.N;
   F.z_out = z_out;
   if (int rc = ensure_transpose(h, static_cast<cudaStream_t>(stream))) return rc;
   F.row_ptrT = h->rpT;
@@ -1467,8 +1465,31 @@ int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int preco
   F.iters = iters;
   F.precond = precond ? 1 : 0;
   F.power_iters = 100;   // at most; stops earlier when ‖M v‖ settles (relative change < 1e-6 over 8 iterations)
-  CK(launch_fista(h->hp.P, F, h->hp.out_bytes, static_cast<cudaStream_t>(stream), tau));
+  F.rows = h->rows();
+  F.row0 = h->hp.row0;
+  F.reduce = reduce;
+  F.rctx = ctx;
+  int cb_failed = 0;
+  const cudaError_t e = launch_fista(h->hp.P, F, h->hp.out_bytes, static_cast<cudaStream_t>(stream), tau, &cb_failed);
+  if (cb_failed) return fail(PCWD_E_PARAM, "the reduce callback failed");
+  CK(e);
   return PCWD_OK;
+}
+
+int pcwd_fista(void* handle, const void* z0, const void* w, int iters, int precond, double* tau, void* z_out,
+               void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !z0 || !w || !z_out || !tau) return fail(PCWD_E_PARAM, "NULL argument");
+  if (h->decomposed && h->rows() != h->hp.P.N)
+    return fail(PCWD_E_STATE, "FISTA needs the whole Θ on one handle (world = 1); use pcwd_fista_sharded");
+  return fista_common(h, z0, w, iters, precond, tau, z_out, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+int pcwd_fista_sharded(void* handle, const void* z0, const void* w, int iters, int precond, double* tau, void* z_out,
+                       pcwd_reduce_fn reduce, void* ctx, void* xg, double* xd, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !z0 || !w || !z_out || !tau || !reduce || !xg || (precond && !xd)) return fail(PCWD_E_PARAM, "NULL argument");
+  return fista_common(h, z0, w, iters, precond, tau, z_out, reduce, ctx, xg, xd, stream);
 }
 
 int pcwd_apply(void* handle, const void* x, void* y, int transpose, void* stream) {

@@ -136,12 +136,16 @@ __global__ void fista_update(Real* __restrict__ y, Real* __restrict__ zprev, Rea
   }
 }
 
-// Jacobi diagonal: D[λ] = Σ_μ Θ[μ][λ]² (fp64 accumulation), then σ = 1 / D (0 where D = 0)
+// Jacobi diagonal: D[λ] = Σ_μ Θ[μ][λ]² (fp64), over column λ of the transposed CSR in its fixed (row) order —
+// the same bits on every run; then σ = 1 / D (0 where D = 0)
 template <typename Real>
-__global__ void colsq_kernel(const int32_t* __restrict__ col, const Real* __restrict__ val, double* __restrict__ D,
-                             int64_t nnz) {
-  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < nnz; j += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(&D[col[j]], double(val[j]) * double(val[j]));
+__global__ void colsq_kernel(const int64_t* __restrict__ row_ptrT, const Real* __restrict__ valT,
+                             double* __restrict__ D, int64_t n) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n; c += int64_t(gridDim.x) * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t j = row_ptrT[c]; j < row_ptrT[c + 1]; ++j) acc += double(valT[j]) * double(valT[j]);
+    D[c] = acc;
+  }
 }
 template <typename Real>
 __global__ void inv_kernel(const double* __restrict__ D, Real* __restrict__ sigma, int64_t n, Real* __restrict__ ssig) {
@@ -152,10 +156,10 @@ __global__ void inv_kernel(const double* __restrict__ D, Real* __restrict__ sigm
   }
 }
 
-// out = s ⊙ in (s may be null: copy); sum of squares of out accumulated into *nrm (fp64)
+// out = s ⊙ in (s may be null: copy); the block's sum of squares of out (fp64) into parts[blockIdx.x]
 template <typename Real>
 __global__ void scale_norm(const Real* __restrict__ in, const Real* __restrict__ s, Real* __restrict__ out, int64_t n,
-                           double* __restrict__ nrm) {
+                           double* __restrict__ parts) {
   __shared__ double red[kFB / 32];
   double acc = 0.0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -169,8 +173,15 @@ __global__ void scale_norm(const Real* __restrict__ in, const Real* __restrict__
   if (threadIdx.x < 32) {
     acc = threadIdx.x < kFB / 32 ? red[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (threadIdx.x == 0) atomicAdd(nrm, acc);
+    if (threadIdx.x == 0) parts[blockIdx.x] = acc;
   }
+}
+// *nrm = Σ parts in a fixed order (one warp): the norm is the same bits on every run and on every rank
+__global__ void sum_parts(const double* __restrict__ parts, int np, double* __restrict__ nrm) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += 32) acc += parts[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (threadIdx.x == 0) *nrm = acc;
 }
 // v = in / sqrt(*nrm)
 template <typename Real>
@@ -243,8 +254,16 @@ cudaError_t launch_wavelet_transform(const Plan& P, const void* in, void* out, v
   return rb == 4 ? run(float()) : run(double());
 }
 
-cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t st, double* tau_io) {
-  const int64_t N = F.N;
+cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t st, double* tau_io, int* cb_failed) {
+  const int64_t N = F.N, rows = F.rows;
+  *cb_failed = 0;
+  // sharded Θ (rows [row0, row0 + rows)): Θ y is local to the rows, Θᵀ r = Σ_ranks Θ_rᵀ r_r is summed by the
+  // caller's reduce; every other vector is replicated and updated identically on every rank
+  auto reduce = [&](int which) -> cudaError_t {
+    if (!F.reduce) return cudaSuccess;
+    if (F.reduce(which, F.rctx) != 0) { *cb_failed = 1; return cudaErrorUnknown; }
+    return cudaSuccess;
+  };
   auto run = [&](auto tag) -> cudaError_t {
     using Real = decltype(tag);
     Real* y = static_cast<Real*>(F.y);
@@ -252,37 +271,37 @@ cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t
     Real* r = static_cast<Real*>(F.r);
     Real* g = static_cast<Real*>(F.g);
     Real* sig = F.precond ? static_cast<Real*>(F.sigma) : nullptr;
-    const Real* z0 = static_cast<const Real*>(F.z0);
+    const Real* z0 = static_cast<const Real*>(F.z0) + F.row0;
     const Real* w = static_cast<const Real*>(F.w);
     Real* zo = static_cast<Real*>(F.z_out);
     cudaError_t e;
     Real* ssig = sig ? static_cast<Real*>(F.sqrt_sigma) : nullptr;
-    if (F.precond) {   // Jacobi diagonal of ΘᵀΘ, σ = D⁻¹, and σ^½
-      if ((e = cudaMemsetAsync(F.dbuf, 0, N * sizeof(double), st))) return e;
-      colsq_kernel<Real><<<grid_of(F.nnz), kFB, 0, st>>>(F.col, static_cast<const Real*>(F.val), F.dbuf, F.nnz);
-      inv_kernel<Real><<<grid_of(N), kFB, 0, st>>>(F.dbuf, sig, N, ssig);
+    if (F.precond) {   // Jacobi diagonal of ΘᵀΘ (column sums of squares over all rows), σ = D⁻¹, and σ^½
+      colsq_kernel<Real><<<grid_of(N), kFB, 0, st>>>(F.row_ptrT, static_cast<const Real*>(F.valT), F.D, N);
+      if ((e = reduce(1))) return e;
+      inv_kernel<Real><<<grid_of(N), kFB, 0, st>>>(F.D, sig, N, ssig);
     }
     double tau = *tau_io;
     if (tau <= 0.0) {   // power iteration on M = Σ^½ ΘᵀΘ Σ^½ (Σ = I for FISTA-W): v ← M v / ‖M v‖
       Real* v = y;
-      double* nrm = F.dbuf + N;
-      init_vec<<<grid_of(N), kFB, 0, st>>>(rb == 4 ? reinterpret_cast<float*>(v) : nullptr,
-                                          rb == 8 ? reinterpret_cast<double*>(v) : nullptr, N, 12345u);
+      double* nrm = F.dbuf;
+      double* parts = F.dbuf + 1;
+      const int gN = grid_of(N);
+      init_vec<<<gN, kFB, 0, st>>>(rb == 4 ? reinterpret_cast<float*>(v) : nullptr,
+                                   rb == 8 ? reinterpret_cast<double*>(v) : nullptr, N, 12345u);
       double lam = 0.0;
       for (int it = 0; it < F.power_iters; ++it) {
         // u = Σ^½ v (into g), r = Θ u, g = Θᵀ r, u = Σ^½ g (into r), ‖u‖
-        if (ssig) {
-          if ((e = cudaMemsetAsync(nrm, 0, sizeof(double), st))) return e;
-          scale_norm<Real><<<grid_of(N), kFB, 0, st>>>(v, ssig, g, N, nrm);
-        } else {
-          copy_kernel<Real><<<grid_of(N), kFB, 0, st>>>(v, g, N);
-        }
-        if ((e = launch_spmv(F.row_ptr, F.col, F.val, g, r, N, N, 0, rb, st))) return e;
-        if ((e = launch_spmv(F.row_ptrT, F.rowT, F.valT, r, g, N, N, 0, rb, st))) return e;
-        if ((e = cudaMemsetAsync(nrm, 0, sizeof(double), st))) return e;
-        scale_norm<Real><<<grid_of(N), kFB, 0, st>>>(g, ssig, r, N, nrm);
-        normalize<Real><<<grid_of(N), kFB, 0, st>>>(r, v, N, nrm);
-        // every 8 iterations: stop once ‖M v‖ changes by less than 1e-6 (relative)
+        if (ssig) scale_norm<Real><<<gN, kFB, 0, st>>>(v, ssig, g, N, parts);
+        else copy_kernel<Real><<<gN, kFB, 0, st>>>(v, g, N);
+        if ((e = launch_spmv(F.row_ptr, F.col, F.val, g, r, rows, N, 0, rb, st))) return e;
+        if ((e = launch_spmv(F.row_ptrT, F.rowT, F.valT, r, g, N, rows, 0, rb, st))) return e;
+        if ((e = reduce(0))) return e;
+        scale_norm<Real><<<gN, kFB, 0, st>>>(g, ssig, r, N, parts);
+        sum_parts<<<1, 32, 0, st>>>(parts, gN, nrm);
+        normalize<Real><<<gN, kFB, 0, st>>>(r, v, N, nrm);
+        // every 8 iterations: stop once ‖M v‖ changes by less than 1e-6 (relative); the norm is deterministic and
+        // g is the same on every rank after the reduce, so every rank takes the same decision
         if ((it + 1) % 8 == 0 && it + 1 < F.power_iters) {
           double cur = 0.0;
           if ((e = cudaMemcpyAsync(&cur, nrm, sizeof(double), cudaMemcpyDeviceToHost, st))) return e;
@@ -301,9 +320,10 @@ cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t
     if ((e = cudaMemsetAsync(y, 0, N * rb, st))) return e;
     if ((e = cudaMemsetAsync(zp, 0, N * rb, st))) return e;
     for (int i = 1; i <= F.iters; ++i) {
-      if ((e = launch_spmv(F.row_ptr, F.col, F.val, y, r, N, N, 0, rb, st))) return e;    // r = Θ y
-      sub_kernel<Real><<<grid_of(N), kFB, 0, st>>>(r, z0, N);                              // r −= z0
-      if ((e = launch_spmv(F.row_ptrT, F.rowT, F.valT, r, g, N, N, 0, rb, st))) return e;   // g = Θᵀ r (gather)
+      if ((e = launch_spmv(F.row_ptr, F.col, F.val, y, r, rows, N, 0, rb, st))) return e;    // r = Θ y (rows)
+      sub_kernel<Real><<<grid_of(rows), kFB, 0, st>>>(r, z0, rows);                          // r −= z0 (rows)
+      if ((e = launch_spmv(F.row_ptrT, F.rowT, F.valT, r, g, N, rows, 0, rb, st))) return e;  // g = Θᵀ r (gather)
+      if ((e = reduce(0))) return e;                                                         // Σ over the shards
       const Real beta = Real(double(i - 1) / double(i + 2));
       fista_update<Real><<<grid_of(N), kFB, 0, st>>>(y, zp, zo, g, w, sig, Real(tau), beta, N);
     }

@@ -163,10 +163,16 @@ struct FistaArgs {
   const void* z0;     // Ψ* f0
   const void* w;      // ℓ1 weights w[λ]
   void *y, *zprev, *r, *g, *sigma, *sqrt_sigma, *z_out;
-  double* dbuf;
+  double* D;          // Jacobi diagonal (N, fp64)
+  double* dbuf;       // norm (1) + per-block partial sums (kFistaParts)
   int iters, precond, power_iters;
+  int64_t rows, row0;                    // the handle's rows of Θ (rows = N, row0 = 0: the whole Θ)
+  int (*reduce)(int which, void* ctx);   // sharded Θ: sum g (which = 0) / D (which = 1) over the ranks, in place,
+  void* rctx;                            // ordered on the stream; null: the whole Θ is on this handle
 };
-cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t st, double* tau_io);
+constexpr int kFistaParts = 4096;        // ≥ the element-wise kernels' grid (grid_of in fista.cu)
+// cb_failed: set when the reduce callback returned nonzero (the launch then stops and returns cudaErrorUnknown)
+cudaError_t launch_fista(const Plan& P, const FistaArgs& F, int rb, cudaStream_t st, double* tau_io, int* cb_failed);
 // Ψ* (inverse = 0) or Ψ (inverse = 1) of one length-N array on the plan's grid; work0/1: N elements each.
 cudaError_t launch_wavelet_transform(const Plan& P, const void* in, void* out, void* work0, void* work1, int inverse,
                                      int rb, cudaStream_t st);

@@ -60,8 +60,9 @@ EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_m
            "pcwd_last_error", "pcwd_validate", "pcwd_plan_shard", "pcwd_plan_stencil",
            "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile",
            "pcwd_set_kernels", "pcwd_decompose_to_host", "pcwd_wavelet_transform", "pcwd_fista",
-           "pcwd_approx", "pcwd_operator_apply", "pcwd_pc_from_samples", "pcwd_pc_from_svir", "pcwd_columns"]
+           "pcwd_fista_sharded", "pcwd_approx", "pcwd_operator_apply", "pcwd_pc_from_samples", "pcwd_pc_from_svir", "pcwd_columns"]
 
+REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_void_p)   # pcwd_reduce_fn
 _lib = None
 
 
@@ -97,6 +98,8 @@ def lib():
         L.pcwd_decompose_to_host.argtypes = [vp, vp, vp, vp, vp]
         L.pcwd_wavelet_transform.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         L.pcwd_fista.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), vp, vp]
+        L.pcwd_fista_sharded.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), vp,
+                                         REDUCE_FN, vp, vp, vp, vp]
         L.pcwd_approx.argtypes = [vp, ctypes.c_double, ctypes.c_int, vp, ctypes.POINTER(ApproxInfo)]
         L.pcwd_operator_apply.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         L.pcwd_pc_from_samples.argtypes = [i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]
@@ -204,6 +207,33 @@ class Decomposition:
         t = ctypes.c_double(tau)
         _check(lib().pcwd_fista(self._h, ctypes.c_void_p(_ptr(z0)), ctypes.c_void_p(_ptr(w)), int(iters), int(precond),
                                 ctypes.byref(t), ctypes.c_void_p(_ptr(z)), ctypes.c_void_p(stream)), "pcwd_fista")
+        return z, t.value
+
+    def fista_sharded(self, z0, w, iters: int, reduce, precond: bool = False, tau: float = 0.0, stream: int = 0):
+        """FISTA over this handle's rows of a row-sharded Θ_L (pcwd_fista_sharded); returns (z, τ).
+        reduce(which, buf) must sum the CUDA tensor buf over the ranks in place, ordered on `stream` (which = 0:
+        the gradient, N values of the handle's dtype; 1: the Jacobi column sums, N fp64)."""
+        import torch
+        z = torch.empty_like(z0)
+        xg = torch.empty_like(z0)
+        xd = torch.empty(z0.numel(), dtype=torch.float64, device=z0.device)
+        err = []
+
+        def cb(which, _ctx):
+            try:
+                reduce(int(which), xg if which == 0 else xd)
+                return 0
+            except Exception as e:   # reported through the library's return code
+                err.append(e)
+                return 1
+        fn = REDUCE_FN(cb)
+        t = ctypes.c_double(tau)
+        rc = lib().pcwd_fista_sharded(self._h, ctypes.c_void_p(_ptr(z0)), ctypes.c_void_p(_ptr(w)), int(iters),
+                                      int(precond), ctypes.byref(t), ctypes.c_void_p(_ptr(z)), fn, None,
+                                      ctypes.c_void_p(_ptr(xg)), ctypes.c_void_p(_ptr(xd)), ctypes.c_void_p(stream))
+        if err:
+            raise err[0]
+        _check(rc, "pcwd_fista_sharded")
         return z, t.value
 
     def approx(self, eta: float, rule: str = "index", stream: int = 0) -> dict:
@@ -465,6 +495,19 @@ def apply_distributed(dec: "Decomposition", x, transpose: bool = False):
     y = dec.apply(x[info.row0:info.row1].contiguous(), transpose=True)
     dist.all_reduce(y, op=dist.ReduceOp.SUM)
     return y
+
+
+def fista_distributed(dec: "Decomposition", z0, w, iters: int, precond: bool = False, tau: float = 0.0, group=None):
+    """FISTA-W / WP over a Θ_L sharded by rows across the ranks of `group` (one handle per rank): the
+    per-iteration exchange is one all-reduce of the N-vector gradient (NCCL on the current stream).  z0, w: the whole
+    N-vectors on every rank; returns (z, τ), the same on every rank."""
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream(z0.device).cuda_stream if z0.is_cuda else 0
+
+    def reduce(_which, buf):
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return dec.fista_sharded(z0, w, iters, reduce, precond=precond, tau=tau, stream=stream)
 
 
 # ---- host-only plan queries (no GPU) ---------------------------------------------------------

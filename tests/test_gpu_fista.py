@@ -113,3 +113,121 @@ def test_fista_needs_decompose_and_one_shard():
     with pytest.raises(PcwdError):
         d2.fista(z, z, 5)
     d2.close()
+
+
+def _fista_problem(dtype):
+    p = C.micro(32, 2, 4, 3, 3, 3, 51, retain="band", band_L=64)
+    TL = _theta_band_dense(p)
+    rng = np.random.default_rng(9)
+    z_true = rng.standard_normal(p.N) * (rng.uniform(size=p.N) < 0.2)
+    z0 = TL @ z_true + 1e-3 * rng.standard_normal(p.N)
+    lev, _, _, _ = basis.index_of(p.d, p.n, p.J)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    return p, TL, torch.from_numpy(z0).to(tdt).cuda(), torch.from_numpy(2e-3 * (1.0 + lev)).to(tdt).cuda()
+
+
+@pytest.mark.parametrize("precond", [False, True])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_fista_sharded_world1_is_fista(precond, dtype):
+    """pcwd_fista_sharded on the whole Θ with a one-rank reduce (nothing to add) = pcwd_fista, bit for bit."""
+    p, _, z0, w = _fista_problem(dtype)
+    dec = _handle(p, dtype)
+    dec.decompose()
+    za, ta = dec.fista(z0, w, 25, precond=precond)
+    calls = []
+    zb, tb = dec.fista_sharded(z0, w, 25, lambda which, buf: calls.append(which), precond=precond)
+    assert ta == tb and torch.equal(za, zb)
+    assert calls.count(0) >= 25 + 8 and calls.count(1) == (1 if precond else 0)
+    dec.close()
+
+
+@pytest.mark.parametrize("precond", [False, True])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_fista_two_shards_match_whole(precond, dtype):
+    """Θ_L split over two handles (rank 0 / 1 of world 2), each running pcwd_fista_sharded in its own thread and
+    stream; the reduce sums the two partial gradients (a two-party all-reduce on the host threads).  The iterates
+    equal the one-handle FISTA up to the summation order of Θᵀr, and both ranks return the same z and τ."""
+    import threading
+    p, TL, z0, w = _fista_problem(dtype)
+    whole = _handle(p, dtype)
+    whole.decompose()
+    zr, tr = whole.fista(z0, w, 40, precond=precond)
+    whole.close()
+    decs = [Decomposition(Spec(p.d, p.n, p.J, p.h, p.u, p.v, dtype=dtype, retain="band", band_L=p.band_L, rank=r,
+                               world=2)) for r in range(2)]
+    for d in decs:
+        d.decompose()
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    bar = threading.Barrier(2, timeout=120)   # a failing rank breaks the barrier instead of hanging the test
+    bufs = [None, None]
+    out = [None, None]
+
+    def reduce_for(r):
+        def reduce(_which, buf):
+            streams[r].synchronize()
+            bufs[r] = buf
+            bar.wait()
+            if r == 0:
+                s = bufs[0] + bufs[1]
+                bufs[0].copy_(s)
+                bufs[1].copy_(s)
+                torch.cuda.synchronize()
+            bar.wait()
+        return reduce
+
+    def run(r):
+        with torch.cuda.stream(streams[r]):
+            out[r] = decs[r].fista_sharded(z0, w, 40, reduce_for(r), precond=precond,
+                                           stream=streams[r].cuda_stream)
+        streams[r].synchronize()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert out[0] is not None and out[1] is not None
+    (z_a, t_a), (z_b, t_b) = out
+    assert t_a == t_b and torch.equal(z_a, z_b)
+    assert abs(t_a / tr - 1.0) < (1e-5 if dtype == "f32" else 1e-10)
+    err = _rel(z_a.double().cpu().numpy(), zr.double().cpu().numpy())
+    from conftest import record_parity
+    record_parity(f"fista{'wp' if precond else 'w'}_2shards_vs_whole", dtype, err, p.N)
+    assert err <= (1e-5 if dtype == "f32" else 1e-10)
+    # and against the oracle's FISTA at the same step
+    sigma = OF.jacobi_sigma(TL) if precond else None
+    ref = OF.fista(TL, z0.double().cpu().numpy(), w.double().cpu().numpy(), 40, sigma=sigma, tau=t_a)
+    assert _rel(z_a.double().cpu().numpy(), ref) <= (1e-5 if dtype == "f32" else 1e-10)
+    for d in decs:
+        d.close()
+
+
+def test_fista_distributed_nccl_world1(tmp_path):
+    """fista_distributed through a real NCCL process group (world 1, one process): same z as pcwd_fista."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+from paper_2005_09870_b200 import Decomposition, Spec, pcwd as PW
+from synth import configs as C
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+p = C.micro(32, 2, 4, 3, 3, 3, 51, retain="band", band_L=64)
+dec = Decomposition(Spec(p.d, p.n, p.J, p.h, p.u, p.v, dtype="f64", retain="band", band_L=64))
+dec.decompose()
+rng = np.random.default_rng(3)
+z0 = torch.from_numpy(rng.standard_normal(p.N)).cuda()
+w = torch.full((p.N,), 1e-3, dtype=torch.float64, device="cuda")
+za, ta = dec.fista(z0, w, 20, precond=True)
+zb, tb = PW.fista_distributed(dec, z0, w, 20, precond=True)
+torch.cuda.synchronize()
+assert ta == tb and torch.equal(za, zb), (ta, tb)
+dist.destroy_process_group()
+print("NCCL-FISTA-OK")
+'''
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29500 + os.getpid() % 1000))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert "NCCL-FISTA-OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

@@ -3,7 +3,8 @@
 The data path has no collective (units are independent); what crosses ranks is
 (a) the cost-balanced shard plan each rank derives on its own, which must partition Λ, (b) the
 threshold rule's MAX all-reduce of the per-rank maxima (P:1179 threshold, reading R15), and
-(c) the bench's max-over-ranks timing and sum of retained entries.  The per-rank maxima here come
+(c) the bench's max-over-ranks timing and sum of retained entries, and (d) the consumer's exchange: the
+sharded FISTA's all-reduce of the gradient Θ_Lᵀr = Σ_r Θ_rᵀ r_r.  The per-rank maxima here come
 from the oracle (the GPU computes them in the real run) — the exchange is what is tested.
 """
 import os
@@ -131,3 +132,49 @@ def test_gloo_world2_offsets_gather_apply():
     for r in res:                                                           # C-d: Σ_r Θ_rᵀ x_r = Θᵀ x
         assert np.allclose(r[2], dense.T @ x, rtol=1e-13, atol=1e-13)
         assert list(r[3]) == [2.0, 5.0]                                     # per-step max over ranks
+
+
+class _ShardStub:
+    """Stands in for a sharded handle on CPU: fista_sharded calls the reduce it is given on this rank's partial
+    gradient (and Jacobi column sums), as pcwd_fista_sharded does, and returns what the reduce left."""
+    def __init__(self, rank):
+        self.rank = rank
+
+    def fista_sharded(self, z0, w, iters, reduce, precond=False, tau=0.0, stream=0):
+        import torch
+        g = torch.full_like(z0, float(self.rank + 1))
+        calls = 0
+        for _ in range(iters):
+            reduce(0, g)
+            calls += 1
+            g /= 2.0                          # keep values exact: 3 → 1.5 + 1.5 …
+        d = torch.arange(z0.numel(), dtype=torch.float64) * (self.rank + 1)
+        if precond:
+            reduce(1, d)
+        return g, d
+
+
+def _worker_fista(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        from paper_2005_09870_b200 import pcwd as P
+        z0 = torch.zeros(8, dtype=torch.float64)
+        g, d = P.fista_distributed(_ShardStub(rank), z0, z0, 1, precond=True)
+        out[rank] = (g.numpy(), d.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_fista_distributed_reduces_over_ranks():
+    """fista_distributed's exchange: the gradient (which 0) and the Jacobi column sums (which 1) are summed over
+    the ranks in place (gloo, world 2) — the host side of the sharded FISTA."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_fista, args=(world, port, out), nprocs=world, join=True)
+    for r in range(world):
+        g, d = out[r]
+        assert np.array_equal(g, np.full(8, 1.5)) and np.array_equal(d, np.arange(8) * 3.0)
