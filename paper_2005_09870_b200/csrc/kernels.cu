@@ -229,7 +229,8 @@ __device__ __forceinline__ int qdiv(int a, int b, float inv_b) {
 // outputs at 2j + t share all but two inputs): 14 + 2δ loads and one bounds test each for 8·2δ FMAs, instead of
 // 2δ loads, tests and index computations per output.  TL2 = 2δ is a compile-time constant (taps from the
 // kernel-parameter bank by compile-time index).  mode 0: window clear of wrapping (signed offset, zero outside);
-// mode 1: whole periodic line (index mod the line).
+// mode 1: whole periodic line (index mod the line); mode 2: a window whose taps can wrap onto it (local index
+// mod the line, zero outside the window: local_index per input).
 constexpr int kNQ = 4;   // outputs per task (4: the kernel keeps ≤ 80 registers, 3 CTAs per SM)
 
 template <typename Real, int TL2>
@@ -241,9 +242,15 @@ __device__ __forceinline__ void run_load(const Real* __restrict__ base, int64_t 
 #pragma unroll
     for (int i = 0; i < 2 * kNQ - 2 + TL2; ++i)
       x[i] = unsigned(dq + i) < unsigned(in.len) ? base[int64_t(dq + i) * stride] : Real(0);
-  } else {
+  } else if (mode == 1) {
 #pragma unroll
     for (int i = 0; i < 2 * kNQ - 2 + TL2; ++i) x[i] = base[int64_t((q0 + i - in.lo) & (in.nl - 1)) * stride];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 2 * kNQ - 2 + TL2; ++i) {
+      const int li = (q0 + i - in.lo) & (in.nl - 1);
+      x[i] = li < in.len ? base[int64_t(li) * stride] : Real(0);
+    }
   }
 }
 
@@ -253,8 +260,9 @@ __device__ void pass_a_blk(const Plan& P, const Real* __restrict__ cur, Real* __
   const int ycols = a1.len + d1.len;
   const int ga = (a1.len + kNQ - 1) / kNQ, gd = (d1.len + kNQ - 1) / kNQ;
   const int tot = in0.len * (ga + gd);
+  const float inv = 1.0f / float(in0.len);
   for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-    const int g = idx / in0.len, i0 = idx - g * in0.len;   // consecutive threads: consecutive rows
+    const int g = qdiv(idx, in0.len, inv), i0 = idx - g * in0.len;   // consecutive threads: consecutive rows
     const int e1 = g >= ga;
     const int j0 = kNQ * (e1 ? g - ga : g);
     const Range& R = e1 ? d1 : a1;
@@ -279,8 +287,9 @@ __device__ void pass_b_blk(const Plan& P, const Real* __restrict__ Y, Real* __re
   const int s01 = a0.len * d1.len, s10 = d0.len * a1.len;
   const int ga = (a0.len + kNQ - 1) / kNQ, gd = (d0.len + kNQ - 1) / kNQ;
   const int tot = ycols * (ga + gd);
+  const float inv = 1.0f / float(ycols);
   for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-    const int g = idx / ycols, colY = idx - g * ycols;     // consecutive threads: consecutive columns
+    const int g = qdiv(idx, ycols, inv), colY = idx - g * ycols;     // consecutive threads: consecutive columns
     const int e0 = g >= ga;
     const int j0 = kNQ * (e0 ? g - ga : g);
     const Range& R = e0 ? d0 : a0;
@@ -363,8 +372,9 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) unit_kernel(const __gri
       const bool f1 = S.tW[1] >= n;
       const int tw1 = S.tRS;
       const int total = r0.len * r1.len;
+      const float inv_r1 = 1.0f / float(r1.len);
       for (int idx = tid; idx < total; idx += NT) {
-        const int i0 = idx / r1.len, i1 = idx - i0 * r1.len;
+        const int i0 = qdiv(idx, r1.len, inv_r1), i1 = idx - i0 * r1.len;
         const int y0 = D == 2 ? ((r0.lo + i0) & mask) : 0;
         const int y1 = (r1.lo + i1) & mask;
         const int t0 = f0 ? ((y0 - (p0 << S.level)) & mask) : i0;
@@ -415,7 +425,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) unit_kernel(const __gri
         const int totA = in0.len * ycols;
         const float inv_y = 1.0f / float(ycols), inv_a1 = 1.0f / float(a1.len), inv_d1 = 1.0f / float(d1.len);
         const int k1 = kind(in1);
-        const bool blkA = k1 <= 1 && pass_a_dispatch<Real>(P, cur, Y, in0, in1, a1, d1, k1);
+        const bool blkA = pass_a_dispatch<Real>(P, cur, Y, in0, in1, a1, d1, k1);
         for (int idx = blkA ? totA : tid; idx < totA; idx += NT) {       // pass A: axis 1
           const int i0 = qdiv(idx, ycols, inv_y), j = idx - i0 * ycols;
           const int e1 = j >= a1.len;
@@ -449,7 +459,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) unit_kernel(const __gri
         s10 = d0.len * a1.len;
         const int s11 = d0.len * d1.len;
         const int totB = s00 + s01 + s10 + s11;
-        const bool blkB = k0 <= 1 && pass_b_dispatch<Real>(P, Y, nxt, Dd, in0, a0, d0, a1, d1, k0);
+        const bool blkB = pass_b_dispatch<Real>(P, Y, nxt, Dd, in0, a0, d0, a1, d1, k0);
         for (int idx = blkB ? totB : tid; idx < totB; idx += NT) {       // pass B: axis 0
           int e0, e1, j0, j1, rem;
           Real* dst;
