@@ -37,6 +37,7 @@ struct Launch {
   int64_t appr0[kMaxJ + 1] = {}, appr1[kMaxJ + 1] = {};   // batched: per-step max approximation window
   int steps = 0;
   int gu = 1;       // fine: units per round (chunks of a launch are multiples of it)
+  int hybrid = 0;   // generic kernel, global scratch: smem (bytes) holds the buffers of steps ≥ 2
   size_t bs_off = 0;  // batched: byte offset of this launch's slice of the batched scratch
   int64_t gs_off = -1, gs_stride = 0;   // generic, global scratch: element offset of this launch's slice, per-CTA stride
 };
@@ -435,7 +436,8 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     A.unitmax = h->unitmax;
     A.cnt = h->cnt;
     A.tau = tau;
-    A.use_smem = L.smem > 0;
+    A.use_smem = L.smem > 0 && !L.hybrid;
+    A.hybrid = L.hybrid;
     A.cand = h->cand;
     static const int unit_dbg = getenv("PCWD_UNIT_DBG") ? atoi(getenv("PCWD_UNIT_DBG")) : 0;
     A.dbg = unit_dbg;
@@ -642,6 +644,16 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
       L.gs_stride = (scr + 31) & ~int64_t(31);
       L.gs_off = gmax;
       gmax += L.gs_stride * L.grid;
+      // hybrid: the step-1 approximation and every buffer of steps ≥ 2 (small windows, latency-bound chains of
+      // barriers) in shared memory; the k-sum window and the step-1 pass-A / detail buffers stay in global
+      int64_t hs = 0;
+      for (int q = 0; q < P.nsb; ++q)
+        if (P.sb[q].offset < u1 && P.sb[q].offset + P.sb[q].count > u0) hs = std::max(hs, P.sb[q].hs_size);
+      static const size_t hcap = size_t(getenv("PCWD_HYBRID_KB") ? atoi(getenv("PCWD_HYBRID_KB")) : 40) << 10;
+      if (hs > 0 && size_t(hs) * rb <= std::min<size_t>(budget, hcap)) {
+        L.smem = size_t(hs) * rb;
+        L.hybrid = 1;
+      }
     }
     h->launches.push_back(L);
   };

@@ -88,6 +88,10 @@ struct SubBand {
   int tRS;          // template row stride (tW[1] rounded up to 4 unless the row is a whole line)
   // per-unit scratch layout (elements of the compute type)
   int64_t offX0, offX1, offY, offD, offStage, scratch;
+  // hybrid layout (global-scratch launches): the buffers of steps ≥ 2 and the step-1 approximation in shared
+  // memory (elements): approximations X1 (steps 1, 3, …) and X2 (steps 2, 4, …), pass-A output Y and detail
+  // boxes D of steps ≥ 2; hs_size = their total
+  int64_t hs_X1, hs_X2, hs_Y, hs_D, hs_size;
   int stencil_off;  // BAND: first entry of this sub-band's stencil
   int any_full;     // some window of this sub-band covers a whole line (general path only)
   int tSu[2];       // template window start, unwrapped: -zhi + (e_a ? 2^{ℓ-1}(2-2δ) : 0)

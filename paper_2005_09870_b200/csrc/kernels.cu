@@ -359,7 +359,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) unit_kernel(const __gri
     const Range r0 = D == 2 ? unit_window(P, S, 0, p0) : Range{0, 1, 1};
     const Range r1 = unit_window(P, S, 1, p1);
     Real* X0 = scratch + S.offX0;
-    Real* X1 = scratch + S.offX1;
+    Real* hs = reinterpret_cast<Real*>(smem_raw);   // hybrid: shared-memory buffers of steps ≥ 2
+    Real* X1 = A.hybrid ? hs + S.hs_X1 : scratch + S.offX1;
     Real* Y = scratch + S.offY;
     Real* Dd = scratch + S.offD;
     Real* stage_val = scratch + S.offStage;
@@ -392,6 +393,7 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) unit_kernel(const __gri
     }
     // PATTERN: the cascade runs up to the coarsest level among the unit's listed partners
     int nsteps = S.steps;
+    if (A.dbg >> 4) nsteps = min(nsteps, A.dbg >> 4);   // timing experiment (PCWD_UNIT_DBG = 16·s): stop after step s
     if (MODE == MODE_PATTERN) {
       int mx = 0;
       for (int64_t j = A.row_ptr[row] + tid; j < A.row_ptr[row + 1]; j += NT) mx = max(mx, P.sb[find_subband(P, A.col[j])].level);
@@ -644,6 +646,11 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 6 : 3) unit_kernel(const __gri
       }
       __syncthreads();
       Real* tswap = cur; cur = nxt; nxt = tswap;
+      if (A.hybrid && s == 1) {   // steps ≥ 2 work in shared memory: approximations X1 / X2, Y, D
+        nxt = hs + S.hs_X2;
+        Y = hs + S.hs_Y;
+        Dd = hs + S.hs_D;
+      }
       in0 = a0;
       in1 = a1;
     }

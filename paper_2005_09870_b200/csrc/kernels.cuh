@@ -23,6 +23,7 @@ struct UnitArgs {
   int32_t* cnt;             // TCOUNT / TWRITE: [row][sb]
   double tau;               // threshold (fp64)
   int use_smem;
+  int hybrid;               // global-scratch launch with the step ≥ 2 buffers in shared memory (SubBand::hs_*)
   double* cand;             // TSTORE: every structural partner value of the unit, window by window in column order
   int dbg;                  // timing experiments only (PCWD_UNIT_DBG, results invalid): 1 = no k-sum, 2 = no candidate stores
 };

@@ -345,6 +345,7 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
     auto rs4 = [](int64_t x) { return (x + 3) & ~int64_t(3); };   // batched path: 16-byte row strides
     int64_t X0 = w0 * rs4(w1);
     int64_t maxA = 0, maxY = 0, maxD = 0;
+    int64_t hA1 = 0, hA2 = 0, hY = 0, hD = 0;   // hybrid layout: step-1 / step-2 approximations, steps ≥ 2
     double fma = double(P.m) * X0;
     S.any_full = (S.tW[1] >= n) || (P.d == 2 && S.tW[0] >= n);
     for (int st = 1; st <= S.steps; ++st) {
@@ -354,10 +355,14 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
         maxY = std::max(maxY, w0 * 2 * o1);
         maxA = std::max(maxA, o0 * rs4(o1));
         maxD = std::max(maxD, 3 * o0 * o1);
+        if (st % 2) hA1 = std::max(hA1, o0 * o1); else hA2 = std::max(hA2, o0 * o1);
+        if (st >= 2) { hY = std::max(hY, w0 * 2 * o1); hD = std::max(hD, 3 * o0 * o1); }
         fma += double(L2) * (w0 * 2.0 * o1 + 4.0 * o0 * o1);
       } else {
         maxA = std::max(maxA, o1);
         maxD = std::max(maxD, o1);
+        if (st % 2) hA1 = std::max(hA1, o1); else hA2 = std::max(hA2, o1);
+        if (st >= 2) { hY = std::max(hY, 2 * o1); hD = std::max(hD, o1); }
         fma += double(L2) * 2.0 * o1;
       }
       w0 = o0; w1 = o1;
@@ -373,6 +378,11 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
     int64_t stage = 0;
     if (P.retain == PCWD_RETAIN_BAND) stage = P.band_Lpad + (int64_t(P.band_Lpad) * 4 + rb - 1) / rb;
     S.scratch = S.offStage + al(stage);
+    S.hs_X1 = 0;
+    S.hs_X2 = al(hA1);
+    S.hs_Y = S.hs_X2 + al(hA2);
+    S.hs_D = S.hs_Y + al(hY);
+    S.hs_size = S.hs_D + al(hD);
     S.fma = fma;
 
     // warp kernel: band rule, d = 2, windows never cover a whole line, per-warp scratch small
