@@ -1241,7 +1241,14 @@ int pcwd_decompose(void* handle, void* stream) {
     }
     const double tau = h->desc.tau_rel * h->M;
     CK(cudaMemsetAsync(h->cnt, 0, size_t(std::max<int64_t>(rows * P.nsb, 1)) * sizeof(int32_t), st));
-    if (h->cand_valid) {
+    // fp32 values: count and compact in one read of the candidates (the CSR copy follows the scan)
+    static const bool no_compact = getenv("PCWD_NO_COMPACT") != nullptr;
+    const bool compact = h->cand_valid && h->hp.out_bytes == 4 && !no_compact;
+    if (compact) {
+      CK(launch_cand_compact(P, static_cast<double*>(h->cand), h->hp.row0, rows, tau, h->cnt, st));
+      h->nlaunch++;
+      h->cand_valid = false;   // the buffer now holds the compacted rows (a failed decompose must recompute)
+    } else if (h->cand_valid) {
       CK(launch_cand_filter(P, h->cand, h->hp.row0, rows, tau, 0, h->cnt, nullptr, nullptr, nullptr, h->hp.out_bytes, st));
       h->nlaunch++;
     } else if ((rc = run_units(h, MODE_TCOUNT, st, tau))) {
@@ -1273,8 +1280,9 @@ int pcwd_decompose(void* handle, void* stream) {
         return true;
       };
       bool ok = grow(nnz + nnz / 8 + 1024) || grow(nnz);
-      if (!ok && h->cand) {
-        // the store-then-filter buffer starves the CSR: drop it and write the rows by the recompute pass
+      if (!ok && h->cand && !compact) {
+        // the store-then-filter buffer starves the CSR: drop it and write the rows by the recompute pass (not after
+        // a compaction: the compacted rows live in that buffer)
         cudaFree(h->cand);
         h->cand = nullptr;
         h->cand_valid = false;
@@ -1286,7 +1294,11 @@ int pcwd_decompose(void* handle, void* stream) {
       h->cap = got;
     }
     h->nnz = nnz;
-    if (h->cand_valid) {
+    if (compact) {
+      CK(launch_cand_copy(P, static_cast<const double*>(h->cand), h->hp.row0, rows, h->cnt, h->row_ptr, h->col,
+                          static_cast<float*>(h->val), st));
+      h->nlaunch++;
+    } else if (h->cand_valid) {
       CK(launch_cand_filter(P, h->cand, h->hp.row0, rows, tau, 1, h->cnt, h->row_ptr, h->col, h->val,
                             h->hp.out_bytes, st));
       h->nlaunch++;

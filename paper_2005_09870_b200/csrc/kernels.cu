@@ -770,6 +770,125 @@ __global__ void __launch_bounds__(kBlock) cand_filter_kernel(const __grid_consta
   }
 }
 
+// THRESHOLD, fp32 values: one read of the candidates instead of two.  cand_compact_kernel walks a unit's windows in
+// emission order (as cand_filter_kernel), counts the kept entries per (unit, sub-band) into cnt and compacts them IN
+// PLACE at the front of the unit's own candidate slot as (fp32 value bits | column << 32) — the write position never
+// passes the read position, and a chunk's loads complete before its ballot; cand_copy_kernel then moves each
+// sub-band's compacted run to its CSR position (row_ptr from the counts; sub-bands in Λ order = column order).
+constexpr int kCU = 4;   // candidate chunks of 32 loaded ahead per warp in the compaction
+
+template <int D>
+__global__ void __launch_bounds__(kBlock) cand_compact_kernel(const __grid_constant__ Plan P, double* cand, int64_t row0,
+                                                              int64_t rows, double tau, int32_t* cnt) {
+  const int lane = threadIdx.x & 31, L2 = P.L2;
+  const int64_t warp0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t row = warp0; row < rows; row += nwarps) {
+    const int64_t unit = row0 + row;
+    const int sbi = find_subband(P, unit);
+    const SubBand& S = P.sb[sbi];
+    const int64_t pos = unit - S.offset;
+    const int p0 = D == 2 ? int(pos / S.nl) : 0;
+    const int p1 = D == 2 ? int(pos - int64_t(p0) * S.nl) : int(pos);
+    Range in0 = D == 2 ? unit_window(P, S, 0, p0) : Range{0, 1, 1};
+    Range in1 = unit_window(P, S, 1, p1);
+    double* cb = cand + S.cand_off + (unit - (S.offset > row0 ? S.offset : row0)) * S.cand_slot;
+    unsigned long long* out = reinterpret_cast<unsigned long long*>(cb);
+    int64_t crun = 0, wpos = 0;
+    for (int s = 1; s <= S.steps; ++s) {
+      const Range a0 = D == 2 ? step_out(in0, L2, 0) : Range{0, 1, 1};
+      const Range d0 = D == 2 ? step_out(in0, L2, 1) : Range{0, 1, 1};
+      const Range a1 = step_out(in1, L2, 0);
+      const Range d1 = step_out(in1, L2, 1);
+      Range wr0[4], wr1[4];
+      int wsb[4], nw = 0;
+      const int base_sb = 1 + (P.J - s) * (D == 2 ? 3 : 1);
+      if (D == 2) {
+        wr0[nw] = a0; wr1[nw] = d1; wsb[nw++] = base_sb + 0;
+        wr0[nw] = d0; wr1[nw] = a1; wsb[nw++] = base_sb + 1;
+        wr0[nw] = d0; wr1[nw] = d1; wsb[nw++] = base_sb + 2;
+      } else {
+        wr0[nw] = Range{0, 1, 1}; wr1[nw] = d1; wsb[nw++] = base_sb;
+      }
+      if (s == P.J) { wr0[nw] = a0; wr1[nw] = a1; wsb[nw++] = 0; }
+      for (int wi = 0; wi < nw; ++wi) {
+        const int tot = wr0[wi].len * wr1[wi].len;
+        const double* cw = cb + crun;
+        const SubBand& L = P.sb[wsb[wi]];
+        int running = 0;
+        const float inv_w = 1.0f / float(wr1[wi].len);
+        for (int k0 = 0; k0 < tot; k0 += kCU * 32) {   // kCU loads in flight per lane before the first ballot
+          double xs[kCU];
+#pragma unroll
+          for (int u = 0; u < kCU; ++u) {
+            const int k = k0 + 32 * u + lane;
+            xs[u] = k < tot ? cw[k] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kCU; ++u) {
+            const int k = k0 + 32 * u + lane;
+            const int keep = k < tot && fabs(xs[u]) >= tau;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+              const int ks0 = qdiv(k, wr1[wi].len, inv_w), ks1 = k - ks0 * wr1[wi].len;
+              const int i0 = sorted_to_local(wr0[wi], ks0), i1 = sorted_to_local(wr1[wi], ks1);
+              const int g0 = (wr0[wi].lo + i0) & (wr0[wi].nl - 1);
+              const int g1 = (wr1[wi].lo + i1) & (wr1[wi].nl - 1);
+              const unsigned c = unsigned(L.offset + int64_t(g0) * L.nl + g1);
+              out[wpos + running + __popc(m & lt)] =
+                  (static_cast<unsigned long long>(c) << 32) | __float_as_uint(float(xs[u]));
+            }
+            running += __popc(m);
+          }
+        }
+        if (lane == 0) cnt[row * P.nsb + wsb[wi]] = running;
+        wpos += running;
+        crun += tot;
+      }
+      in0 = a0;
+      in1 = a1;
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBlock) cand_copy_kernel(const __grid_constant__ Plan P, const double* __restrict__ cand,
+                                                           int64_t row0, int64_t rows, const int32_t* __restrict__ cnt,
+                                                           const int64_t* __restrict__ row_ptr, int32_t* col,
+                                                           float* val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t row = warp0; row < rows; row += nwarps) {
+    const int64_t unit = row0 + row;
+    const SubBand& S = P.sb[find_subband(P, unit)];
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(
+        cand + S.cand_off + (unit - (S.offset > row0 ? S.offset : row0)) * S.cand_slot);
+    const int32_t* c = cnt + row * P.nsb;
+    const int64_t base = row_ptr[row];
+    int64_t spos = 0;
+    for (int s = 1; s <= S.steps; ++s) {   // emission order of the compaction
+      const int base_sb = 1 + (P.J - s) * (D == 2 ? 3 : 1);
+      const int nw = (D == 2 ? 3 : 1) + (s == P.J);
+      for (int wi = 0; wi < nw; ++wi) {
+        const int sb = wi < (D == 2 ? 3 : 1) ? base_sb + wi : 0;
+        const int want = c[sb];
+        if (want > 0) {
+          int64_t dst = base;
+          for (int q = 0; q < sb; ++q) dst += c[q];
+          for (int k = lane; k < want; k += 32) {
+            const unsigned long long e = src[spos + k];
+            col[dst + k] = int32_t(e >> 32);
+            val[dst + k] = __uint_as_float(unsigned(e & 0xffffffffull));
+          }
+        }
+        spos += want;
+      }
+    }
+  }
+}
+
 // ============================================================================= small kernels
 
 __global__ void fill_band_rowptr(int64_t* row_ptr, int64_t rows, int64_t L) {
@@ -1008,6 +1127,24 @@ cudaError_t launch_cand_filter(const Plan& P, const double* cand, int64_t row0, 
     if (P.d == 2) PCWD_CF(double, 2, 1); else PCWD_CF(double, 1, 1);
   }
 #undef PCWD_CF
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cand_compact(const Plan& P, double* cand, int64_t row0, int64_t rows, double tau, int32_t* cnt,
+                                cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const int grid = int(std::min<int64_t>((rows * 32 + kBlock - 1) / kBlock, 148 * 16));
+  if (P.d == 2) cand_compact_kernel<2><<<grid, kBlock, 0, st>>>(P, cand, row0, rows, tau, cnt);
+  else cand_compact_kernel<1><<<grid, kBlock, 0, st>>>(P, cand, row0, rows, tau, cnt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cand_copy(const Plan& P, const double* cand, int64_t row0, int64_t rows, const int32_t* cnt,
+                             const int64_t* row_ptr, int32_t* col, float* val, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const int grid = int(std::min<int64_t>((rows * 32 + kBlock - 1) / kBlock, 148 * 16));
+  if (P.d == 2) cand_copy_kernel<2><<<grid, kBlock, 0, st>>>(P, cand, row0, rows, cnt, row_ptr, col, val);
+  else cand_copy_kernel<1><<<grid, kBlock, 0, st>>>(P, cand, row0, rows, cnt, row_ptr, col, val);
   return cudaGetLastError();
 }
 

@@ -245,6 +245,11 @@ cudaError_t set_unit_smem_attr(size_t bytes);
 cudaError_t launch_fill_band_rowptr(int64_t* row_ptr, int64_t rows, int64_t L, cudaStream_t st);
 cudaError_t launch_fill_full(int64_t* row_ptr, int32_t* col, int64_t rows, int64_t N, cudaStream_t st);
 // THRESHOLD store-then-filter: per unit of the shard, count / write the candidates ≥ tau stored by MODE_TSTORE.
+// THRESHOLD, fp32 values: count + in-place compaction of the kept candidates (one read), then the copy into the CSR
+cudaError_t launch_cand_compact(const Plan& P, double* cand, int64_t row0, int64_t rows, double tau, int32_t* cnt,
+                                cudaStream_t st);
+cudaError_t launch_cand_copy(const Plan& P, const double* cand, int64_t row0, int64_t rows, const int32_t* cnt,
+                             const int64_t* row_ptr, int32_t* col, float* val, cudaStream_t st);
 cudaError_t launch_cand_filter(const Plan& P, const double* cand, int64_t row0, int64_t rows, double tau, int write,
                                int32_t* cnt, const int64_t* row_ptr, int32_t* col, void* val, int out_bytes,
                                cudaStream_t st);

@@ -91,3 +91,17 @@ def test_switch_matches_default_path(tmp_path, case, env):
     assert np.array_equal(got["rp"], ref["rp"]) and np.array_equal(got["col"], ref["col"])
     err = np.linalg.norm(got["val"] - ref["val"]) / np.linalg.norm(ref["val"])
     assert err <= (2e-6 if dtype == "f32" else 1e-13), err
+
+
+@pytest.mark.parametrize("env", [{"PCWD_NO_COMPACT": "1"}, {"PCWD_HYBRID_KB": "0"}, {"PCWD_HYBRID_KB": "200"}],
+                         ids=["no-compact", "no-hybrid", "hybrid-200KB"])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_threshold_filter_and_scratch_switches(tmp_path, env, dtype):
+    """Threshold rule: the two-read filter (count pass + write pass, PCWD_NO_COMPACT) instead of the one-read
+    in-place compaction + copy (fp32 values), and the generic kernel's step ≥ 2 buffers in global instead of shared
+    memory (PCWD_HYBRID_KB=0) or a larger shared part: the same fp64 arithmetic and decisions, so the same CSR bit
+    for bit."""
+    ref = _run(tmp_path, "c2", dtype, {})
+    got = _run(tmp_path, "c2", dtype, env)
+    for k in ("rp", "col", "val"):
+        assert np.array_equal(got[k], ref[k])
