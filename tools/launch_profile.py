@@ -16,7 +16,13 @@ from synth import configs as C  # noqa: E402
 
 name = sys.argv[1]
 dtype = sys.argv[2] if len(sys.argv) > 2 else "f32"
-p = C.get(name)
+if name.startswith("n"):   # the size sweep's operators: n<side> (tools/size_sweep.py)
+    import numpy as np
+    side = int(name[1:])
+    p = C.micro(side, 2, 4, side.bit_length() - 3, 10, 18, 60 + side, retain="band", band_L=128)
+    p.u, p.v = np.ascontiguousarray(p.u), np.ascontiguousarray(p.v)
+else:
+    p = C.get(name)
 dec = Decomposition(Spec(p.d, p.n, p.J, p.h, torch.from_numpy(p.u).cuda(), torch.from_numpy(p.v).cuda(), dtype=dtype,
                          retain=p.retain, tau_rel=p.tau_rel, band_L=p.band_L))
 

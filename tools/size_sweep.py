@@ -12,7 +12,7 @@ import torch  # noqa: E402
 from paper_2005_09870_b200 import Decomposition, Spec  # noqa: E402
 from synth import configs as C  # noqa: E402
 
-for n, J in ((256, 6), (512, 7), (1024, 8), (2048, 9)):
+for n, J in ((128, 5), (256, 6), (512, 7), (1024, 8), (2048, 9), (4096, 10)):   # the paper's range
     p = C.micro(n, 2, 4, J, 10, 18, 60 + n, retain="band", band_L=128)
     dec = Decomposition(Spec(p.d, p.n, p.J, p.h, torch.from_numpy(np.ascontiguousarray(p.u)).cuda(),
                              torch.from_numpy(np.ascontiguousarray(p.v)).cuda(), dtype="f32", retain="band",
