@@ -53,6 +53,11 @@ struct Handle {
   int4* stencil_d = nullptr;
   int4* box_d = nullptr;
   FGeom* fgeom_d = nullptr;
+  SepClass* sepc_d = nullptr;   // separable direct path tables (plan.cpp build_sep)
+  SepRun* seprun_d = nullptr;
+  SepPart* seppart_d = nullptr;
+  int* septask_d = nullptr;
+  void* atoms_d = nullptr;
   void* vpad_d = nullptr;   // periodically padded v (fine path TMA source)
   void* vwrap_d = nullptr;  // v extended periodically by kt_pr rows / kt_pc columns (tiled k-sum TMA source)
   CUtensorMap* amaps_d = nullptr;   // TMA maps of the batched approximation steps
@@ -132,7 +137,7 @@ bool is_device_ptr(const void* p) {
 }
 
 void free_all(Handle* h) {
-  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->vpad_d, h->vwrap_d, h->amaps_d, h->gscratch, h->bscratch,
+  void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->sepc_d, h->seprun_d, h->seppart_d, h->septask_d, h->atoms_d, h->vpad_d, h->vwrap_d, h->amaps_d, h->gscratch, h->bscratch,
                   h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->cand, h->ustage, h->vstage, h->flag_d, h->fbuf, h->rpT, h->rowT, h->valT, h->twork};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -350,6 +355,11 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
       F.T = h->T_d;
       F.stencil = h->stencil_d;
       F.geom = h->fgeom_d;
+      F.sepc = h->sepc_d;
+      F.seprun = h->seprun_d;
+      F.seppart = h->seppart_d;
+      F.septask = h->septask_d;
+      F.atoms = h->atoms_d;
       F.row0 = h->hp.row0;
       F.col = h->col;
       F.val = h->val;
@@ -625,6 +635,24 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     CKB(dalloc(&h->fgeom_d, h->hp.fgeom.size() * sizeof(FGeom)));
     CKB(cudaMemcpy(h->fgeom_d, h->hp.fgeom.data(), h->hp.fgeom.size() * sizeof(FGeom), cudaMemcpyHostToDevice));
   }
+  if (!h->hp.sepcls.empty() && !h->hp.seprun.empty()) {
+    const HostPlan& hp = h->hp;
+    auto up = [&](auto** dst, const auto& vec) -> cudaError_t {
+      cudaError_t e = dalloc(dst, vec.size() * sizeof(vec[0]));
+      if (e != cudaSuccess) return e;
+      return cudaMemcpy(*dst, vec.data(), vec.size() * sizeof(vec[0]), cudaMemcpyHostToDevice);
+    };
+    CKB(up(&h->sepc_d, hp.sepcls));
+    CKB(up(&h->seprun_d, hp.seprun));
+    CKB(up(&h->seppart_d, hp.seppart));
+    CKB(up(&h->septask_d, hp.septask));
+    if (rb == 8) {
+      CKB(up(reinterpret_cast<double**>(&h->atoms_d), hp.atoms));
+    } else {
+      std::vector<float> af(hp.atoms.begin(), hp.atoms.end());
+      CKB(up(reinterpret_cast<float**>(&h->atoms_d), af));
+    }
+  }
   int64_t gmax = 0;
   h->conc = P.retain == PCWD_RETAIN_BAND && !getenv("PCWD_COARSE_SERIAL");
   auto add_generic = [&](int64_t u0, int64_t u1, int64_t scr) {
@@ -729,7 +757,16 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         // staging ring depth: the ring may use the whole dynamic smem (R, Yt and D regions are all idle
         // during the k-sum); as many buffers as fit, up to the kernel's NST
         // Yt slots (pass-A output of any step, then the gather stage) are max(YSZ, YSZ2) apart
-        const int64_t YSL = std::max<int64_t>(YSZ, YSZ2);
+        int64_t YSL = std::max<int64_t>(YSZ, YSZ2);
+        // separable direct a3 + a4 (plan.cpp build_sep): Q (R0 rows × QS) then the gather stage in each slot
+        const bool sep = h->hp.sep_ok[lev] && !getenv("PCWD_NO_SEP");
+        int QS = 0;
+        int64_t QSZ = 0;
+        if (sep) {
+          QS = h->hp.sep_nq[lev] | 1;
+          QSZ = (int64_t(R0) * QS + VW - 1) / VW * VW;
+          YSL = std::max<int64_t>(YSL, QSZ + 2 * int64_t(P.band_Lpad) + VW);
+        }
         const int64_t regS = SLK + std::max<int64_t>(fc.CG * YSL, fc.GU * YSZ2) + SLK;
         const int64_t regD = regR + regS;
         int64_t total_el = regD + fc.GU * DS;
@@ -760,6 +797,9 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           A.regS = regR; A.regD = regD;
           A.TSZ = TSZ; A.VSZ = VSZ;
           A.nst = nst;
+          A.sep = sep ? 1 : 0;
+          A.QS = QS;
+          A.QSZ = int(QSZ);
           // partner levels computed directly from the last cascade approximation: PCWD_FINE_DIRECT = "d1,d2,d3"
           // per fine level (2 = one step of 2δ × 2δ taps plus one composite step, 1 = the 2δ × 2δ step only)
           {

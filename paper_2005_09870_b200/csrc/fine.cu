@@ -135,6 +135,83 @@ __device__ __forceinline__ void filt8hg(const Plan& P, const Real* __restrict__ 
   }
 }
 
+// a3 + a4 by the separable direct form (geom.h "sep"): for each unit of the round (CG at a time, one thread
+// group each), stage 1 filters the needed rows of R with the distinct column atoms of the stencil into Q,
+// stage 2 contracts each partner's row atom with its Q column, then the row is written in CSR column order.
+// Rwin: window (0, 0) of unit 0 (rows of stride RS, zero columns on both sides of every row).
+template <typename Real, int GU, int CG>
+__device__ __forceinline__ void sep_units(const Plan& P, const FineArgs& A, const SubBand& S, int p0, int p1f,
+                                          int64_t ufirst, const Real* Rwin, Real* Ybase, int slot, int gt,
+                                          int* wflag) {
+  constexpr int GT = kFT / CG;
+  const Real* __restrict__ atoms = reinterpret_cast<const Real*>(A.atoms);
+  const int lev = S.level;
+  const int4* st = A.stencil + S.stencil_off;
+  const int L = P.band_L;
+  Real* outv = reinterpret_cast<Real*>(A.val);
+  for (int w0 = 0; w0 < GU; w0 += CG) {
+    const int u = w0 + slot;
+    const int p1 = p1f + u;
+    const int cls0 = p0 & (S.fg_m - 1), cls1 = p1 & (S.fg_m - 1);
+    const SepClass C = A.sepc[S.fg_off + cls0 * S.fg_m + cls1];
+    const Real* X = Rwin + u * A.RSZ;
+    Real* Q = Ybase + slot * A.YSZ;
+    Real* sv = Q + A.QSZ;
+    int* sc = reinterpret_cast<int*>(sv + P.band_Lpad);
+    if (gt == 0) wflag[slot] = 0;
+    // stage 1: Q[row][q + b] = Σ_i W[i] · R[row][c + step·b + i]
+    for (int t = gt; t < C.ntask; t += GT) {
+      const int tk = __ldg(A.septask + C.task_off + t);
+      const SepRun R = A.seprun[C.run_off + (tk >> 16)];
+      const int row = tk & 0xffff;
+      const Real* x = X + row * A.RS + R.c;
+      const Real* w = atoms + R.tofs;
+      for (int b = 0; b < R.B; ++b) {
+        Real acc = Real(0);
+        const Real* xb = x + R.step * b;
+        for (int i = 0; i < R.len; ++i) acc = ffma_(__ldg(w + i), xb[i], acc);
+        Q[row * A.QS + R.q + b] = acc;
+      }
+    }
+    bar_group(1 + slot, GT);
+    // stage 2: Θ[μ][λ_jj] = Σ_i W[fo + i] · Q[fs + i][g]; CSR columns in stencil order
+    const int64_t base = (ufirst + u - A.row0) * L;
+    int wrap = 0;
+    for (int jj = gt; jj < L; jj += GT) {
+      const SepPart pp = A.seppart[C.part_off + jj];
+      Real x = Real(0);
+      if (pp.g >= 0) {
+        const Real* q = Q + pp.fs * A.QS + pp.g;
+        const Real* w = atoms + pp.fo;
+        for (int i = 0; i < pp.fl; ++i) x = ffma_(__ldg(w + i), q[i * A.QS], x);
+      }
+      const int4 e = st[jj];
+      const SubBand& Lb = P.sb[e.x];
+      const int D = e.w - lev;
+      const int b0 = D == 0 ? p0 : (D < 0 ? (p0 << -D) : (p0 >> D));
+      const int b1 = D == 0 ? p1 : (D < 0 ? (p1 << -D) : (p1 >> D));
+      const int l0 = b0 + e.y, l1 = b1 + e.z;
+      wrap |= (l0 < 0) | (l0 >= Lb.nl) | (l1 < 0) | (l1 >= Lb.nl);
+      sv[jj] = x;
+      sc[jj] = int(Lb.offset + int64_t(l0 & (Lb.nl - 1)) * Lb.nl + (l1 & (Lb.nl - 1)));
+    }
+    if (wrap) wflag[slot] = 1;
+    bar_group(1 + slot, GT);
+    wrap = wflag[slot];
+    for (int jj = gt; jj < L; jj += GT) {
+      const int c = sc[jj];
+      int rank = jj;
+      if (wrap) {
+        rank = 0;
+        for (int i = 0; i < L; ++i) rank += sc[i] < c;
+      }
+      A.col[base + rank] = c;
+      outv[base + rank] = sv[jj];
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 // Shared-memory layout (elements of Real), all offsets from the dynamic smem base:
@@ -310,6 +387,10 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     if (A.dbg && tid == 0) { const long long t = clock64(); t_ksum += t - t_last; t_last = t; }
     // ------------------------------------------------------------------ a3: cascade of unit u
     // (CG units at a time, one thread group each; Yt, D and the step descriptors are per group slot)
+    if (A.sep) {
+      sep_units<Real, GU, CG>(P, A, S, p0, p1f, ufirst, Rbase + roff, Ybase, slot, gt, wflag);
+      continue;
+    }
     for (int w0 = 0; w0 < GU; w0 += CG) {
     const int u = w0 + slot;
     const int p1 = p1f + u;

@@ -141,4 +141,35 @@ PCWD_HD void compute_fgeom(const Plan& P, const SubBand& S, int p0, int p1, BoxF
 // Translate a class record computed at position q to position p (p ≡ q mod 2^{steps-ℓ} per axis).
 PCWD_HD int g_shift(int dp, int lev, int s) { return s <= lev ? dp * (1 << (lev - s)) : (dp >> (s - lev)); }
 
+// ---------------------------------------------------------------------------------------------------
+// Separable direct path of the fine kernel ("sep").  The 2-D basis is a tensor product
+// (P:93-127): the analysis atom of coefficient λ = (s, e0, e1, l0, l1) is
+//     ψ_λ(y0, y1) = w_{s,e0,l0}(y0) · w_{s,e1,l1}(y1),   w_{s,e,l}(y) = W_{s,e}(y − 2^s l),
+// with the 1-D base atoms of the analysis step of common.h:
+//     W_{1,e}(y) = f_e[y − o_e],   W_{s,e}(y) = Σ_j f_e[j] · W_{s−1,0}(y − 2^{s−1}(o_e + j)),
+// supported on [2^{s−1} o_e, 2^{s−1} o_e + (2^s − 1)(2δ − 1) + 1).  Entry Θ[μ][λ] = ⟨R_μ, ψ_λ⟩ over μ's
+// window therefore factorises:  Q[y0][g] = Σ_{y1} R_μ(y0, y1) w_g(y1)  (stage 1, one column per distinct
+// column atom g of the stencil), then  Θ[μ][λ] = Σ_{y0} w_{s,e0,l0}(y0) Q[y0][g(λ)]  (stage 2).
+// Every position is relative to the unit's window; for a unit of class q = p mod 2^{steps−ℓ} the whole
+// record is a translate of its class representative's (see g_shift), so one record per class suffices.
+struct SepRun {            // B column atoms of one (level, e1) at consecutive positions (stage 1)
+  int tofs;                // first tap in the atom table (clipped runs: the first tap inside the window)
+  int c;                   // window column of the first atom's first tap (may be < 0: zero row pads)
+  int len;                 // taps per atom
+  int step;                // 2^s: column shift between consecutive atoms
+  int B;                   // atoms in the run
+  int q;                   // Q column of the first atom
+  int r0, r1;              // Q rows the stencil reads: [r0, r1)
+};
+struct SepPart {           // one stencil entry (stage 2): Θ = Σ_i atoms[fo + i] · Q[fs + i][g]
+  int g;                   // Q column (-1: the atom misses the window, Θ = 0)
+  int fs, fo, fl;          // first row, first tap, taps (row atom clipped to the window)
+};
+struct SepClass {
+  int run_off, nrun;       // runs of this class
+  int task_off, ntask;     // stage-1 tasks (run << 16 | row), grouped by run
+  int part_off;            // band_L partner records
+  int nq;                  // Q columns
+};
+
 }  // namespace pcwd

@@ -52,6 +52,9 @@ cudaError_t launch_band_tile(const Plan& P, const TileArgs& A, int real_bytes, i
                              cudaStream_t st);
 
 struct FGeom;
+struct SepClass;
+struct SepRun;
+struct SepPart;
 
 struct FineArgs {
   CUtensorMap tmV;          // TMA map of the periodically padded v (3-D: x, y, k), box VS × R0 × 1
@@ -77,6 +80,14 @@ struct FineArgs {
   int direct;               // partner levels (0, 1 or 2, the coarsest ones) computed directly in the gather
   unsigned long long* dbg;  // optional phase clock counters (PCWD_DEBUG_PHASES): k-sum, cascade
   int dbg_flags;            // debug experiments (PCWD_FINE_DBG, results invalid): 2 = no cascade, 4 = step 1 only
+  // separable direct a3 + a4 (geom.h "sep"; sep = 0: the cascade)
+  int sep;
+  int QS, QSZ;              // Q row stride, Q region size (elements); the gather stage follows Q in the slot
+  const SepClass* sepc;     // indexed like geom
+  const SepRun* seprun;
+  const SepPart* seppart;
+  const int* septask;
+  const void* atoms;        // base atoms W_{s,e} in the compute type
 };
 
 // Template configuration of the fine kernel for (real_bytes, level): units per round GU, template

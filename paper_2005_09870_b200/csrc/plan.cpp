@@ -190,6 +190,134 @@ static void build_stencil(const Plan& P, int s_mu, int L, std::vector<Stencil>* 
   }
 }
 
+// Separable direct path of the fine kernel (geom.h): base atoms W_{s,e} and, per fine sub-band and class,
+// the stage-1 runs over the distinct column atoms and the stage-2 partner records.  A level is marked usable
+// only if every one of its class records could be built (no atom wraps onto the window, partner levels
+// ≤ sep_smax).
+static void build_sep(HostPlan* hp) {
+  Plan& P = hp->P;
+  const int L2 = P.L2, n = P.n, J = P.J, ns = P.nsb;
+  hp->atoms.clear();
+  hp->sepcls.assign(hp->fgeom.size(), SepClass{});
+  hp->seprun.clear();
+  hp->seppart.clear();
+  hp->septask.clear();
+  for (int l = 0; l <= kMaxJ; ++l) hp->sep_ok[l] = hp->sep_nq[l] = 0;
+  if (P.retain != PCWD_RETAIN_BAND || P.d != 2 || hp->fgeom.empty()) return;
+  const int smax = std::min(J, 6);
+  hp->sep_smax = smax;
+  std::vector<double> prev;   // W_{s-1,0}
+  for (int s = 1; s <= smax; ++s) {
+    const int len = ((1 << s) - 1) * (L2 - 1) + 1;
+    hp->atom_len[s] = len;
+    std::vector<double> w0;
+    for (int e = 0; e < 2; ++e) {
+      std::vector<double> w(len, 0.0);
+      if (s == 1) {
+        for (int j = 0; j < L2; ++j) w[j] = P.td[e][j];
+      } else {
+        const int dil = 1 << (s - 1);
+        for (int j = 0; j < L2; ++j)
+          for (size_t i = 0; i < prev.size(); ++i) w[dil * j + i] += P.td[e][j] * prev[i];
+      }
+      hp->atom_off[s][e] = int(hp->atoms.size());
+      hp->atoms.insert(hp->atoms.end(), w.begin(), w.end());
+      if (e == 0) w0 = w;
+    }
+    prev = w0;
+  }
+  auto sstart = [&](int s, int e) { return e ? (1 << (s - 1)) * (2 - L2) : 0; };   // support start of W_{s,e}
+  const int PADC = L2;    // zero columns guaranteed on both sides of every R row (fine kernel layout)
+  const int BMAX = 8;
+  int ok_lev[kMaxJ + 1], seen[kMaxJ + 1];
+  for (int l = 0; l <= kMaxJ; ++l) ok_lev[l] = 1, seen[l] = 0;
+  for (int sbi = 0; sbi < ns; ++sbi) {
+    const SubBand& S = P.sb[sbi];
+    if (S.fg_m <= 0) continue;
+    const int lev = S.level, M = S.fg_m;
+    seen[lev] = 1;
+    const int R0 = S.tW[0], R1 = S.tW[1];
+    for (int q0 = 0; q0 < M && ok_lev[lev]; ++q0)
+      for (int q1 = 0; q1 < M && ok_lev[lev]; ++q1) {
+        SepClass& C = hp->sepcls[S.fg_off + q0 * M + q1];
+        const int w0 = (q0 << lev) + S.tSu[0], w1 = (q1 << lev) + S.tSu[1];
+        struct Ent { int sp, e0, e1, l0, l1; };
+        std::vector<Ent> ents(P.band_L);
+        std::vector<std::tuple<int, int, int>> keys;   // distinct column atoms (s, e1, l1)
+        for (int jj = 0; jj < P.band_L; ++jj) {
+          const Stencil& st = hp->stencil[S.stencil_off + jj];
+          const SubBand& T = P.sb[st.sb];
+          const int sp = T.level, D = sp - lev;
+          if (sp > smax || hp->atom_len[sp] + std::max(R0, R1) > n) { ok_lev[lev] = 0; break; }
+          const int b0 = D == 0 ? q0 : (D < 0 ? (q0 << -D) : (q0 >> D));
+          const int b1 = D == 0 ? q1 : (D < 0 ? (q1 << -D) : (q1 >> D));
+          ents[jj] = Ent{sp, T.e0, T.e1, b0 + st.o0, b1 + st.o1};
+          keys.emplace_back(sp, T.e1, b1 + st.o1);
+        }
+        if (!ok_lev[lev]) break;
+        std::sort(keys.begin(), keys.end());
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        // runs and Q columns
+        std::vector<int> qcol(keys.size(), -1), qrun(keys.size(), -1);
+        std::vector<SepRun> runs;
+        int nq = 0;
+        bool open = false;
+        int last_sp = -1, last_e = -1, last_l = 0;
+        for (size_t k = 0; k < keys.size(); ++k) {
+          const int sp = std::get<0>(keys[k]), e1 = std::get<1>(keys[k]), l1 = std::get<2>(keys[k]);
+          const int len = hp->atom_len[sp];
+          const int st1 = l1 * (1 << sp) + sstart(sp, e1) - w1;
+          const bool inside = st1 >= -PADC && st1 + len <= R1 + PADC;
+          if (inside) {
+            if (open && sp == last_sp && e1 == last_e && l1 == last_l + 1 && runs.back().B < BMAX) {
+              runs.back().B++;
+            } else {
+              runs.push_back(SepRun{hp->atom_off[sp][e1], st1, len, 1 << sp, 1, nq, 1 << 30, -(1 << 30)});
+              open = true;
+            }
+            last_sp = sp; last_e = e1; last_l = l1;
+          } else {
+            open = false;
+            const int ta = std::max(0, -st1), tb = std::min(len, R1 - st1);
+            if (tb <= ta) continue;   // the atom misses the window: its partners are 0
+            runs.push_back(SepRun{hp->atom_off[sp][e1] + ta, st1 + ta, tb - ta, 1 << sp, 1, nq, 1 << 30, -(1 << 30)});
+          }
+          qcol[k] = nq++;
+          qrun[k] = int(runs.size()) - 1;
+        }
+        // partners: row atoms clipped to the window; rows each run must provide
+        C.part_off = int(hp->seppart.size());
+        for (int jj = 0; jj < P.band_L; ++jj) {
+          const Ent& E = ents[jj];
+          const size_t k = std::lower_bound(keys.begin(), keys.end(), std::make_tuple(E.sp, E.e1, E.l1)) - keys.begin();
+          const int len = hp->atom_len[E.sp];
+          const int st0 = E.l0 * (1 << E.sp) + sstart(E.sp, E.e0) - w0;
+          const int ta = std::max(0, -st0), tb = std::min(len, R0 - st0);
+          SepPart pp{-1, 0, 0, 0};
+          if (qcol[k] >= 0 && tb > ta) {
+            pp = SepPart{qcol[k], st0 + ta, hp->atom_off[E.sp][E.e0] + ta, tb - ta};
+            SepRun& r = runs[qrun[k]];
+            r.r0 = std::min(r.r0, st0 + ta);
+            r.r1 = std::max(r.r1, st0 + tb);
+          }
+          hp->seppart.push_back(pp);
+        }
+        C.run_off = int(hp->seprun.size());
+        C.nrun = int(runs.size());
+        C.task_off = int(hp->septask.size());
+        for (size_t r = 0; r < runs.size(); ++r) {
+          if (runs[r].r1 <= runs[r].r0) runs[r].r0 = runs[r].r1 = 0;
+          for (int row = runs[r].r0; row < runs[r].r1; ++row) hp->septask.push_back(int(r) << 16 | row);
+          hp->seprun.push_back(runs[r]);
+        }
+        C.ntask = int(hp->septask.size()) - C.task_off;
+        C.nq = nq;
+        hp->sep_nq[lev] = std::max(hp->sep_nq[lev], nq);
+      }
+  }
+  for (int l = 1; l <= kMaxJ; ++l) hp->sep_ok[l] = seen[l] && ok_lev[l];
+}
+
 int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::string* msg) {
   int rc = validate_desc(d, msg);
   if (rc) return rc;
@@ -438,6 +566,7 @@ int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::stri
         hp->fgeom.push_back(g);
       }
   }
+  build_sep(hp);
 
   // shard: contiguous unit ranges (Λ order) with equal estimated time.  A unit's time is its algorithmic
   // FMA count times a per-path weight: time per algorithmic FMA of each level's kernel path relative to

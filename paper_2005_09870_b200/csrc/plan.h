@@ -31,6 +31,17 @@ struct HostPlan {
   double tmpl_fma_level[kMaxJ + 1] = {};   // template FMAs of each level's à-trous step
   std::vector<FGeom> fgeom;       // BAND, fine levels: class geometry records (SubBand::fg_off / fg_m)
   int64_t cand_total = 0;         // THRESHOLD: candidate slots of the shard (store-then-filter), fp64 values
+  // separable direct path of the fine kernel (geom.h SepRun / SepPart / SepClass), records indexed like fgeom
+  std::vector<double> atoms;      // base atoms W_{s,e}, s = 1..sep_smax, e = 0, 1 (fp64; cast on upload)
+  int atom_off[kMaxJ + 1][2] = {};
+  int atom_len[kMaxJ + 1] = {};
+  int sep_smax = 0;
+  std::vector<SepClass> sepcls;   // one per fgeom record (valid where SubBand::fg_m > 0 and sep_ok[level])
+  std::vector<SepRun> seprun;
+  std::vector<SepPart> seppart;
+  std::vector<int> septask;
+  int sep_ok[kMaxJ + 1] = {};     // level ℓ: every class record of every sub-band built
+  int sep_nq[kMaxJ + 1] = {};     // max Q columns over the level's classes
 };
 
 // Returns a pcwd_status; msg receives the reason on error.
