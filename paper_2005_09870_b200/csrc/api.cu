@@ -646,11 +646,17 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
     CKB(up(&h->seprun_d, hp.seprun));
     CKB(up(&h->seppart_d, hp.seppart));
     CKB(up(&h->septask_d, hp.septask));
-    if (rb == 8) {
-      CKB(up(reinterpret_cast<double**>(&h->atoms_d), hp.atoms));
-    } else {
-      std::vector<float> af(hp.atoms.begin(), hp.atoms.end());
-      CKB(up(reinterpret_cast<float**>(&h->atoms_d), af));
+    {   // tap table in the kernel's shared-memory layout (geom.h sep_toff), compute type
+      std::vector<double> tab(sep_ttot(P.L2), 0.0);
+      for (int s2 = 1; s2 <= hp.sep_smax; ++s2)
+        for (int e2 = 0; e2 < 2; ++e2)
+          for (int i = 0; i < hp.atom_len[s2]; ++i) tab[sep_toff(s2, e2, P.L2) + i] = hp.atoms[hp.atom_off[s2][e2] + i];
+      if (rb == 8) {
+        CKB(up(reinterpret_cast<double**>(&h->atoms_d), tab));
+      } else {
+        std::vector<float> tf(tab.begin(), tab.end());
+        CKB(up(reinterpret_cast<float**>(&h->atoms_d), tf));
+      }
     }
   }
   int64_t gmax = 0;
@@ -738,7 +744,11 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         auto pair_stride = [&](int w) { int x = (w + 1) / 2 * 2; if ((x / 2) % 2 == 0) x += 2; return x; };
         int roffmax = 0;   // R rows are shifted by one column when a window starts at an odd column
         for (int q = s; q < e; ++q) roffmax |= P.sb[q].tSu[1] & 1;
-        const int RS = pair_stride(R1 + roffmax + P.L2 + 2);
+        // separable direct a3 + a4 (plan.cpp build_sep): odd R row stride (a warp's lanes read 32 rows of one column)
+        // PCWD_SEP: bit mask over fine levels 1..3 (default 0: the cascade, measured faster at c5 — DESIGN.md §6)
+        static const int sep_mask = getenv("PCWD_SEP") ? atoi(getenv("PCWD_SEP")) : 0;
+        const bool sep = h->hp.sep_ok[lev] && ((sep_mask >> (lev - 1)) & 1);
+        const int RS = sep ? ((R1 + std::max(kSepPad, roffmax + P.L2 + 2)) | 1) : pair_stride(R1 + roffmax + P.L2 + 2);
         const int zmaxT = (SH - 1) + SH * fc.GZ * (NZB - 1) + SH * (fc.GZ - 1);
         const int zmaxV = zmaxT + SH * (fc.GU - 1);
         const int TS = odd_stride(std::max(S0.tRS, zmaxT + 1));
@@ -758,25 +768,27 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         // during the k-sum); as many buffers as fit, up to the kernel's NST
         // Yt slots (pass-A output of any step, then the gather stage) are max(YSZ, YSZ2) apart
         int64_t YSL = std::max<int64_t>(YSZ, YSZ2);
-        // separable direct a3 + a4 (plan.cpp build_sep): Q (R0 rows × QS) then the gather stage in each slot
-        const bool sep = h->hp.sep_ok[lev] && !getenv("PCWD_NO_SEP");
+        // separable path: Q (R0 rows × QS) then the gather stage in each slot
         int QS = 0;
         int64_t QSZ = 0;
         if (sep) {
-          QS = h->hp.sep_nq[lev] | 1;
-          QSZ = (int64_t(R0) * QS + VW - 1) / VW * VW;
-          YSL = std::max<int64_t>(YSL, QSZ + 2 * int64_t(P.band_Lpad) + VW);
+          QS = R0 | 1;   // Q is column-major: column stride (rows)
+          QSZ = (int64_t(h->hp.sep_nq[lev]) * QS + VW - 1) / VW * VW;
+          // Q, the gather stage (values, columns) and the class's stage-1 runs; no Yt / D buffers (cascade only)
+          YSL = QSZ + (2 * int64_t(P.band_Lpad) + int64_t(h->hp.sep_nrun[lev]) * int64_t(sizeof(SepRun)) / rb + VW - 1) / VW * VW;
         }
-        const int64_t regS = SLK + std::max<int64_t>(fc.CG * YSL, fc.GU * YSZ2) + SLK;
+        const int64_t regS = SLK + (sep ? fc.CG * YSL : std::max<int64_t>(fc.CG * YSL, fc.GU * YSZ2)) + SLK;
         const int64_t regD = regR + regS;
-        int64_t total_el = regD + fc.GU * DS;
+        int64_t total_el = regD + (sep ? 0 : fc.GU * DS);
         int nst = int(std::min<int64_t>(fc.NST, (total_el - SLK - al) / (TSZ + VSZ)));
         if (nst < 1) {   // enlarge the allocation to hold one staging buffer
           total_el = SLK + al + (TSZ + VSZ);
           nst = 1;
         }
         const int64_t stg = int64_t(nst) * (TSZ + VSZ) + al;
-        const size_t smem = size_t(std::max<int64_t>(total_el, regD + fc.GU * DS)) * rb;
+        const int64_t elA = (std::max<int64_t>(total_el, regD + (sep ? 0 : fc.GU * DS)) + 3) & ~int64_t(3);   // atom taps (sep)
+        const int ntap = sep ? sep_ttot(P.L2) : 0;
+        const size_t smem = size_t(elA + ntap) * rb;
         ok = ok && smem + 4096 <= size_t(smem_optin > 0 ? smem_optin : 48 * 1024);
         int64_t a0 = (u0 + fc.GU - 1) / fc.GU * fc.GU, a1 = u1 / fc.GU * fc.GU;
         if (getenv("PCWD_DEBUG_PLAN"))
@@ -798,6 +810,8 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
           A.TSZ = TSZ; A.VSZ = VSZ;
           A.nst = nst;
           A.sep = sep ? 1 : 0;
+          A.regA = elA;
+          A.ntap = ntap;
           A.QS = QS;
           A.QSZ = int(QSZ);
           // partner levels computed directly from the last cascade approximation: PCWD_FINE_DIRECT = "d1,d2,d3"

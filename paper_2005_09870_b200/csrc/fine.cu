@@ -135,19 +135,96 @@ __device__ __forceinline__ void filt8hg(const Plan& P, const Real* __restrict__ 
   }
 }
 
-// a3 + a4 by the separable direct form (geom.h "sep"): for each unit of the round (CG at a time, one thread
-// group each), stage 1 filters the needed rows of R with the distinct column atoms of the stencil into Q,
-// stage 2 contracts each partner's row atom with its Q column, then the row is written in CSR column order.
-// Rwin: window (0, 0) of unit 0 (rows of stride RS, zero columns on both sides of every row).
-template <typename Real, int GU, int CG>
+// ---- separable direct a3 + a4 (geom.h "sep")
+// BM atoms W (taps in shared memory, zero-padded to whole blocks of 2^S) at offsets c + 2^S b of a contiguous
+// line x:  out[b·ostr] = Σ_i W[i] x[c + 2^S b + i]  for b < B ≤ BM.  MASK: entries outside [lo, hi) read 0
+// (predicated loads); otherwise the caller guarantees zeros (or, beyond the B real atoms, finite values) there.
+// Register window over the shift: for each residue r < 2^S the BM inputs x[c + 2^S j + r], j = k .. k + BM − 1,
+// are held in registers (slot j mod BM); a block of 2^S taps costs 2^S tap loads (vectorised), 2^S new inputs
+// and 2^S·BM FMAs.  Blocks are unrolled (compile-time count from 2δ), so the window rotates without moves.
+template <typename Real, int L2, int S, int BM, bool MASK>
+__device__ __noinline__ void sep_slide(const Real* __restrict__ x, int c, int lo, int hi, const Real* __restrict__ taps,
+                                       int B, Real* __restrict__ out, int ostr) {
+  constexpr int ST = 1 << S, NB = sep_atom_blk(S, L2);
+  Real xr[ST][BM];
+  Real acc[BM];
+  const Real* xc = x + c;
+  const unsigned span = unsigned(hi - lo);
+  auto ld = [&](int j) -> Real {   // x[c + j]
+    if constexpr (MASK) {
+      Real v = Real(0);
+      if (unsigned(c + j - lo) < span) v = xc[j];
+      return v;
+    } else {
+      return xc[j];
+    }
+  };
+#pragma unroll
+  for (int b = 0; b < BM; ++b) acc[b] = Real(0);
+#pragma unroll
+  for (int r = 0; r < ST; ++r)
+#pragma unroll
+    for (int b = 0; b < BM; ++b) xr[r][b] = ld(r + ST * b);
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    Real w[ST];
+    if constexpr (ST * sizeof(Real) >= 16) {
+      using V = typename std::conditional<sizeof(Real) == 4, float4, double2>::type;
+      constexpr int VW = 16 / sizeof(Real);
+#pragma unroll
+      for (int v = 0; v < ST / VW; ++v) {
+        const V t = reinterpret_cast<const V*>(taps + k * ST)[v];
+        const Real* tp = reinterpret_cast<const Real*>(&t);
+#pragma unroll
+        for (int q = 0; q < VW; ++q) w[VW * v + q] = tp[q];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < ST; ++r) w[r] = taps[k * ST + r];
+    }
+#pragma unroll
+    for (int r = 0; r < ST; ++r)
+#pragma unroll
+      for (int b = 0; b < BM; ++b) acc[b] = ffma_(w[r], xr[r][(b + k) % BM], acc[b]);
+    if (k + 1 < NB) {   // slot k mod BM (atom 0's entry of this block) takes the entry atom BM − 1 needs next
+#pragma unroll
+      for (int r = 0; r < ST; ++r) xr[r][k % BM] = ld((k + BM) * ST + r);
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < BM; ++b)
+    if (b < B) out[b * ostr] = acc[b];
+}
+
+template <typename Real, int L2, bool MASK>
+__device__ __forceinline__ void sep_dispatch(int s, int B, const Real* x, int c, int lo, int hi, const Real* taps,
+                                             Real* out, int ostr) {
+#define SEP_CASE(SS, BB) \
+  case SS * 16 + BB: sep_slide<Real, L2, SS, BB, MASK>(x, c, lo, hi, taps, B, out, ostr); break;
+  switch (s * 16 + sep_bsel(s, B)) {
+    SEP_CASE(1, 1) SEP_CASE(1, 2) SEP_CASE(1, 3) SEP_CASE(1, 4) SEP_CASE(1, 6) SEP_CASE(1, 8)
+    SEP_CASE(2, 1) SEP_CASE(2, 2) SEP_CASE(2, 3) SEP_CASE(2, 4) SEP_CASE(2, 6) SEP_CASE(2, 8)
+    SEP_CASE(3, 1) SEP_CASE(3, 2) SEP_CASE(3, 3) SEP_CASE(3, 4) SEP_CASE(3, 6)
+    SEP_CASE(4, 1) SEP_CASE(4, 2)
+    SEP_CASE(5, 1)
+    default: break;
+  }
+#undef SEP_CASE
+}
+
+// a3 + a4 by the separable direct form: for each unit of the round (CG at a time, one thread group each),
+// stage 1 filters the needed rows of R with the distinct column atoms of the stencil into Q, stage 2
+// contracts the partners' row atoms with their Q columns, then the row is written in CSR column order.
+// Rwin: window (0, 0) of unit 0 (rows of stride RS); taps: the shared-memory atom table (sep_toff).
+template <typename Real, int L2, int GU, int CG>
 __device__ __forceinline__ void sep_units(const Plan& P, const FineArgs& A, const SubBand& S, int p0, int p1f,
-                                          int64_t ufirst, const Real* Rwin, Real* Ybase, int slot, int gt,
-                                          int* wflag) {
+                                          int64_t ufirst, const Real* Rwin, Real* Ybase, const Real* taps, int slot,
+                                          int gt, int* wflag) {
   constexpr int GT = kFT / CG;
-  const Real* __restrict__ atoms = reinterpret_cast<const Real*>(A.atoms);
   const int lev = S.level;
   const int4* st = A.stencil + S.stencil_off;
   const int L = P.band_L;
+  const int R1 = S.tW[1];
   Real* outv = reinterpret_cast<Real*>(A.val);
   for (int w0 = 0; w0 < GU; w0 += CG) {
     const int u = w0 + slot;
@@ -158,33 +235,39 @@ __device__ __forceinline__ void sep_units(const Plan& P, const FineArgs& A, cons
     Real* Q = Ybase + slot * A.YSZ;
     Real* sv = Q + A.QSZ;
     int* sc = reinterpret_cast<int*>(sv + P.band_Lpad);
+    SepRun* srun = reinterpret_cast<SepRun*>(sc + P.band_Lpad);
     if (gt == 0) wflag[slot] = 0;
-    // stage 1: Q[row][q + b] = Σ_i W[i] · R[row][c + step·b + i]
+    for (int jj = gt; jj < L; jj += GT) sv[jj] = Real(0);   // entries whose atoms miss the window stay 0
+    for (int r = gt; r < C.nrun; r += GT) srun[r] = A.seprun[C.run_off + r];
+    bar_group(1 + slot, GT);
+    // stage 1: Q[q + b][row] = Σ_i W_{s,e}[i] · R[row][c + 2^s b + i]   (Q column-major, column stride QS)
+    // task t = row r0 + (t − tbeg) of run r (runs in shared memory; t grows, so r only advances)
+    int r = 0;
     for (int t = gt; t < C.ntask; t += GT) {
-      const int tk = __ldg(A.septask + C.task_off + t);
-      const SepRun R = A.seprun[C.run_off + (tk >> 16)];
-      const int row = tk & 0xffff;
-      const Real* x = X + row * A.RS + R.c;
-      const Real* w = atoms + R.tofs;
-      for (int b = 0; b < R.B; ++b) {
-        Real acc = Real(0);
-        const Real* xb = x + R.step * b;
-        for (int i = 0; i < R.len; ++i) acc = ffma_(__ldg(w + i), xb[i], acc);
-        Q[row * A.QS + R.q + b] = acc;
+      while (r + 1 < C.nrun && srun[r + 1].tbeg <= t) ++r;
+      const SepRun& R = srun[r];
+      const int row = R.r0 + t - R.tbeg;
+      if constexpr (L2 >= 4) {
+        if (R.mask)
+          sep_dispatch<Real, L2, true>(R.s, R.B, X + row * A.RS, R.c, 0, R1, taps + R.toff, Q + R.q * A.QS + row,
+                                       A.QS);
+        else
+          sep_dispatch<Real, L2, false>(R.s, R.B, X + row * A.RS, R.c, 0, R1, taps + R.toff, Q + R.q * A.QS + row,
+                                        A.QS);
       }
     }
     bar_group(1 + slot, GT);
-    // stage 2: Θ[μ][λ_jj] = Σ_i W[fo + i] · Q[fs + i][g]; CSR columns in stencil order
+    // stage 2: Θ[μ][λ] = Σ_i W_{s,e}[i] · Q[g][fs + 2^s b + i]  (rows outside the computed [r0, r1) read 0)
+    for (int t = gt; t < C.npart; t += GT) {
+      const SepPart R = A.seppart[C.part_off + t];
+      if constexpr (L2 >= 4)
+        sep_dispatch<Real, L2, true>(R.s, R.B, Q + R.g * A.QS, R.fs, R.r0, R.r1, taps + R.toff,
+                                     sv + R.jj, R.jstr);
+    }
+    // CSR columns in stencil order
     const int64_t base = (ufirst + u - A.row0) * L;
     int wrap = 0;
     for (int jj = gt; jj < L; jj += GT) {
-      const SepPart pp = A.seppart[C.part_off + jj];
-      Real x = Real(0);
-      if (pp.g >= 0) {
-        const Real* q = Q + pp.fs * A.QS + pp.g;
-        const Real* w = atoms + pp.fo;
-        for (int i = 0; i < pp.fl; ++i) x = ffma_(__ldg(w + i), q[i * A.QS], x);
-      }
       const int4 e = st[jj];
       const SubBand& Lb = P.sb[e.x];
       const int D = e.w - lev;
@@ -192,7 +275,6 @@ __device__ __forceinline__ void sep_units(const Plan& P, const FineArgs& A, cons
       const int b1 = D == 0 ? p1 : (D < 0 ? (p1 << -D) : (p1 >> D));
       const int l0 = b0 + e.y, l1 = b1 + e.z;
       wrap |= (l0 < 0) | (l0 >= Lb.nl) | (l1 < 0) | (l1 >= Lb.nl);
-      sv[jj] = x;
       sc[jj] = int(Lb.offset + int64_t(l0 & (Lb.nl - 1)) * Lb.nl + (l1 & (Lb.nl - 1)));
     }
     if (wrap) wflag[slot] = 1;
@@ -249,6 +331,10 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
   Real* Sbase = sm + kSlack + (((s_raw + 127u) & ~127u) - s_raw) / sizeof(Real);
   Real* Ybase = sm + A.regS + kSlack;
   for (int i = tid; i < kSlack; i += kFT) sm[i] = Real(0);   // zero rows before R_0 row 0 (left pad)
+  if (A.sep) {   // the separable path's atom taps (geom.h sep_toff layout)
+    const Real* at = reinterpret_cast<const Real*>(A.atoms);
+    for (int i = tid; i < A.ntap; i += kFT) sm[A.regA + i] = at[i];
+  }
   Real* Dbase = sm + A.regD;
   const int64_t rounds = (A.u1 - A.u0) / GU;
   __shared__ __align__(8) unsigned long long fullbar[NST];
@@ -388,7 +474,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     // ------------------------------------------------------------------ a3: cascade of unit u
     // (CG units at a time, one thread group each; Yt, D and the step descriptors are per group slot)
     if (A.sep) {
-      sep_units<Real, GU, CG>(P, A, S, p0, p1f, ufirst, Rbase + roff, Ybase, slot, gt, wflag);
+      sep_units<Real, L2, GU, CG>(P, A, S, p0, p1f, ufirst, Rbase + roff, Ybase, sm + A.regA, slot, gt, wflag);
       continue;
     }
     for (int w0 = 0; w0 < GU; w0 += CG) {

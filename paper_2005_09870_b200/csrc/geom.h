@@ -152,24 +152,50 @@ PCWD_HD int g_shift(int dp, int lev, int s) { return s <= lev ? dp * (1 << (lev 
 // column atom g of the stencil), then  Θ[μ][λ] = Σ_{y0} w_{s,e0,l0}(y0) Q[y0][g(λ)]  (stage 2).
 // Every position is relative to the unit's window; for a unit of class q = p mod 2^{steps−ℓ} the whole
 // record is a translate of its class representative's (see g_shift), so one record per class suffices.
-struct SepRun {            // B column atoms of one (level, e1) at consecutive positions (stage 1)
-  int tofs;                // first tap in the atom table (clipped runs: the first tap inside the window)
-  int c;                   // window column of the first atom's first tap (may be < 0: zero row pads)
-  int len;                 // taps per atom
-  int step;                // 2^s: column shift between consecutive atoms
-  int B;                   // atoms in the run
+struct SepRun {            // stage 1: B column atoms of one (s, e1) at consecutive positions, one row per task
+  int s, e;                // atom level and orientation bit
+  int c;                   // window column of the first atom's tap 0 (unclipped; columns outside [0, R1) read 0)
+  int B;                   // atoms in the run (≤ sep_bmax(s))
   int q;                   // Q column of the first atom
-  int r0, r1;              // Q rows the stencil reads: [r0, r1)
+  int r0, r1;              // Q rows the stage-2 partners read: [r0, r1)
+  int mask;                // 1: some tap read lies beyond the kSepPad zero columns around the row (masked loads)
+  int toff;                // sep_toff(s, e): the atom's taps in the shared-memory table
+  int tbeg;                // first stage-1 task of the run (tasks of a class are its runs' rows, in run order)
 };
-struct SepPart {           // one stencil entry (stage 2): Θ = Σ_i atoms[fo + i] · Q[fs + i][g]
-  int g;                   // Q column (-1: the atom misses the window, Θ = 0)
-  int fs, fo, fl;          // first row, first tap, taps (row atom clipped to the window)
+struct SepPart {           // stage 2: B partners of one Q column g, row atoms W_{s,e} at consecutive positions
+  int g;                   // Q column
+  int s, e;
+  int fs;                  // window row of the first atom's tap 0 (unclipped)
+  int B;
+  int jj, jstr;            // stencil slots jj + b·jstr
+  int r0, r1;              // rows of column g computed by stage 1 (everything else reads 0)
+  int toff;                // sep_toff(s, e)
+  int pad[2];
 };
+constexpr int kSepSmax = 5;
+constexpr int kSepMaxRuns = 64;
+constexpr int kSepPartB = 1;      // partners per stage-2 task (1: balanced over the unit's threads)   // stage-1 runs per class (staged in shared memory per unit)
+constexpr int kSepPad = 12;   // zero columns the fine kernel keeps on both sides of every R row in sep mode
+// register-window widths instantiated per atom level (the run's B is rounded up to the next one)
+PCWD_HD constexpr int sep_bsel(int s, int B) {
+  return B <= 1 ? 1 : B <= 2 ? 2 : (s >= 4 ? 2 : B <= 3 ? 3 : B <= 4 ? 4 : B <= 6 ? 6 : 8);
+}   // atom levels of the separable path (plan.cpp keeps the cascade beyond)
+PCWD_HD constexpr int sep_atom_len(int s, int L2) { return ((1 << s) - 1) * (L2 - 1) + 1; }
+PCWD_HD constexpr int sep_bmax(int s) { return s <= 2 ? 8 : (s == 3 ? 6 : (s == 4 ? 2 : 1)); }   // atoms per run (max)
+// shared-memory tap table: W_{s,e} (s ≤ kSepSmax) at 16-byte aligned offsets, each followed by zeros up to a
+// whole number of 2^s-tap blocks
+PCWD_HD constexpr int sep_atom_blk(int s, int L2) { return (sep_atom_len(s, L2) + (1 << s) - 1) >> s; }
+PCWD_HD constexpr int sep_atom_slot(int s, int L2) { return ((sep_atom_blk(s, L2) << s) + 3) & ~3; }
+PCWD_HD constexpr int sep_toff(int s, int e, int L2) {
+  return s <= 1 ? e * sep_atom_slot(1, L2) : sep_toff(s - 1, 1, L2) + sep_atom_slot(s - 1, L2) + e * sep_atom_slot(s, L2);
+}
+PCWD_HD constexpr int sep_ttot(int L2) { return sep_toff(kSepSmax, 1, L2) + sep_atom_slot(kSepSmax, L2); }
 struct SepClass {
-  int run_off, nrun;       // runs of this class
+  int run_off, nrun;       // stage-1 runs of this class
   int task_off, ntask;     // stage-1 tasks (run << 16 | row), grouped by run
-  int part_off;            // band_L partner records
+  int part_off, npart;     // stage-2 runs
   int nq;                  // Q columns
+  int pad;
 };
 
 }  // namespace pcwd

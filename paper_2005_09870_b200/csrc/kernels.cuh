@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "common.h"
+#include "geom.h"
 
 namespace pcwd {
 
@@ -87,7 +88,9 @@ struct FineArgs {
   const SepRun* seprun;
   const SepPart* seppart;
   const int* septask;
-  const void* atoms;        // base atoms W_{s,e} in the compute type
+  const void* atoms;        // atom tap table (compute type, geom.h sep_toff layout), copied to shared memory
+  int64_t regA;             // its shared-memory offset (elements; beyond everything the staging ring may use)
+  int ntap;                 // its size (elements)
 };
 
 // Template configuration of the fine kernel for (real_bytes, level): units per round GU, template

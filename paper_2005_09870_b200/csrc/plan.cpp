@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <tuple>
@@ -202,9 +204,9 @@ static void build_sep(HostPlan* hp) {
   hp->seprun.clear();
   hp->seppart.clear();
   hp->septask.clear();
-  for (int l = 0; l <= kMaxJ; ++l) hp->sep_ok[l] = hp->sep_nq[l] = 0;
-  if (P.retain != PCWD_RETAIN_BAND || P.d != 2 || hp->fgeom.empty()) return;
-  const int smax = std::min(J, 6);
+  for (int l = 0; l <= kMaxJ; ++l) hp->sep_ok[l] = hp->sep_nq[l] = hp->sep_nrun[l] = 0;
+  if (P.retain != PCWD_RETAIN_BAND || P.d != 2 || hp->fgeom.empty() || (L2 != 4 && L2 != 8 && L2 != 12)) return;
+  const int smax = std::min(J, kSepSmax);
   hp->sep_smax = smax;
   std::vector<double> prev;   // W_{s-1,0}
   for (int s = 1; s <= smax; ++s) {
@@ -228,7 +230,6 @@ static void build_sep(HostPlan* hp) {
   }
   auto sstart = [&](int s, int e) { return e ? (1 << (s - 1)) * (2 - L2) : 0; };   // support start of W_{s,e}
   const int PADC = L2;    // zero columns guaranteed on both sides of every R row (fine kernel layout)
-  const int BMAX = 8;
   int ok_lev[kMaxJ + 1], seen[kMaxJ + 1];
   for (int l = 0; l <= kMaxJ; ++l) ok_lev[l] = 1, seen[l] = 0;
   for (int sbi = 0; sbi < ns; ++sbi) {
@@ -257,7 +258,7 @@ static void build_sep(HostPlan* hp) {
         if (!ok_lev[lev]) break;
         std::sort(keys.begin(), keys.end());
         keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
-        // runs and Q columns
+        // stage-1 runs: consecutive positions of one (s, e1), at most sep_bmax(s) atoms; Q columns in run order
         std::vector<int> qcol(keys.size(), -1), qrun(keys.size(), -1);
         std::vector<SepRun> runs;
         int nq = 0;
@@ -267,55 +268,108 @@ static void build_sep(HostPlan* hp) {
           const int sp = std::get<0>(keys[k]), e1 = std::get<1>(keys[k]), l1 = std::get<2>(keys[k]);
           const int len = hp->atom_len[sp];
           const int st1 = l1 * (1 << sp) + sstart(sp, e1) - w1;
-          const bool inside = st1 >= -PADC && st1 + len <= R1 + PADC;
-          if (inside) {
-            if (open && sp == last_sp && e1 == last_e && l1 == last_l + 1 && runs.back().B < BMAX) {
-              runs.back().B++;
-            } else {
-              runs.push_back(SepRun{hp->atom_off[sp][e1], st1, len, 1 << sp, 1, nq, 1 << 30, -(1 << 30)});
-              open = true;
-            }
-            last_sp = sp; last_e = e1; last_l = l1;
+          if (st1 >= R1 || st1 + len <= 0) { open = false; continue; }   // misses the window: its partners are 0
+          if (open && sp == last_sp && e1 == last_e && l1 == last_l + 1 && runs.back().B < sep_bmax(sp)) {
+            runs.back().B++;
           } else {
-            open = false;
-            const int ta = std::max(0, -st1), tb = std::min(len, R1 - st1);
-            if (tb <= ta) continue;   // the atom misses the window: its partners are 0
-            runs.push_back(SepRun{hp->atom_off[sp][e1] + ta, st1 + ta, tb - ta, 1 << sp, 1, nq, 1 << 30, -(1 << 30)});
+            runs.push_back(SepRun{sp, e1, st1, 1, nq, 1 << 30, -(1 << 30), 0, sep_toff(sp, e1, L2), 0});
+            open = true;
           }
+          last_sp = sp; last_e = e1; last_l = l1;
           qcol[k] = nq++;
           qrun[k] = int(runs.size()) - 1;
         }
-        // partners: row atoms clipped to the window; rows each run must provide
-        C.part_off = int(hp->seppart.size());
+        // partners: Q column, row atom (clipped range → rows stage 1 must provide)
+        struct PR { int g, sp, e0, l0, jj, st0; };
+        std::vector<PR> prs;
         for (int jj = 0; jj < P.band_L; ++jj) {
           const Ent& E = ents[jj];
           const size_t k = std::lower_bound(keys.begin(), keys.end(), std::make_tuple(E.sp, E.e1, E.l1)) - keys.begin();
           const int len = hp->atom_len[E.sp];
           const int st0 = E.l0 * (1 << E.sp) + sstart(E.sp, E.e0) - w0;
           const int ta = std::max(0, -st0), tb = std::min(len, R0 - st0);
-          SepPart pp{-1, 0, 0, 0};
-          if (qcol[k] >= 0 && tb > ta) {
-            pp = SepPart{qcol[k], st0 + ta, hp->atom_off[E.sp][E.e0] + ta, tb - ta};
-            SepRun& r = runs[qrun[k]];
-            r.r0 = std::min(r.r0, st0 + ta);
-            r.r1 = std::max(r.r1, st0 + tb);
-          }
-          hp->seppart.push_back(pp);
+          if (qcol[k] < 0 || tb <= ta) continue;   // Θ entry 0 (the kernel zeroes every slot first)
+          SepRun& r = runs[qrun[k]];
+          r.r0 = std::min(r.r0, st0 + ta);
+          r.r1 = std::max(r.r1, st0 + tb);
+          prs.push_back(PR{qcol[k], E.sp, E.e0, E.l0, jj, st0});
         }
+        // stage-2 runs: partners of one (g, s, e0) at consecutive l0 with a constant slot stride
+        std::sort(prs.begin(), prs.end(), [](const PR& x, const PR& y) {
+          return std::tie(x.g, x.sp, x.e0, x.l0) < std::tie(y.g, y.sp, y.e0, y.l0);
+        });
+        std::vector<SepPart> parts;
+        for (size_t i = 0; i < prs.size(); ++i) {
+          const PR& x = prs[i];
+          if (!parts.empty() && i > 0) {
+            SepPart& pp = parts.back();
+            const PR& y = prs[i - 1];
+            const bool same = x.g == y.g && x.sp == y.sp && x.e0 == y.e0 && x.l0 == y.l0 + 1;
+            const int js = x.jj - y.jj;
+            if (same && pp.B < kSepPartB && (pp.B == 1 || js == pp.jstr)) {
+              pp.jstr = js;
+              pp.B++;
+              continue;
+            }
+          }
+          parts.push_back(SepPart{x.g, x.sp, x.e0, x.st0, 1, x.jj, 0, 0, 0, sep_toff(x.sp, x.e0, L2), {0, 0}});
+        }
+        for (auto& r : runs) {
+          if (r.r1 <= r.r0) r.r0 = r.r1 = 0;
+          // columns read by the register window (incl. the rounded-up atoms) vs the zero pads around the row
+          const int end = r.c + (sep_atom_blk(r.s, L2) << r.s) + (sep_bsel(r.s, r.B) - 1) * (1 << r.s);
+          r.mask = (r.c < -kSepPad || end > R1 + kSepPad) ? 1 : 0;
+        }
+        std::vector<int> colrun(nq, 0);
+        for (size_t r = 0; r < runs.size(); ++r)
+          for (int b = 0; b < runs[r].B; ++b) colrun[runs[r].q + b] = int(r);
+        for (auto& pp : parts) { pp.r0 = runs[colrun[pp.g]].r0; pp.r1 = runs[colrun[pp.g]].r1; }
+        C.part_off = int(hp->seppart.size());
+        C.npart = int(parts.size());
+        hp->seppart.insert(hp->seppart.end(), parts.begin(), parts.end());
         C.run_off = int(hp->seprun.size());
         C.nrun = int(runs.size());
         C.task_off = int(hp->septask.size());
+        if (runs.size() > size_t(kSepMaxRuns)) { ok_lev[lev] = 0; break; }
         for (size_t r = 0; r < runs.size(); ++r) {
-          if (runs[r].r1 <= runs[r].r0) runs[r].r0 = runs[r].r1 = 0;
+          runs[r].tbeg = int(hp->septask.size()) - C.task_off;
           for (int row = runs[r].r0; row < runs[r].r1; ++row) hp->septask.push_back(int(r) << 16 | row);
           hp->seprun.push_back(runs[r]);
         }
         C.ntask = int(hp->septask.size()) - C.task_off;
         C.nq = nq;
         hp->sep_nq[lev] = std::max(hp->sep_nq[lev], nq);
+        hp->sep_nrun[lev] = std::max(hp->sep_nrun[lev], C.nrun);
       }
   }
   for (int l = 1; l <= kMaxJ; ++l) hp->sep_ok[l] = seen[l] && ok_lev[l];
+  if (getenv("PCWD_DEBUG_SEP")) {   // per level: executed FMAs per unit (padded runs) by atom level, both stages
+    for (int lev = 1; lev <= J; ++lev) {
+      if (!hp->sep_ok[lev]) continue;
+      double f1[kSepSmax + 1] = {}, f2[kSepSmax + 1] = {}, ncls = 0, ntask = 0, npart = 0, nmask = 0;
+      for (int sbi = 0; sbi < ns; ++sbi) {
+        const SubBand& S = P.sb[sbi];
+        if (S.fg_m <= 0 || S.level != lev) continue;
+        for (int c = 0; c < S.fg_m * S.fg_m; ++c) {
+          const SepClass& C = hp->sepcls[S.fg_off + c];
+          ncls += 1; ntask += C.ntask; npart += C.npart;
+          for (int r = 0; r < C.nrun; ++r) {
+            const SepRun& R = hp->seprun[C.run_off + r];
+            f1[R.s] += double(sep_bsel(R.s, R.B)) * (sep_atom_blk(R.s, L2) << R.s) * (R.r1 - R.r0);
+            nmask += R.mask * (R.r1 - R.r0);
+          }
+          for (int r = 0; r < C.npart; ++r) {
+            const SepPart& R = hp->seppart[C.part_off + r];
+            f2[R.s] += double(sep_bsel(R.s, R.B)) * (sep_atom_blk(R.s, L2) << R.s);
+          }
+        }
+      }
+      fprintf(stderr, "[pcwd sep] level %d classes %.0f stage-1 tasks/unit %.1f (masked %.1f) stage-2 runs/unit %.1f nq %d | executed FMA/unit"
+              " by s=1..5: stage 1 %.0f %.0f %.0f %.0f %.0f, stage 2 %.0f %.0f %.0f %.0f %.0f\n", lev, ncls, ntask / ncls, nmask / ncls,
+              npart / ncls, hp->sep_nq[lev], f1[1] / ncls, f1[2] / ncls, f1[3] / ncls, f1[4] / ncls, f1[5] / ncls,
+              f2[1] / ncls, f2[2] / ncls, f2[3] / ncls, f2[4] / ncls, f2[5] / ncls);
+    }
+  }
 }
 
 int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::string* msg) {

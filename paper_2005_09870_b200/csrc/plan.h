@@ -42,6 +42,7 @@ struct HostPlan {
   std::vector<int> septask;
   int sep_ok[kMaxJ + 1] = {};     // level ℓ: every class record of every sub-band built
   int sep_nq[kMaxJ + 1] = {};     // max Q columns over the level's classes
+  int sep_nrun[kMaxJ + 1] = {};   // max stage-1 runs over the level's classes
 };
 
 // Returns a pcwd_status; msg receives the reason on error.

@@ -41,6 +41,7 @@ SWITCHES = [
     {"PCWD_NO_DIRECT": "1"},
     {"PCWD_FINE_DIRECT": "1,1,1"},
     {"PCWD_NO_FINE": "1", "PCWD_NO_TILE": "1", "PCWD_NO_BATCHED": "1"},
+    {"PCWD_SEP": "7"},
 ]
 
 
