@@ -241,12 +241,15 @@ __device__ __forceinline__ void sep_units(const Plan& P, const FineArgs& A, cons
     for (int r = gt; r < C.nrun; r += GT) srun[r] = A.seprun[C.run_off + r];
     bar_group(1 + slot, GT);
     // stage 1: Q[q + b][row] = Σ_i W_{s,e}[i] · R[row][c + 2^s b + i]   (Q column-major, column stride QS)
-    // task t = row r0 + (t − tbeg) of run r (runs in shared memory; t grows, so r only advances)
-    int r = 0;
+    // tasks (run << 16 | row) grouped by code path in whole warps; -1 = padding.  The next task is fetched one
+    // iteration ahead (run records in shared memory).
+    int tk = gt < C.ntask ? __ldg(A.septask + C.task_off + gt) : -1;
     for (int t = gt; t < C.ntask; t += GT) {
-      while (r + 1 < C.nrun && srun[r + 1].tbeg <= t) ++r;
-      const SepRun& R = srun[r];
-      const int row = R.r0 + t - R.tbeg;
+      const int cur = tk;
+      tk = t + GT < C.ntask ? __ldg(A.septask + C.task_off + t + GT) : -1;
+      if (cur < 0) continue;
+      const SepRun& R = srun[cur >> 16];
+      const int row = cur & 0xffff;
       if constexpr (L2 >= 4) {
         if (R.mask)
           sep_dispatch<Real, L2, true>(R.s, R.B, X + row * A.RS, R.c, 0, R1, taps + R.toff, Q + R.q * A.QS + row,
@@ -260,6 +263,7 @@ __device__ __forceinline__ void sep_units(const Plan& P, const FineArgs& A, cons
     // stage 2: Θ[μ][λ] = Σ_i W_{s,e}[i] · Q[g][fs + 2^s b + i]  (rows outside the computed [r0, r1) read 0)
     for (int t = gt; t < C.npart; t += GT) {
       const SepPart R = A.seppart[C.part_off + t];
+      if (R.g < 0) continue;
       if constexpr (L2 >= 4)
         sep_dispatch<Real, L2, true>(R.s, R.B, Q + R.g * A.QS, R.fs, R.r0, R.r1, taps + R.toff,
                                      sv + R.jj, R.jstr);

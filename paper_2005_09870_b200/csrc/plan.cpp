@@ -324,18 +324,33 @@ static void build_sep(HostPlan* hp) {
         for (size_t r = 0; r < runs.size(); ++r)
           for (int b = 0; b < runs[r].B; ++b) colrun[runs[r].q + b] = int(r);
         for (auto& pp : parts) { pp.r0 = runs[colrun[pp.g]].r0; pp.r1 = runs[colrun[pp.g]].r1; }
+        // stage-2 tasks grouped by kernel variant (atom level), each group padded to whole warps (g = -1: no-op)
+        std::stable_sort(parts.begin(), parts.end(), [](const SepPart& x, const SepPart& y) { return x.s < y.s; });
         C.part_off = int(hp->seppart.size());
-        C.npart = int(parts.size());
-        hp->seppart.insert(hp->seppart.end(), parts.begin(), parts.end());
+        for (size_t i = 0; i < parts.size(); ++i) {
+          hp->seppart.push_back(parts[i]);
+          if (i + 1 == parts.size() || parts[i + 1].s != parts[i].s)
+            while ((hp->seppart.size() - C.part_off) % 32) hp->seppart.push_back(SepPart{-1, parts[i].s, 0, 0, 0, 0, 0, 0, 0, 0, {0, 0}});
+        }
+        C.npart = int(hp->seppart.size()) - C.part_off;
         C.run_off = int(hp->seprun.size());
         C.nrun = int(runs.size());
         C.task_off = int(hp->septask.size());
         if (runs.size() > size_t(kSepMaxRuns)) { ok_lev[lev] = 0; break; }
-        for (size_t r = 0; r < runs.size(); ++r) {
+        // stage-1 tasks (run << 16 | row) grouped by kernel variant (atom level, register-window width, mask) so
+        // that a warp's 32 consecutive tasks take one code path; each group padded to whole warps (-1: no-op)
+        std::vector<int> ord(runs.size());
+        for (size_t r = 0; r < runs.size(); ++r) ord[r] = int(r);
+        auto vkey = [&](int r) { return std::make_tuple(runs[r].s, sep_bsel(runs[r].s, runs[r].B), runs[r].mask); };
+        std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return vkey(x) < vkey(y); });
+        for (size_t i = 0; i < ord.size(); ++i) {
+          const int r = ord[i];
           runs[r].tbeg = int(hp->septask.size()) - C.task_off;
-          for (int row = runs[r].r0; row < runs[r].r1; ++row) hp->septask.push_back(int(r) << 16 | row);
-          hp->seprun.push_back(runs[r]);
+          for (int row = runs[r].r0; row < runs[r].r1; ++row) hp->septask.push_back(r << 16 | row);
+          if (i + 1 == ord.size() || vkey(ord[i + 1]) != vkey(r))
+            while ((hp->septask.size() - C.task_off) % 32) hp->septask.push_back(-1);
         }
+        hp->seprun.insert(hp->seprun.end(), runs.begin(), runs.end());
         C.ntask = int(hp->septask.size()) - C.task_off;
         C.nq = nq;
         hp->sep_nq[lev] = std::max(hp->sep_nq[lev], nq);
