@@ -304,7 +304,7 @@ __device__ __forceinline__ void sep_units(const Plan& P, const FineArgs& A, cons
 //   [slack] R_0 .. R_{GU-1} (RS × R0 each; later the approximation of each step, row stride RS) [slack]
 //   [slack] staging: NST × (T_k tile R0 × TS, v_k strip R0 × VS)  ∪  Yt_0 .. Yt_{GU-1} (YC × YS)  [slack]
 //   D_0 .. D_{GU-1} (DS each)
-template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG, int MINB>
+template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG, int MINB, bool SEP>
 __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__ Plan P, const __grid_constant__ FineArgs A) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ int wflag[CG];
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
   Real* Sbase = sm + kSlack + (((s_raw + 127u) & ~127u) - s_raw) / sizeof(Real);
   Real* Ybase = sm + A.regS + kSlack;
   for (int i = tid; i < kSlack; i += kFT) sm[i] = Real(0);   // zero rows before R_0 row 0 (left pad)
-  if (A.sep) {   // the separable path's atom taps (geom.h sep_toff layout)
+  if constexpr (SEP) {   // the separable path's atom taps (geom.h sep_toff layout)
     const Real* at = reinterpret_cast<const Real*>(A.atoms);
     for (int i = tid; i < A.ntap; i += kFT) sm[A.regA + i] = at[i];
   }
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kFT, MINB) fine_kernel(const __grid_constant__
     if (A.dbg && tid == 0) { const long long t = clock64(); t_ksum += t - t_last; t_last = t; }
     // ------------------------------------------------------------------ a3: cascade of unit u
     // (CG units at a time, one thread group each; Yt, D and the step descriptors are per group slot)
-    if (A.sep) {
+    if constexpr (SEP) {
       sep_units<Real, L2, GU, CG>(P, A, S, p0, p1f, ufirst, Rbase + roff, Ybase, sm + A.regA, slot, gt, wflag);
       continue;
     }
@@ -789,9 +789,15 @@ bool fine_config(int real_bytes, int level, int L2, FineCfg* c) {
   return false;
 }
 
+// The separable variant is a separate instance (SEP = true) so the cascade instances carry none of its code; it is
+// built only where build_sep can plan it (2δ ∈ {4, 8, 12}).
 template <typename Real, int L2, int LEV, int GU, int GZ, int NT, int NST, int CG, int MINB>
 static cudaError_t launch_fine_t(const Plan& P, const FineArgs& A, int grid, size_t smem, cudaStream_t st) {
-  auto k = fine_kernel<Real, L2, LEV, GU, GZ, NT, NST, CG, MINB>;
+  auto k = fine_kernel<Real, L2, LEV, GU, GZ, NT, NST, CG, MINB, false>;
+  if constexpr (L2 >= 4) {
+    if (A.sep) k = fine_kernel<Real, L2, LEV, GU, GZ, NT, NST, CG, MINB, true>;
+  }
+  if (A.sep && L2 < 4) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
