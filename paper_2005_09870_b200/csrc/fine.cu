@@ -25,6 +25,9 @@
 #include "kernels.cuh"
 #include "tma.h"
 
+// the SEP instances return from the round before the cascade loop (if constexpr + continue)
+#pragma nv_diag_suppress 128
+
 namespace pcwd {
 
 namespace {
