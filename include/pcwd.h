@@ -278,6 +278,14 @@ int pcwd_plan_stencil(const pcwd_desc* desc, int32_t sb, int32_t* out_sb, int32_
                       int32_t* out_o1);
 /* Number of sub-bands of the Λ layout. */
 int pcwd_plan_num_subbands(const pcwd_desc* desc, int32_t* out);
+/* Host only.  The 1-D analysis atom of the separable fine path (reading R-S1; the analysis step of
+ * P:96 iterated): W_{s,e}(y) for y = *out_start + i, i < *out_len, i.e. the level-s coefficient of
+ * orientation e (0 = scaling, 1 = wavelet) at position 0 on the integer line is Σ_y x(y) W_{s,e}(y); the atom of
+ * position l is W_{s,e}(y − 2^s l).  desc supplies the filter (validated like pcwd_create; u, v may be NULL).
+ * out: caller-owned host array of cap doubles (may be NULL to query the length).  1 ≤ s ≤ 16, e ∈ {0, 1};
+ * PCWD_E_PARAM on a bad argument or cap < length. */
+int pcwd_plan_atom(const pcwd_desc* desc, int32_t s, int32_t e, double* out, int32_t cap, int32_t* out_len,
+                   int32_t* out_start);
 
 #ifdef __cplusplus
 }

@@ -537,6 +537,30 @@ int pcwd_plan_stencil(const pcwd_desc* desc, int32_t sb, int32_t* out_sb, int32_
   return PCWD_OK;
 }
 
+int pcwd_plan_atom(const pcwd_desc* desc, int32_t s, int32_t e, double* out, int32_t cap, int32_t* out_len,
+                   int32_t* out_start) {
+  std::string msg;
+  int rc = validate_desc(desc, &msg);
+  if (rc) return fail(rc, msg);
+  if (s < 1 || s > kMaxJ || (e != 0 && e != 1) || !out_len || !out_start) return fail(PCWD_E_PARAM, "pcwd_plan_atom arguments");
+  Plan P{};
+  P.L2 = desc->filter_len;
+  for (int j = 0; j < P.L2; ++j) {   // f_0 = h, f_1[j] = g[2 − 2δ + j] = (−1)^{1−i} h[1−i], i = 2 − 2δ + j (common.h)
+    const int i = 2 - P.L2 + j;
+    P.td[0][j] = desc->h[j];
+    P.td[1][j] = ((1 - i) % 2 == 0 ? 1.0 : -1.0) * desc->h[1 - i];
+  }
+  std::vector<double> w;
+  sep_base_atom(P, s, e, &w);
+  *out_len = int32_t(w.size());
+  *out_start = sep_atom_start(s, e, P.L2);
+  if (out) {
+    if (cap < int32_t(w.size())) return fail(PCWD_E_PARAM, "pcwd_plan_atom: cap smaller than the atom");
+    std::copy(w.begin(), w.end(), out);
+  }
+  return PCWD_OK;
+}
+
 int pcwd_create(const pcwd_desc* desc, void** out_handle) {
   if (!out_handle) return fail(PCWD_E_PARAM, "out_handle is NULL");
   *out_handle = nullptr;

@@ -181,6 +181,7 @@ PCWD_HD constexpr int sep_bsel(int s, int B) {
   return B <= 1 ? 1 : B <= 2 ? 2 : (s >= 4 ? 2 : B <= 3 ? 3 : B <= 4 ? 4 : B <= 6 ? 6 : 8);
 }   // atom levels of the separable path (plan.cpp keeps the cascade beyond)
 PCWD_HD constexpr int sep_atom_len(int s, int L2) { return ((1 << s) - 1) * (L2 - 1) + 1; }
+PCWD_HD constexpr int sep_atom_start(int s, int e, int L2) { return e ? (1 << (s - 1)) * (2 - L2) : 0; }
 PCWD_HD constexpr int sep_bmax(int s) { return s <= 2 ? 8 : (s == 3 ? 6 : (s == 4 ? 2 : 1)); }   // atoms per run (max)
 // shared-memory tap table: W_{s,e} (s ≤ kSepSmax) at 16-byte aligned offsets, each followed by zeros up to a
 // whole number of 2^s-tap blocks

@@ -192,6 +192,28 @@ static void build_stencil(const Plan& P, int s_mu, int L, std::vector<Stencil>* 
   }
 }
 
+// Base atom W_{s,e} of the separable path (geom.h): the level-s analysis functional of orientation e at position
+// 0 on the integer line, W_{1,e}(y) = f_e[y − o_e], W_{s,e}(y) = Σ_j f_e[j] · W_{s−1,0}(y − 2^{s−1}(o_e + j)) (P:96,
+// R5); w[i] = W_{s,e}(sep_atom_start(s, e) + i), i < sep_atom_len(s).  fp64.
+void sep_base_atom(const Plan& P, int s, int e, std::vector<double>* out) {
+  const int L2 = P.L2;
+  std::vector<double> prev;   // W_{s'-1,0}
+  for (int s2 = 1; s2 <= s; ++s2) {
+    const int len = sep_atom_len(s2, L2);
+    const int ee = s2 == s ? e : 0;
+    std::vector<double> w(len, 0.0);
+    if (s2 == 1) {
+      for (int j = 0; j < L2; ++j) w[j] = P.td[ee][j];
+    } else {
+      const int dil = 1 << (s2 - 1);
+      for (int j = 0; j < L2; ++j)
+        for (size_t i = 0; i < prev.size(); ++i) w[dil * j + i] += P.td[ee][j] * prev[i];
+    }
+    if (s2 == s) *out = w;
+    else prev = w;
+  }
+}
+
 // Separable direct path of the fine kernel (geom.h): base atoms W_{s,e} and, per fine sub-band and class,
 // the stage-1 runs over the distinct column atoms and the stage-2 partner records.  A level is marked usable
 // only if every one of its class records could be built (no atom wraps onto the window, partner levels
@@ -208,27 +230,16 @@ static void build_sep(HostPlan* hp) {
   if (P.retain != PCWD_RETAIN_BAND || P.d != 2 || hp->fgeom.empty() || (L2 != 4 && L2 != 8 && L2 != 12)) return;
   const int smax = std::min(J, kSepSmax);
   hp->sep_smax = smax;
-  std::vector<double> prev;   // W_{s-1,0}
   for (int s = 1; s <= smax; ++s) {
-    const int len = ((1 << s) - 1) * (L2 - 1) + 1;
-    hp->atom_len[s] = len;
-    std::vector<double> w0;
+    hp->atom_len[s] = sep_atom_len(s, L2);
     for (int e = 0; e < 2; ++e) {
-      std::vector<double> w(len, 0.0);
-      if (s == 1) {
-        for (int j = 0; j < L2; ++j) w[j] = P.td[e][j];
-      } else {
-        const int dil = 1 << (s - 1);
-        for (int j = 0; j < L2; ++j)
-          for (size_t i = 0; i < prev.size(); ++i) w[dil * j + i] += P.td[e][j] * prev[i];
-      }
+      std::vector<double> w;
+      sep_base_atom(P, s, e, &w);
       hp->atom_off[s][e] = int(hp->atoms.size());
       hp->atoms.insert(hp->atoms.end(), w.begin(), w.end());
-      if (e == 0) w0 = w;
     }
-    prev = w0;
   }
-  auto sstart = [&](int s, int e) { return e ? (1 << (s - 1)) * (2 - L2) : 0; };   // support start of W_{s,e}
+  auto sstart = [&](int s, int e) { return sep_atom_start(s, e, L2); };   // support start of W_{s,e}
   const int PADC = L2;    // zero columns guaranteed on both sides of every R row (fine kernel layout)
   int ok_lev[kMaxJ + 1], seen[kMaxJ + 1];
   for (int l = 0; l <= kMaxJ; ++l) ok_lev[l] = 1, seen[l] = 0;

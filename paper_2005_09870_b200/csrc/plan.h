@@ -51,6 +51,9 @@ int validate_desc(const pcwd_desc* d, std::string* msg);
 // u_host: m × N fp64 on the host (may be NULL: then the bounding box is the whole torus).
 int build_plan(const pcwd_desc* d, const double* u_host, HostPlan* hp, std::string* msg);
 
+// Base atom W_{s,e} of the separable fine path (fp64, sep_atom_len(s) taps from sep_atom_start(s, e)).
+void sep_base_atom(const Plan& P, int s, int e, std::vector<double>* out);
+
 // Λ order index of sub-band (level, e).
 int sb_index(int d, int J, int level, int e);
 

@@ -60,7 +60,8 @@ EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_m
            "pcwd_last_error", "pcwd_validate", "pcwd_plan_shard", "pcwd_plan_stencil",
            "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile",
            "pcwd_set_kernels", "pcwd_decompose_to_host", "pcwd_wavelet_transform", "pcwd_fista",
-           "pcwd_fista_sharded", "pcwd_approx", "pcwd_operator_apply", "pcwd_pc_from_samples", "pcwd_pc_from_svir", "pcwd_columns"]
+           "pcwd_fista_sharded", "pcwd_approx", "pcwd_operator_apply", "pcwd_pc_from_samples", "pcwd_pc_from_svir", "pcwd_columns",
+           "pcwd_plan_atom"]
 
 REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_void_p)   # pcwd_reduce_fn
 _lib = None
@@ -90,6 +91,7 @@ def lib():
         L.pcwd_plan_shard.argtypes = [ctypes.POINTER(Desc), i64p, i64p]
         L.pcwd_plan_stencil.argtypes = [ctypes.POINTER(Desc), i32, i32p, i32p, i32p]
         L.pcwd_plan_num_subbands.argtypes = [ctypes.POINTER(Desc), i32p]
+        L.pcwd_plan_atom.argtypes = [ctypes.POINTER(Desc), i32, i32, ctypes.POINTER(ctypes.c_double), i32, i32p, i32p]
         L.pcwd_profile.argtypes = [vp, ctypes.c_int]
         L.pcwd_phase_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         dp = ctypes.POINTER(ctypes.c_double)
@@ -535,6 +537,18 @@ def plan_stencil(spec: Spec, sb: int):
     p = lambda x: x.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))  # noqa: E731
     _check(lib().pcwd_plan_stencil(ctypes.byref(d), sb, p(a), p(b), p(c)), "pcwd_plan_stencil")
     return a, b, c
+
+
+def plan_atom(spec: Spec, s: int, e: int):
+    """The separable path's 1-D analysis atom W_{s,e} (host only): (taps, start) with W(start + i) = taps[i]."""
+    keep = []
+    d = make_desc(spec, keep)
+    n, st = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().pcwd_plan_atom(ctypes.byref(d), s, e, None, 0, ctypes.byref(n), ctypes.byref(st)), "pcwd_plan_atom")
+    out = np.zeros(n.value, dtype=np.float64)
+    _check(lib().pcwd_plan_atom(ctypes.byref(d), s, e, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n.value,
+                                ctypes.byref(n), ctypes.byref(st)), "pcwd_plan_atom")
+    return out, st.value
 
 
 def num_subbands(spec: Spec) -> int:

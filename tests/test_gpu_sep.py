@@ -21,7 +21,7 @@ def test_sep_path_oracle_parity():
     env["PCWD_SEP"] = "7"
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-m", "gpu",
                         "-x", "-q", "-p", "no:cacheprovider", "-k",
-                        "micro or c3_band or c5_band_fp32 or fine_kernel or every_fine or all_units_128"],
+                        "micro or c3_band or c5_band_fp32 or fine_kernel or every_fine or all_units_128 or symlet"],
                        env=env, cwd=ROOT, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
