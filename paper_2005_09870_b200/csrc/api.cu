@@ -769,9 +769,11 @@ int pcwd_create(const pcwd_desc* desc, void** out_handle) {
         int roffmax = 0;   // R rows are shifted by one column when a window starts at an odd column
         for (int q = s; q < e; ++q) roffmax |= P.sb[q].tSu[1] & 1;
         // separable direct a3 + a4 (plan.cpp build_sep): odd R row stride (a warp's lanes read 32 rows of one column)
-        // PCWD_SEP: bit mask over fine levels 1..3; default 4 = level 3 only (c5, B200: level 3 1.95 ms separable vs
-        // 2.11 ms cascade; levels 1 / 2 8.1 / 2.66 ms vs 7.3 / 2.54 ms — DESIGN.md §6)
-        static const int sep_mask = getenv("PCWD_SEP") ? atoi(getenv("PCWD_SEP")) : 4;
+        // PCWD_SEP: bit mask over fine levels 1..3; default fp32 4 = level 3 only (c5, B200: level 3 1.95 ms separable
+        // vs 2.11 ms cascade; levels 1 / 2 8.1 / 2.66 ms vs 7.3 / 2.54 ms), fp64 6 = levels 2-3 (7.91 / 5.68 ms vs
+        // 8.35 / 6.15; level 1 17.1 vs 16.3 ms) — DESIGN.md §6
+        static const int sep_env = getenv("PCWD_SEP") ? atoi(getenv("PCWD_SEP")) : -1;
+        const int sep_mask = sep_env >= 0 ? sep_env : (rb == 8 ? 6 : 4);
         const bool sep = h->hp.sep_ok[lev] && ((sep_mask >> (lev - 1)) & 1);
         const int RS = sep ? ((R1 + std::max(kSepPad, roffmax + P.L2 + 2)) | 1) : pair_stride(R1 + roffmax + P.L2 + 2);
         const int zmaxT = (SH - 1) + SH * fc.GZ * (NZB - 1) + SH * (fc.GZ - 1);
