@@ -308,6 +308,10 @@ int run_units(Handle* h, int mode, cudaStream_t st, double tau) {
     // levels overlap the other fine levels; it runs alone, then the coarse streams fork beside the rest
     const int li = (sk || (conc && overlap)) ? nL - 1 - it : it;
     const Launch& L = h->launches[li];
+    {   // timing experiment only (results invalid): PCWD_SKIP_LEVELS = bit mask of levels whose launches are skipped
+      static const int skip = getenv("PCWD_SKIP_LEVELS") ? atoi(getenv("PCWD_SKIP_LEVELS")) : 0;
+      if (skip && ((skip >> P.sb[find_subband(P, L.u0)].level) & 1)) continue;
+    }
     ls = st;
     // level 1 beside the coarse streams too (default: the shorter step, c5 r01 15.36 vs 15.74 ms); PCWD_OVERLAP_ALL=0
     // runs the first (largest) level alone
