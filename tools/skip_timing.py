@@ -3,7 +3,7 @@ sys.path.insert(0, os.getcwd())
 import torch
 from paper_2005_09870_b200 import Decomposition, Spec
 from synth import configs as C
-p = C.get("c4")
+p = C.get(sys.argv[1] if len(sys.argv) > 1 else "c4")
 dec = Decomposition(Spec(p.d, p.n, p.J, p.h, torch.from_numpy(p.u).cuda(), torch.from_numpy(p.v).cuda(), dtype="f32",
                          retain=p.retain, tau_rel=p.tau_rel, band_L=p.band_L))
 for _ in range(2): dec.decompose()
