@@ -132,7 +132,9 @@ int pcwd_copy_csr(void* handle, int64_t* row_ptr, int32_t* col, void* val, void*
  * supp u_k must lie inside the periodic bounding box of the u given to pcwd_create (the windows
  * of the plan are derived from it): checked on the GPU, PCWD_E_PARAM otherwise (the
  * handle then keeps its previous kernels).  Invalidates the last decompose.  Enqueued on stream,
- * then synchronises it once for the support check. */
+ * then synchronises it once for the support check; BAND: v is then copied on an internal stream while
+ * the templates of the new u are built on `stream` (the next decompose uses them instead of building
+ * them), and both are synchronised before return, so u and v may be released on return. */
 int pcwd_set_kernels(void* handle, const double* u, const double* v, void* stream);
 
 /* pcwd_decompose followed by the copy of the CSR into caller buffers (as pcwd_copy_csr; NULL

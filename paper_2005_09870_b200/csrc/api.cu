@@ -86,6 +86,8 @@ struct Handle {
   bool cand_valid = false;
   double M = 0.0;
   bool M_set = false, tmpl_fresh = false, decomposed = false;
+  bool tmpl_ready = false;   // BAND: templates of the current u built by pcwd_set_kernels, consumed by the next decompose
+  cudaStream_t cv = nullptr; // pcwd_set_kernels: v's host-to-device copy beside the template build
   int nlaunch = 0;
   bool profile = false;
   bool profile_serial = false;      // pcwd_profile(h, 2): launches serialised (per-kernel times, no overlap)
@@ -146,6 +148,7 @@ void free_all(Handle* h) {
   if (h->cjoin) cudaEventDestroy(h->cjoin);
   h->cjoin = nullptr;
   if (h->cs) cudaStreamDestroy(h->cs);
+  if (h->cv) cudaStreamDestroy(h->cv);
   h->cs = nullptr;
   for (int i = 0; i < Handle::kNCS; ++i) {
     if (h->cstream[i]) cudaStreamDestroy(h->cstream[i]);
@@ -1291,7 +1294,8 @@ int pcwd_decompose(void* handle, void* stream) {
       CK(launch_wrap_v(h->v_d, h->vwrap_d, P.n, 0, h->kt_offx, P.n + h->kt_pr, P.n + h->kt_pc, P.m, h->hp.real_bytes, st));
       h->nlaunch++;
     }
-    if ((rc = build_templates(h, st))) return rc;
+    if (h->tmpl_ready) h->tmpl_ready = false;   // built by pcwd_set_kernels beside v's copy (same u)
+    else if ((rc = build_templates(h, st))) return rc;
     rec(1);
     if ((rc = run_units(h, MODE_BAND, st, 0.0))) return rc;
     rec(2);
@@ -1438,16 +1442,32 @@ int pcwd_set_kernels(void* handle, const double* u, const double* v, void* strea
   CK(cudaMemsetAsync(h->flag_d, 0, sizeof(int), st));
   CK(cudaMemcpyAsync(h->ustage, u, mN * sizeof(double), cudaMemcpyDefault, st));
   CK(launch_support_check(h->ustage, mN, P.n, P.d, P.zlo, P.zhi, h->flag_d, st));
-  CK(cudaMemcpyAsync(h->vstage, v, mN * sizeof(double), cudaMemcpyDefault, st));
+  // BAND: v is copied on a second stream while the templates (which read only u) are built, so the next decompose
+  // need not build them; other rules copy v behind u as before
+  const bool overlap = P.retain == PCWD_RETAIN_BAND && !getenv("PCWD_NO_SETK_OVERLAP");
+  if (!overlap) CK(cudaMemcpyAsync(h->vstage, v, mN * sizeof(double), cudaMemcpyDefault, st));
   int flag = 0;
   CK(cudaMemcpyAsync(&flag, h->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (flag)
     return fail(PCWD_E_PARAM, "supp u_k leaves the periodic bounding box the plan was built for (create a new handle)");
   std::swap(h->u_d, h->ustage);
+  h->tmpl_ready = false;
   // v_d stays in place: the k-sum TMA maps hold its address
-  if (rb == 8) CK(cudaMemcpyAsync(h->v_d, h->vstage, mN * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  else CK(launch_cast(static_cast<const double*>(h->vstage), h->v_d, mN, 4, st));
+  cudaStream_t vs = st;
+  if (overlap) {
+    if (!h->cv) CK(cudaStreamCreateWithFlags(&h->cv, cudaStreamNonBlocking));
+    vs = h->cv;
+    CK(cudaMemcpyAsync(h->vstage, v, mN * sizeof(double), cudaMemcpyDefault, vs));
+  }
+  if (rb == 8) CK(cudaMemcpyAsync(h->v_d, h->vstage, mN * sizeof(double), cudaMemcpyDeviceToDevice, vs));
+  else CK(launch_cast(static_cast<const double*>(h->vstage), h->v_d, mN, 4, vs));
+  if (overlap) {
+    if (int rc = build_templates(h, st)) return rc;
+    CK(cudaStreamSynchronize(vs));   // the caller may release v on return
+    CK(cudaStreamSynchronize(st));   // the templates are complete whatever stream the next decompose uses
+    h->tmpl_ready = true;
+  }
   h->M_set = false;
   h->tmpl_fresh = false;
   h->cand_valid = false;
