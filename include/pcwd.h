@@ -137,6 +137,18 @@ int pcwd_copy_csr(void* handle, int64_t* row_ptr, int32_t* col, void* val, void*
  * them), and both are synchronised before return, so u and v may be released on return. */
 int pcwd_set_kernels(void* handle, const double* u, const double* v, void* stream);
 
+/* The periodic bounding box of supp u_k the plan was built from (the windows of the plan follow
+ * from it): per axis a start offset lo[a] (in [0, n)) and a width w[a] (1 ≤ w[a] ≤ n), axis 0 = rows
+ * (d = 1: lo[0] = 0, w[0] = 1).  Host only; never fails on a valid handle. */
+int pcwd_kernel_box(void* handle, int32_t lo[2], int32_t w[2]);
+
+/* pcwd_set_kernels with u_k given on that box only (the compact impulse responses of P:234-246 are
+ * naturally stored this way): u_box = m × w[0] × w[1] fp64, row-major, entry (k, i0, i1) = u_k at grid
+ * point ((lo[0] + i0) mod n, (lo[1] + i1) mod n); u_k is zero elsewhere by construction, so there is no
+ * support check and no synchronisation before the template build.  v, streams, synchronisation on
+ * return and invalidation as pcwd_set_kernels; host (pinned) or device pointers, caller keeps ownership. */
+int pcwd_set_kernels_box(void* handle, const double* u_box, const double* v, void* stream);
+
 /* pcwd_decompose followed by the copy of the CSR into caller buffers (as pcwd_copy_csr; NULL
  * skips an array), with the copies overlapped with the computation: BAND and FULL rows have a
  * fixed width, so each launch's rows are copied (on a second stream, event-ordered) as soon as

@@ -98,6 +98,8 @@ struct Handle {
   cudaEvent_t cjoin = nullptr;      // decompose_to_host: copies done
   double* ustage = nullptr;         // set_kernels: staging of u (swapped with u_d once checked)
   void* vstage = nullptr;           // set_kernels: staging of v (fp64; swapped with v_d in fp64 compute)
+  double* ubox = nullptr;           // set_kernels_box: u_k on the plan's bounding box (m × w0 × w1)
+  int64_t ubox_cap = 0;
   struct Sink { int64_t width; int32_t* col; char* val; int ob; };
   const Sink* sink = nullptr;       // decompose_to_host: caller buffers the finished rows go to
   int* flag_d = nullptr;            // set_kernels: support check flag
@@ -140,7 +142,7 @@ bool is_device_ptr(const void* p) {
 
 void free_all(Handle* h) {
   void* ptrs[] = {h->u_d, h->v_d, h->T_d, h->phi[0], h->phi[1], h->Ytmp, h->stencil_d, h->box_d, h->fgeom_d, h->sepc_d, h->seprun_d, h->seppart_d, h->septask_d, h->atoms_d, h->vpad_d, h->vwrap_d, h->amaps_d, h->gscratch, h->bscratch,
-                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->cand, h->ustage, h->vstage, h->flag_d, h->fbuf, h->rpT, h->rowT, h->valT, h->twork};
+                  h->row_ptr, h->col, h->val, h->unitmax, h->cnt, h->rowcnt, h->cubtmp, h->dmax, h->cand, h->ustage, h->vstage, h->ubox, h->flag_d, h->fbuf, h->rpT, h->rowT, h->valT, h->twork};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->cev) cudaEventDestroy(e);
@@ -1428,29 +1430,12 @@ int pcwd_copy_csr(void* handle, int64_t* row_ptr, int32_t* col, void* val, void*
   return PCWD_OK;
 }
 
-int pcwd_set_kernels(void* handle, const double* u, const double* v, void* stream) {
-  Handle* h = static_cast<Handle*>(handle);
-  if (!h || !u || !v) return fail(PCWD_E_PARAM, "NULL argument");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  CK(cudaSetDevice(h->desc.device));
+// pcwd_set_kernels / pcwd_set_kernels_box after the new u is staged (and checked) in h->ustage: swap it in, copy v
+// (BAND: on a second stream beside the template build), invalidate the last decompose
+static int set_kernels_finish(Handle* h, const double* v, cudaStream_t st, bool overlap) {
   const Plan& P = h->hp.P;
   const int64_t mN = int64_t(P.m) * P.N;
   const int rb = h->hp.real_bytes;
-  if (!h->ustage) CK(dalloc(&h->ustage, mN * sizeof(double)));
-  if (!h->vstage) CK(dalloc(&h->vstage, mN * sizeof(double)));
-  if (!h->flag_d) CK(dalloc(&h->flag_d, sizeof(int)));
-  CK(cudaMemsetAsync(h->flag_d, 0, sizeof(int), st));
-  CK(cudaMemcpyAsync(h->ustage, u, mN * sizeof(double), cudaMemcpyDefault, st));
-  CK(launch_support_check(h->ustage, mN, P.n, P.d, P.zlo, P.zhi, h->flag_d, st));
-  // BAND: v is copied on a second stream while the templates (which read only u) are built, so the next decompose
-  // need not build them; other rules copy v behind u as before
-  const bool overlap = P.retain == PCWD_RETAIN_BAND && !getenv("PCWD_NO_SETK_OVERLAP");
-  if (!overlap) CK(cudaMemcpyAsync(h->vstage, v, mN * sizeof(double), cudaMemcpyDefault, st));
-  int flag = 0;
-  CK(cudaMemcpyAsync(&flag, h->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (flag)
-    return fail(PCWD_E_PARAM, "supp u_k leaves the periodic bounding box the plan was built for (create a new handle)");
   std::swap(h->u_d, h->ustage);
   h->tmpl_ready = false;
   // v_d stays in place: the k-sum TMA maps hold its address
@@ -1473,6 +1458,70 @@ int pcwd_set_kernels(void* handle, const double* u, const double* v, void* strea
   h->cand_valid = false;
   h->decomposed = false;
   return PCWD_OK;
+}
+
+int pcwd_set_kernels(void* handle, const double* u, const double* v, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !u || !v) return fail(PCWD_E_PARAM, "NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(h->desc.device));
+  const Plan& P = h->hp.P;
+  const int64_t mN = int64_t(P.m) * P.N;
+  if (!h->ustage) CK(dalloc(&h->ustage, mN * sizeof(double)));
+  if (!h->vstage) CK(dalloc(&h->vstage, mN * sizeof(double)));
+  if (!h->flag_d) CK(dalloc(&h->flag_d, sizeof(int)));
+  CK(cudaMemsetAsync(h->flag_d, 0, sizeof(int), st));
+  CK(cudaMemcpyAsync(h->ustage, u, mN * sizeof(double), cudaMemcpyDefault, st));
+  CK(launch_support_check(h->ustage, mN, P.n, P.d, P.zlo, P.zhi, h->flag_d, st));
+  // BAND: v is copied on a second stream while the templates (which read only u) are built, so the next decompose
+  // need not build them; other rules copy v behind u as before
+  const bool overlap = P.retain == PCWD_RETAIN_BAND && !getenv("PCWD_NO_SETK_OVERLAP");
+  if (!overlap) CK(cudaMemcpyAsync(h->vstage, v, mN * sizeof(double), cudaMemcpyDefault, st));
+  int flag = 0;
+  CK(cudaMemcpyAsync(&flag, h->flag_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (flag)
+    return fail(PCWD_E_PARAM, "supp u_k leaves the periodic bounding box the plan was built for (create a new handle)");
+  return set_kernels_finish(h, v, st, overlap);
+}
+
+int pcwd_kernel_box(void* handle, int32_t lo[2], int32_t w[2]) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !lo || !w) return fail(PCWD_E_PARAM, "NULL argument");
+  const Plan& P = h->hp.P;
+  lo[0] = P.d == 2 ? P.zlo[0] : 0;
+  w[0] = P.d == 2 ? P.zhi[0] - P.zlo[0] + 1 : 1;
+  lo[1] = P.zlo[1];
+  w[1] = P.zhi[1] - P.zlo[1] + 1;
+  return PCWD_OK;
+}
+
+int pcwd_set_kernels_box(void* handle, const double* u_box, const double* v, void* stream) {
+  Handle* h = static_cast<Handle*>(handle);
+  if (!h || !u_box || !v) return fail(PCWD_E_PARAM, "NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(h->desc.device));
+  const Plan& P = h->hp.P;
+  const int64_t mN = int64_t(P.m) * P.N;
+  int32_t lo[2], w[2];
+  pcwd_kernel_box(handle, lo, w);
+  const int64_t nb = int64_t(P.m) * w[0] * w[1];
+  if (!h->ustage) CK(dalloc(&h->ustage, mN * sizeof(double)));
+  if (!h->vstage) CK(dalloc(&h->vstage, mN * sizeof(double)));
+  if (h->ubox_cap < nb) {
+    if (h->ubox) cudaFree(h->ubox);
+    h->ubox = nullptr;
+    h->ubox_cap = 0;
+    CK(dalloc(&h->ubox, nb * sizeof(double)));
+    h->ubox_cap = nb;
+  }
+  // the support is inside the box by construction: no check, no synchronisation before the template build
+  const bool overlap = P.retain == PCWD_RETAIN_BAND && !getenv("PCWD_NO_SETK_OVERLAP");
+  CK(cudaMemcpyAsync(h->ubox, u_box, nb * sizeof(double), cudaMemcpyDefault, st));
+  CK(cudaMemsetAsync(h->ustage, 0, mN * sizeof(double), st));
+  CK(launch_box_scatter(h->ubox, P.m, P.n, P.d, P.zlo, P.zhi, h->ustage, st));
+  if (!overlap) CK(cudaMemcpyAsync(h->vstage, v, mN * sizeof(double), cudaMemcpyDefault, st));
+  return set_kernels_finish(h, v, st, overlap);
 }
 
 int pcwd_decompose_to_host(void* handle, int64_t* row_ptr, int32_t* col, void* val, void* stream) {

@@ -1025,6 +1025,30 @@ cudaError_t launch_support_check(const double* u, int64_t total, int n, int d, c
   return cudaGetLastError();
 }
 
+// pcwd_set_kernels_box: u_k given on the plan's periodic bounding box only (m × w0 × w1, row-major);
+// entry (k, i0, i1) goes to u_k at ((zlo0 + i0) mod n, (zlo1 + i1) mod n); the rest of u stays zero
+__global__ void box_scatter_kernel(const double* __restrict__ ub, int64_t total, int n, int d, int zlo0, int w0,
+                                   int zlo1, int w1, double* __restrict__ u) {
+  const int mask = n - 1;
+  const int64_t N = d == 2 ? int64_t(n) * n : n;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = i / (int64_t(w0) * w1);
+    const int r = int(i - k * w0 * w1);
+    const int i0 = r / w1, i1 = r - i0 * w1;
+    const int z1 = (zlo1 + i1) & mask, z0 = d == 2 ? ((zlo0 + i0) & mask) : 0;
+    u[k * N + int64_t(z0) * n + z1] = ub[i];
+  }
+}
+
+cudaError_t launch_box_scatter(const double* ub, int m, int n, int d, const int zlo[2], const int zhi[2], double* u,
+                               cudaStream_t st) {
+  const int w0 = d == 2 ? zhi[0] - zlo[0] + 1 : 1, w1 = zhi[1] - zlo[1] + 1;
+  const int64_t total = int64_t(m) * w0 * w1;
+  box_scatter_kernel<<<std::max<int64_t>(1, std::min(grid_for(total), 148 * 8)), kBlock, 0, st>>>(
+      ub, total, n, d, zlo[0], w0, zlo[1], w1, u);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cast(const double* src, void* dst, int64_t count, int real_bytes, cudaStream_t st) {
   if (real_bytes == 4) cast_kernel<float><<<grid_for(count), kBlock, 0, st>>>(src, (float*)dst, count);
   else cast_kernel<double><<<grid_for(count), kBlock, 0, st>>>(src, (double*)dst, count);

@@ -245,6 +245,8 @@ cudaError_t launch_phi0(const Plan& P, const double* u, double* phi0, int S0, in
 cudaError_t launch_tmpl_level(const Plan& P, const TmplArgs& A, int real_bytes, int coarse_level,
                               cudaStream_t st);
 cudaError_t launch_cast(const double* src, void* dst, int64_t count, int real_bytes, cudaStream_t st);
+cudaError_t launch_box_scatter(const double* ub, int m, int n, int d, const int zlo[2], const int zhi[2], double* u,
+                               cudaStream_t st);
 cudaError_t launch_support_check(const double* u, int64_t total, int n, int d, const int zlo[2], const int zhi[2],
                                  int* flag, cudaStream_t st);
 // K1: v_pad[k][y][x] = v[k][(y - P) mod n][(x - P) mod n], side n + 2P (compute type)

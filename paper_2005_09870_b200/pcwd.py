@@ -61,7 +61,7 @@ EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_m
            "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile",
            "pcwd_set_kernels", "pcwd_decompose_to_host", "pcwd_wavelet_transform", "pcwd_fista",
            "pcwd_fista_sharded", "pcwd_approx", "pcwd_operator_apply", "pcwd_pc_from_samples", "pcwd_pc_from_svir", "pcwd_columns",
-           "pcwd_plan_atom"]
+           "pcwd_plan_atom", "pcwd_kernel_box", "pcwd_set_kernels_box"]
 
 REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_void_p)   # pcwd_reduce_fn
 _lib = None
@@ -97,6 +97,8 @@ def lib():
         dp = ctypes.POINTER(ctypes.c_double)
         L.pcwd_launch_profile.argtypes = [vp, ctypes.c_int, i32p, dp, dp, i32p, i32p]
         L.pcwd_set_kernels.argtypes = [vp, vp, vp, vp]
+        L.pcwd_set_kernels_box.argtypes = [vp, vp, vp, vp]
+        L.pcwd_kernel_box.argtypes = [vp, i32p, i32p]
         L.pcwd_decompose_to_host.argtypes = [vp, vp, vp, vp, vp]
         L.pcwd_wavelet_transform.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         L.pcwd_fista.argtypes = [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), vp, vp]
@@ -186,6 +188,18 @@ class Decomposition:
         self._keep = (u, v)
         _check(lib().pcwd_set_kernels(self._h, ctypes.c_void_p(_ptr(u)), ctypes.c_void_p(_ptr(v)),
                                       ctypes.c_void_p(stream)), "pcwd_set_kernels")
+
+    def kernel_box(self):
+        """(lo, w): the periodic bounding box of supp u_k the plan was built from (pcwd_kernel_box), per axis."""
+        lo, w = (ctypes.c_int32 * 2)(), (ctypes.c_int32 * 2)()
+        _check(lib().pcwd_kernel_box(self._h, lo, w), "pcwd_kernel_box")
+        return (lo[0], lo[1]), (w[0], w[1])
+
+    def set_kernels_box(self, u_box, v, stream: int = 0):
+        """pcwd_set_kernels_box: u_k given on the plan's box only, (m, w0, w1) fp64 (see kernel_box()), v (m, N)."""
+        self._keep = (u_box, v)
+        _check(lib().pcwd_set_kernels_box(self._h, ctypes.c_void_p(_ptr(u_box)), ctypes.c_void_p(_ptr(v)),
+                                          ctypes.c_void_p(stream)), "pcwd_set_kernels_box")
 
     def decompose_to_host(self, row_ptr, col, val, stream: int = 0):
         """Decompose with the CSR streamed into the given (pinned host) buffers as launches finish

@@ -115,3 +115,42 @@ def test_set_kernels_rejects_support_outside_the_plan():
     dec.set_kernels(u, p.v)
     dec.decompose()
     dec.close()
+
+
+def _box_of(dec, p, u):
+    """u restricted to the plan's periodic bounding box (pcwd_kernel_box), m × w0 × w1, computed on the host from
+    the box the library reports; also checks that u vanishes outside that box."""
+    (lo0, lo1), (w0, w1) = dec.kernel_box()
+    m = u.shape[0]
+    full = u.reshape(m, p.n, p.n) if p.d == 2 else u.reshape(m, 1, p.n)
+    r = (lo0 + np.arange(w0)) % full.shape[1]
+    c = (lo1 + np.arange(w1)) % p.n
+    box = np.ascontiguousarray(full[:, r][:, :, c])
+    rest = full.copy()
+    rest[np.ix_(np.arange(m), r, c)] = 0.0
+    assert not rest.any(), "u has nonzeros outside the reported box"
+    return box
+
+
+@pytest.mark.parametrize("name,dtype", CASES, ids=[f"{a}-{b}" for a, b in CASES])
+def test_set_kernels_box_equals_set_kernels(name, dtype):
+    """pcwd_set_kernels_box (u_k given on the plan's support box) = pcwd_set_kernels with the whole u."""
+    p = _problem(name)
+    u2, v2 = _other_kernels(p, 11)
+    dec = Decomposition(_spec(p, dtype))
+    dec.set_kernels(u2, v2)
+    dec.decompose()
+    ref = _csr(dec)
+    box = _box_of(dec, p, u2)
+    assert box.shape[0] == p.u.shape[0] and box.size < u2.size or p.n <= 32
+    dec.set_kernels(p.u, p.v)              # something else in between
+    dec.decompose()
+    dec.set_kernels_box(torch.from_numpy(box).pin_memory(), torch.from_numpy(v2).pin_memory())
+    dec.decompose()
+    for a, b in zip(_csr(dec), ref):
+        assert np.array_equal(a, b)
+    dec.set_kernels_box(torch.from_numpy(box).cuda(), torch.from_numpy(v2).cuda())   # device-resident
+    got = _to_host(dec, ref)
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+    dec.close()
