@@ -996,8 +996,8 @@ __global__ void __launch_bounds__(kB) bk_write(const __grid_constant__ Plan P, c
 // windows through local_index) and the stencil entries of its level — details directly from the step
 // input (2δ × 2δ taps), the coarse block from the approximation (as bk_gather) — then the row (entries of the
 // earlier steps from the stage in the scratch) is sorted by column and written (as bk_write).
-template <typename Real, int L2>
-__global__ void __launch_bounds__(kB) bk_tail(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
+template <typename Real, int L2, int NTT>
+__global__ void __launch_bounds__(NTT) bk_tail(const __grid_constant__ Plan P, const __grid_constant__ BatchArgs A,
                                               int s0, int steps, int amax, int ymax) {
   extern __shared__ __align__(16) unsigned char tsm[];
   const int Lp = P.band_Lpad;
@@ -1016,7 +1016,7 @@ __global__ void __launch_bounds__(kB) bk_tail(const __grid_constant__ Plan P, co
   {  // step-s0 input window
     const Real* X = base + ((s0 & 1) ? S.offX0 : S.offX1);
     const int rs = rstride(in1.len);
-    for (int i = tid; i < in0.len * in1.len; i += kB) {
+    for (int i = tid; i < in0.len * in1.len; i += NTT) {
       const int r = i / in1.len, c = i - r * in1.len;
       buf0[i] = X[int64_t(r) * rs + c];
     }
@@ -1025,7 +1025,7 @@ __global__ void __launch_bounds__(kB) bk_tail(const __grid_constant__ Plan P, co
   const Real* sv = base + S.offStage;
   const int* sc = reinterpret_cast<const int*>(sv + Lp);
   const int4* st = A.stencil + S.stencil_off;
-  for (int j = tid; j < Lp; j += kB) {
+  for (int j = tid; j < Lp; j += NTT) {
     if (j >= P.band_L) { kc[j] = INT_MAX; kv[j] = Real(0); }
     else if (st[j].w < s0) { kc[j] = sc[j]; kv[j] = sv[j]; }
   }
@@ -1045,7 +1045,7 @@ __global__ void __launch_bounds__(kB) bk_tail(const __grid_constant__ Plan P, co
       };
       const int k1 = kind(in1), k0 = kind(in0);
       // axis 1: Ys[i0][l1] = Σ_t h[t] X[i0][2(a1.lo + l1) + t]
-      for (int i = tid; i < in0.len * a1.len; i += kB) {
+      for (int i = tid; i < in0.len * a1.len; i += NTT) {
         const int i0 = i / a1.len, l1 = i - i0 * a1.len;
         const int g = 2 * (a1.lo + l1);
         const Real* xr = X + i0 * in1.len;
@@ -1069,7 +1069,7 @@ __global__ void __launch_bounds__(kB) bk_tail(const __grid_constant__ Plan P, co
       }
       __syncthreads();
       // axis 0: Xn[l0][l1] = Σ_t h[t] Ys[2(a0.lo + l0) + t][l1]
-      for (int i = tid; i < a0.len * a1.len; i += kB) {
+      for (int i = tid; i < a0.len * a1.len; i += NTT) {
         const int l0 = i / a1.len, l1 = i - l0 * a1.len;
         const int g = 2 * (a0.lo + l0);
         const Real* yc = Ys + l1;
@@ -1095,7 +1095,7 @@ __global__ void __launch_bounds__(kB) bk_tail(const __grid_constant__ Plan P, co
       __syncthreads();
     }
     // stencil entries of level s
-    for (int j = tid; j < P.band_L; j += kB) {
+    for (int j = tid; j < P.band_L; j += NTT) {
       const int4 e = st[j];
       if (e.w != s) continue;
       const SubBand& L = P.sb[e.x];
@@ -1138,11 +1138,11 @@ __global__ void __launch_bounds__(kB) bk_tail(const __grid_constant__ Plan P, co
   // the torus; then each entry goes to its rank (columns are distinct)
   const int L = P.band_L;
   int unsorted = 0;
-  for (int i = tid; i + 1 < L; i += kB) unsorted |= kc[i] > kc[i + 1];
+  for (int i = tid; i + 1 < L; i += NTT) unsorted |= kc[i] > kc[i + 1];
   unsorted = __syncthreads_or(unsorted);
   const int64_t row = (unit - A.row0) * L;
   Real* outv = reinterpret_cast<Real*>(A.val);
-  for (int i = tid; i < L; i += kB) {
+  for (int i = tid; i < L; i += NTT) {
     const int c = kc[i];
     int rank = i;
     if (unsorted) {
@@ -1314,19 +1314,28 @@ static cudaError_t run_batch_t(const Plan& P, const BatchArgs& A0, int64_t maxX0
       const int64_t ymax = appr0[s0 - 1] * appr1[s0];
       const size_t sm = ((P.band_Lpad * 4 + 15) & ~15) + size_t((P.band_Lpad + 3) & ~3) * sizeof(Real) +
                         size_t(2 * amax + ymax) * sizeof(Real);
-      auto launch_tail = [&](auto kern) {
+      // threads per unit: 128 for launches of many units (more resident CTAs; c5 level 4, 12,288 units: 297 ->
+      // 210 us), 256 for fewer (c5 levels 5-8 are slower at 128); PCWD_TAIL_NT = 64 / 128 / 256 forces one
+      static const int tnt_env = getenv("PCWD_TAIL_NT") ? atoi(getenv("PCWD_TAIL_NT")) : 0;
+      const int tnt = tnt_env ? tnt_env : (nb >= 148 * 32 ? 128 : 256);
+      auto launch_tail = [&](auto kern, int nt) {
         if (sm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        kern<<<nb, kB, sm, st>>>(P, A, s0, steps, int(amax), int(ymax));
+        kern<<<nb, nt, sm, st>>>(P, A, s0, steps, int(amax), int(ymax));
       };
+#define PCWD_TAIL(L2V)                                                            \
+  if (tnt == 64) launch_tail(bk_tail<Real, L2V, 64>, 64);                         \
+  else if (tnt == 128) launch_tail(bk_tail<Real, L2V, 128>, 128);                 \
+  else launch_tail(bk_tail<Real, L2V, 256>, 256);
       switch (P.L2) {
-        case 2: launch_tail(bk_tail<Real, 2>); break;
-        case 4: launch_tail(bk_tail<Real, 4>); break;
-        case 6: launch_tail(bk_tail<Real, 6>); break;
-        case 8: launch_tail(bk_tail<Real, 8>); break;
-        case 10: launch_tail(bk_tail<Real, 10>); break;
-        case 12: launch_tail(bk_tail<Real, 12>); break;
+        case 2: PCWD_TAIL(2) break;
+        case 4: PCWD_TAIL(4) break;
+        case 6: PCWD_TAIL(6) break;
+        case 8: PCWD_TAIL(8) break;
+        case 10: PCWD_TAIL(10) break;
+        case 12: PCWD_TAIL(12) break;
         default: return cudaErrorInvalidValue;
       }
+#undef PCWD_TAIL
       ++*launches;
     } else {
       const size_t sm = ((P.band_Lpad * 4 + 15) & ~15) + size_t(P.band_Lpad) * sizeof(Real);

@@ -42,6 +42,8 @@ SWITCHES = [
     {"PCWD_FINE_DIRECT": "1,1,1"},
     {"PCWD_NO_FINE": "1", "PCWD_NO_TILE": "1", "PCWD_NO_BATCHED": "1"},
     {"PCWD_SEP": "7"},
+    {"PCWD_TAIL_NT": "128"},
+    {"PCWD_TAIL_NT": "64"},
 ]
 
 
