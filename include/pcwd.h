@@ -238,6 +238,17 @@ int pcwd_operator_apply(void* handle, const void* x, void* y, int adjoint, void*
  * demand and the C1 cross-check.  Synchronous. */
 int pcwd_columns(void* handle, const int64_t* lambdas, int64_t count, double* out, void* stream);
 
+/* The d = 3 variant (the grid is N_1 × … × N_d): rows of Θ = Ψ* H Ψ on the
+ * periodic n × n × n grid, Θ[μ][·] = Ψ*(H* ψ_μ), H f = Σ_k u_k ⋆ (v_k ⊙ f) (R9), in the separable basis of
+ * P:110-119 with axis 0 filtered first, then axis 1, then axis 2.  Λ layout: the (n >> levels)³ coarse block, then
+ * levels J..1, orientations e = 4 e0 + 2 e1 + e2 = 1..7, positions row-major.  A handle-free call: n a power of two
+ * ≤ 256; h: HOST, `taps` values of an orthogonal low-pass filter (else PCWD_E_CONFIG); u, v: DEVICE, m × n³ fp64,
+ * u_k(z) at index z mod n, row-major (z0, z1, z2); units: HOST or DEVICE, `count` Λ indices in [0, n³) (else
+ * PCWD_E_PARAM); out: DEVICE, count × n³ fp64 allocated by the caller (row i = row units[i] of Θ).  Computes in fp64
+ * with whole-torus passes (no windowing); allocates and frees its scratch; synchronous. */
+int pcwd_rows3d(int32_t n, int32_t levels, const double* h, int32_t taps, int32_t m, const double* u, const double* v,
+                const int64_t* units, int64_t count, double* out, void* stream);
+
 /* ---- constructing the product-convolution expansion (§3.3) ------------------
  * Both factor impulse responses given on the window [−R, R]^d around the origin (W = (2R+1)^d values per response,
  * row-major over the offsets (z0, z1) = (a − R, b − R); 2R + 1 ≤ n): u_k = the m leading left singular vectors of

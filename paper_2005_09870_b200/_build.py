@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpcwd.so")
 OBJ = os.path.join(CSRC, "obj")
-SOURCES = ["api.cu", "kernels.cu", "band_tile.cu", "batched.cu", "fine.cu", "fista.cu", "approx.cu", "pca.cu", "sort.cu", "plan.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "band_tile.cu", "batched.cu", "fine.cu", "fista.cu", "approx.cu", "pca.cu", "sort.cu", "volume.cu", "plan.cpp"]
 HEADERS = ["common.h", "kernels.cuh", "plan.h", "geom.h", "tma.h"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]

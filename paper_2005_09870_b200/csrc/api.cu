@@ -1764,6 +1764,41 @@ int pcwd_pc_from_svir(int32_t d, int32_t n, int32_t R, int32_t m, const double* 
                    static_cast<cudaStream_t>(stream));
 }
 
+int pcwd_rows3d(int32_t n, int32_t levels, const double* h, int32_t taps, int32_t m, const double* u, const double* v,
+                const int64_t* units, int64_t count, double* out, void* stream) {
+  if (n < 2 || n > 256 || (n & (n - 1))) return fail(PCWD_E_SHAPE, "pcwd_rows3d: n must be a power of two in [2, 256]");
+  int lg = 0;
+  while ((1 << lg) < n) ++lg;
+  if (levels < 1 || levels > lg) return fail(PCWD_E_CONFIG, "pcwd_rows3d: levels must be in [1, log2 n]");
+  if (taps < 2 || taps > kMaxTaps || (taps & 1)) return fail(PCWD_E_CONFIG, "pcwd_rows3d: taps must be even, 2..20");
+  if (!h || !u || !v || m < 1 || count < 0 || (count > 0 && (!units || !out))) return fail(PCWD_E_PARAM, "pcwd_rows3d: NULL argument or m < 1");
+  double s1 = 0.0;   // an orthogonal wavelet filter, as pcwd_validate checks it
+  for (int i = 0; i < taps; ++i) s1 += h[i];
+  if (std::fabs(s1 - std::sqrt(2.0)) > 1e-9) return fail(PCWD_E_CONFIG, "pcwd_rows3d: h must sum to sqrt(2)");
+  for (int k = 0; 2 * k < taps; ++k) {
+    double a = 0.0;
+    for (int i = 0; i + 2 * k < taps; ++i) a += h[i] * h[i + 2 * k];
+    if (std::fabs(a - (k == 0 ? 1.0 : 0.0)) > 1e-9) return fail(PCWD_E_CONFIG, "pcwd_rows3d: h is not an orthogonal wavelet filter");
+  }
+  if (!is_device_ptr(u) || !is_device_ptr(v) || (count > 0 && !is_device_ptr(out)))
+    return fail(PCWD_E_PARAM, "pcwd_rows3d: u, v and out must be device pointers");
+  const int64_t N = int64_t(n) * n * n;
+  std::vector<int64_t> uh(count);
+  if (count > 0) CK(cudaMemcpy(uh.data(), units, count * sizeof(int64_t), cudaMemcpyDefault));
+  for (int64_t i = 0; i < count; ++i)
+    if (uh[i] < 0 || uh[i] >= N) return fail(PCWD_E_PARAM, "pcwd_rows3d: unit index out of range");
+  if (count == 0) return PCWD_OK;
+  int64_t* ud = nullptr;
+  CK(cudaMalloc(&ud, count * sizeof(int64_t)));
+  cudaError_t e = cudaMemcpy(ud, uh.data(), count * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaError_t(pcwd_vol::rows3d(n, levels, h, taps, m, u, v, ud, count, out, static_cast<cudaStream_t>(stream)));
+  cudaFree(ud);
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? PCWD_E_OOM : PCWD_E_CUDA, std::string("pcwd_rows3d: ") + cudaGetErrorString(e));
+  return PCWD_OK;
+}
+
 int pcwd_approx(void* handle, double eta, int rule, void* stream, pcwd_approx_info* out) {
   Handle* h = static_cast<Handle*>(handle);
   if (!h) return fail(PCWD_E_PARAM, "NULL handle");

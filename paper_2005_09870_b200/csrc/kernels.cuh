@@ -289,3 +289,9 @@ int factor(const double* X, int64_t s, int W, int m, int oversample, int power_i
            double* c, double* sigma, cudaStream_t st);
 int finish(const double* U, const double* c, int d, int n, int R, int g, int m, double* u, double* v, cudaStream_t st);
 }  // namespace pcwd_pca
+
+// volume.cu: the d = 3 variant — rows of Θ on the n³ torus (see the file header).  Returns a cudaError_t as int.
+namespace pcwd_vol {
+int rows3d(int n, int J, const double* h, int taps, int m, const double* u, const double* v, const int64_t* units,
+           int64_t count, double* out, cudaStream_t st);
+}  // namespace pcwd_vol

@@ -61,7 +61,7 @@ EXPORTS = ["pcwd_create", "pcwd_decompose", "pcwd_local_max", "pcwd_set_global_m
            "pcwd_plan_num_subbands", "pcwd_profile", "pcwd_phase_times", "pcwd_launch_profile",
            "pcwd_set_kernels", "pcwd_decompose_to_host", "pcwd_wavelet_transform", "pcwd_fista",
            "pcwd_fista_sharded", "pcwd_approx", "pcwd_operator_apply", "pcwd_pc_from_samples", "pcwd_pc_from_svir", "pcwd_columns",
-           "pcwd_plan_atom", "pcwd_kernel_box", "pcwd_set_kernels_box"]
+           "pcwd_plan_atom", "pcwd_kernel_box", "pcwd_set_kernels_box", "pcwd_rows3d"]
 
 REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_void_p)   # pcwd_reduce_fn
 _lib = None
@@ -109,6 +109,7 @@ def lib():
         L.pcwd_pc_from_samples.argtypes = [i32, i32, i32, i32, i32, vp, vp, vp, vp, vp]
         L.pcwd_columns.argtypes = [vp, vp, ctypes.c_int64, vp, vp]
         L.pcwd_pc_from_svir.argtypes = [i32, i32, i32, i32, vp, i32, i32, ctypes.c_uint64, vp, vp, vp, vp]
+        L.pcwd_rows3d.argtypes = [i32, i32, vp, i32, i32, vp, vp, vp, ctypes.c_int64, vp, vp]
         for f in EXPORTS:
             getattr(L, f)  # every declared symbol must exist
         _lib = L
@@ -571,3 +572,17 @@ def num_subbands(spec: Spec) -> int:
     out = ctypes.c_int32()
     _check(lib().pcwd_plan_num_subbands(ctypes.byref(d), ctypes.byref(out)), "pcwd_plan_num_subbands")
     return out.value
+
+
+def rows3d(n: int, levels: int, h, u, v, units, stream: int = 0):
+    """d = 3 (pcwd_rows3d): rows `units` of Θ on the n³ torus.  u, v: (m, n³) torch.float64 CUDA tensors; returns a
+    (len(units), n³) torch.float64 CUDA tensor."""
+    import torch
+    h = np.ascontiguousarray(h, dtype=np.float64)
+    units = np.ascontiguousarray(units, dtype=np.int64)
+    assert u.is_cuda and v.is_cuda and u.dtype == torch.float64 and v.dtype == torch.float64
+    out = torch.empty((len(units), n ** 3), dtype=torch.float64, device=u.device)
+    _check(lib().pcwd_rows3d(n, levels, ctypes.c_void_p(_ptr(h)), len(h), u.shape[0], ctypes.c_void_p(_ptr(u)),
+                             ctypes.c_void_p(_ptr(v)), ctypes.c_void_p(_ptr(units)), len(units),
+                             ctypes.c_void_p(_ptr(out)), ctypes.c_void_p(stream)), "pcwd_rows3d")
+    return out
