@@ -1788,11 +1788,17 @@ int pcwd_rows3d(int32_t n, int32_t levels, const double* h, int32_t taps, int32_
   for (int64_t i = 0; i < count; ++i)
     if (uh[i] < 0 || uh[i] >= N) return fail(PCWD_E_PARAM, "pcwd_rows3d: unit index out of range");
   if (count == 0) return PCWD_OK;
+  // coarse units (low Λ indices: the widest supports) first, the CTAs take units from a counter as they finish
+  std::vector<int64_t> order(count);
+  for (int64_t i = 0; i < count; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return uh[a] < uh[b]; });
+  uh.insert(uh.end(), order.begin(), order.end());
   int64_t* ud = nullptr;
-  CK(cudaMalloc(&ud, count * sizeof(int64_t)));
-  cudaError_t e = cudaMemcpy(ud, uh.data(), count * sizeof(int64_t), cudaMemcpyHostToDevice);
+  CK(cudaMalloc(&ud, 2 * count * sizeof(int64_t)));
+  cudaError_t e = cudaMemcpy(ud, uh.data(), 2 * count * sizeof(int64_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
-    e = cudaError_t(pcwd_vol::rows3d(n, levels, h, taps, m, u, v, ud, count, out, static_cast<cudaStream_t>(stream)));
+    e = cudaError_t(pcwd_vol::rows3d(n, levels, h, taps, m, u, v, ud, ud + count, count, out,
+                                     static_cast<cudaStream_t>(stream)));
   cudaFree(ud);
   if (e != cudaSuccess)
     return fail(e == cudaErrorMemoryAllocation ? PCWD_E_OOM : PCWD_E_CUDA, std::string("pcwd_rows3d: ") + cudaGetErrorString(e));

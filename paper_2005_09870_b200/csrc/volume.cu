@@ -1,8 +1,9 @@
 // d = 3 variant: rows of Θ = Ψ* H Ψ on the periodic n × n × n grid.
 //
-// Row μ is Ψ*(H* ψ_μ) (R1; H* g = Σ_k v_k ⊙ (ũ_k ⋆ g), R9).  One CTA per unit, the unit's two n³ work arrays in a
-// global scratch slice (they stay in L2 for the sizes this path is meant for):
-//   1. ψ_μ = Ψ e_μ by the synthesis cascade (P:94-96 transposed), axes undone in the order 2, 1, 0 per level;
+// Row μ is Ψ*(H* ψ_μ) (R1; H* g = Σ_k v_k ⊙ (ũ_k ⋆ g), R9).  One CTA per unit, the unit's two n³ work arrays (the
+// analysis cascade's ping-pong) in a global scratch slice:
+//   1. ψ_μ = Ψ e_μ = f_0 ⊗ f_1 ⊗ f_2 (tensor-product basis): three 1-D synthesis cascades (P:94-96
+//      transposed) in shared memory;
 //   2. w(y) = Σ_k v_k(y) Σ_c u_k(c) ψ_μ((y + c) mod n) over the cyclic support box of the u_k, skipping the
 //      (x0, x1) lines on which ψ_μ is identically zero;
 //   3. c = Ψ* w by the analysis cascade, axis 0 first (R6 carried to three axes), written in the Λ layout
@@ -26,6 +27,8 @@ struct Args {
   const double* u;
   const double* v;
   const int64_t* units;
+  const int64_t* order;         // positions into units, most expensive (coarsest, lowest Λ index) first
+  unsigned long long* next;     // launch-wide counter: CTAs take the next position as they finish
   int64_t count;
   double* out;
   double* scratch;              // 2 n³ doubles per CTA
@@ -43,41 +46,49 @@ __global__ void support_kernel(const double* u, int64_t total, int n, int* rad) 
   }
 }
 
-// One analysis step along axis `ax` of a cube of side s (power of two): out holds a | d concatenated on that axis.
-__device__ void analysis_pass(const Args& A, const double* __restrict__ x, double* __restrict__ y, int s, int ax) {
+// Index lists of three 1-D masks (one warp per axis, ballot compaction); all threads of the CTA call it.
+__device__ void build_lists(const unsigned char (*mask)[256], int len, short (*list)[256], int* cnt) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w < 3) {
+    int base = 0;
+    for (int c = 0; c < len; c += 32) {
+      const int i = c + lane;
+      const bool on = i < len && mask[w][i];
+      const unsigned b = __ballot_sync(0xffffffffu, on);
+      if (on) list[w][base + __popc(b & ((1u << lane) - 1u))] = short(i);
+      base += __popc(b);
+    }
+    if (lane == 0) cnt[w] = base;
+  }
+  __syncthreads();
+}
+
+// One analysis step along axis `ax` of a cube of side s (power of two), out = a | d concatenated on that axis,
+// restricted to a product set: outputs (i0, i1, i2) ∈ L0 × L1 × L2 only, inputs read where `min` (the input's mask
+// along `ax`) is set — everything off the product set is an exact zero that is neither stored nor loaded.
+__device__ void analysis_pass(const Args& A, const double* __restrict__ x, double* __restrict__ y, int s, int ax,
+                              const short* L0, int c0, const short* L1, int c1, const short* L2, int c2,
+                              const unsigned char* min) {
   const int half = s >> 1, mask = s - 1;
   const int stride = ax == 0 ? s * s : (ax == 1 ? s : 1);
-  const int total = s * s * s;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int i = (idx / stride) & mask;
+  const int total = c0 * c1 * c2;
+  for (int q = threadIdx.x; q < total; q += blockDim.x) {
+    const int i2 = L2[q % c2], i1 = L1[(q / c2) % c1], i0 = L0[q / (c2 * c1)];
+    const int idx = (i0 * s + i1) * s + i2;
+    const int i = ax == 0 ? i0 : (ax == 1 ? i1 : i2);
     const double* line = x + (idx - i * stride);
     double acc = 0.0;
     if (i < half) {
-      for (int t = 0; t < A.taps; ++t) acc += A.h[t] * line[((2 * i + t) & mask) * stride];
+      for (int t = 0; t < A.taps; ++t) {
+        const int xi = (2 * i + t) & mask;
+        if (min[xi]) acc += A.h[t] * line[xi * stride];
+      }
     } else {
       const int l = i - half;
-      for (int j = 0; j < A.taps; ++j) acc += A.g[j] * line[((2 * l + 2 - A.taps + j) & mask) * stride];
-    }
-    y[idx] = acc;
-  }
-}
-
-// The adjoint step: x holds a | d on axis `ax`; y[i] = Σ_{(2l+t) ≡ i} h[t] a[l] + Σ_{(2l+o) ≡ i} g[o] d[l].
-__device__ void synthesis_pass(const Args& A, const double* __restrict__ x, double* __restrict__ y, int s, int ax) {
-  const int half = s >> 1, mask = s - 1;
-  const int stride = ax == 0 ? s * s : (ax == 1 ? s : 1);
-  const int total = s * s * s;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int i = (idx / stride) & mask;
-    const double* line = x + (idx - i * stride);
-    double acc = 0.0;
-    for (int t = 0; t < A.taps; ++t) {
-      const int r = i - t;
-      if ((r & 1) == 0) acc += A.h[t] * line[((r & mask) >> 1) * stride];
-    }
-    for (int j = 0; j < A.taps; ++j) {
-      const int r = i - (2 - A.taps + j);
-      if ((r & 1) == 0) acc += A.g[j] * line[(half + ((r & mask) >> 1)) * stride];
+      for (int j = 0; j < A.taps; ++j) {
+        const int xi = (2 * l + 2 - A.taps + j) & mask;
+        if (min[xi]) acc += A.g[j] * line[xi * stride];
+      }
     }
     y[idx] = acc;
   }
@@ -97,80 +108,111 @@ __device__ __forceinline__ int64_t subband_offset(int n, int J, int lev, int e) 
 __global__ void __launch_bounds__(512) rows3d_kernel(const Args A) {
   const int n = A.n, J = A.J;
   const int64_t N = int64_t(n) * n * n;
-  __shared__ unsigned linemask[2048];   // one bit per (x0, x1) line of the torus, n ≤ 256
-  __shared__ unsigned outmask[2048];
+  __shared__ unsigned char S[3][256];    // supp f_a
+  __shared__ unsigned char M[3][256];    // per-axis support of the cascade's current input (a product set)
+  __shared__ unsigned char P[3][256];    // … of the current level's output (a | d coordinates)
+  __shared__ short LM[3][256], LP[3][256];
+  __shared__ int cM[3], cP[3];
+  __shared__ double fa[3][256], fb[3][256];   // the 1-D factors of ψ_μ (ping-pong)
+  double (*f)[256] = fa;
   double* X = A.scratch + 2 * N * blockIdx.x;
   double* Y = X + N;
-  for (int64_t ui = blockIdx.x; ui < A.count; ui += gridDim.x) {
+  __shared__ unsigned long long taken;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) taken = atomicAdd(A.next, 1ull);
+    __syncthreads();
+    if (taken >= (unsigned long long)A.count) break;
+    const int64_t ui = A.order[taken];
     const int64_t mu = A.units[ui];
-    // 1. ψ_μ = Ψ e_μ
+    // 1. ψ_μ = Ψ e_μ is a tensor product: ψ_μ(x) = f_0(x0) f_1(x1) f_2(x2), f_a = the 1-D scaling
+    //    function (e_a = 0) or wavelet (e_a = 1) of level ℓ at position l_a — three 1-D synthesis cascades in shared
+    //    memory instead of the 3-D one; ψ_μ is never written out.
+    int lev = J, e = 0;
+    int64_t pos = mu;
     {
-      const int nJ = n >> J;
-      for (int i = threadIdx.x; i < nJ * nJ * nJ; i += blockDim.x) X[i] = (i == mu) ? 1.0 : 0.0;
-      __syncthreads();
-      for (int lev = J; lev >= 1; --lev) {
-        const int nl = n >> lev, s = 2 * nl;
-        const int64_t base = subband_offset(n, J, lev, 1);
-        const int64_t cube = int64_t(nl) * nl * nl;
-        for (int idx = threadIdx.x; idx < s * s * s; idx += blockDim.x) {
-          const int i0 = idx / (s * s), i1 = (idx / s) % s, i2 = idx % s;
-          const int e = (i0 >= nl ? 4 : 0) | (i1 >= nl ? 2 : 0) | (i2 >= nl ? 1 : 0);
-          const int pos = ((i0 % nl) * nl + (i1 % nl)) * nl + (i2 % nl);
-          Y[idx] = e == 0 ? X[pos] : ((base + (e - 1) * cube + pos == mu) ? 1.0 : 0.0);
-        }
-        __syncthreads();
-        synthesis_pass(A, Y, X, s, 2);
-        __syncthreads();
-        synthesis_pass(A, X, Y, s, 1);
-        __syncthreads();
-        synthesis_pass(A, Y, X, s, 0);
-        __syncthreads();
-      }
-    }
-    // 2. w = H* ψ_μ.  ψ_μ is exactly zero off its support (a fine-level wavelet fills a few (x0, x1) lines of the
-    //    torus): lines without a nonzero are skipped — they would add exact zeros.
-    {
-      const int mask = n - 1;
-      for (int i = threadIdx.x; i < (n * n + 31) / 32; i += blockDim.x) linemask[i] = 0u;
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < N; idx += blockDim.x)
-        if (X[idx] != 0.0) atomicOr(&linemask[(idx / n) >> 5], 1u << ((idx / n) & 31));
-      __syncthreads();
-      // output lines (y0, y1) that see a nonzero line through the box; the others are exact zeros
-      for (int i = threadIdx.x; i < (n * n + 31) / 32; i += blockDim.x) outmask[i] = 0u;
-      __syncthreads();
-      for (int l = threadIdx.x; l < n * n; l += blockDim.x) {
-        const int y0 = l / n, y1 = l & mask;
-        bool any = false;
-        for (int a = 0; a < A.cnt[0] && !any; ++a) {
-          const int x0 = (y0 + A.lo[0] + a) & mask;
-          for (int b = 0; b < A.cnt[1]; ++b) {
-            const int line = x0 * n + ((y1 + A.lo[1] + b) & mask);
-            if ((linemask[line >> 5] >> (line & 31)) & 1u) { any = true; break; }
+      const int64_t nJ = n >> J;
+      if (mu >= nJ * nJ * nJ) {
+        for (lev = J; lev >= 1; --lev) {
+          const int64_t nl = n >> lev, cube = nl * nl * nl, base = subband_offset(n, J, lev, 1);
+          if (mu < base + 7 * cube) {
+            e = 1 + int((mu - base) / cube);
+            pos = (mu - base) % cube;
+            break;
           }
         }
-        if (any) atomicOr(&outmask[l >> 5], 1u << (l & 31));
+      }
+    }
+    {
+      const int nl = n >> lev;
+      const int l3[3] = {int(pos / (int64_t(nl) * nl)), int(pos / nl) % nl, int(pos % nl)};
+      double (*src)[256] = fa, (*dst)[256] = fb;
+      for (int idx = threadIdx.x; idx < 3 * nl; idx += blockDim.x) {
+        const int a = idx / nl, i = idx % nl;
+        src[a][i] = (i == (a == 0 ? l3[0] : (a == 1 ? l3[1] : l3[2]))) ? 1.0 : 0.0;
       }
       __syncthreads();
-      for (int y = threadIdx.x; y < N; y += blockDim.x) {
-        const int y0 = y / (n * n), y1 = (y / n) & mask, y2 = y & mask;
-        if (!((outmask[(y / n) >> 5] >> ((y / n) & 31)) & 1u)) { Y[y] = 0.0; continue; }
+      for (int lv = lev; lv >= 1; --lv) {
+        const int s = 2 * (n >> lv), smask = s - 1;
+        for (int idx = threadIdx.x; idx < 3 * s; idx += blockDim.x) {
+          const int a = idx / s, i = idx % s;
+          const bool detail = lv == lev && ((e >> (2 - a)) & 1);
+          double acc = 0.0;
+          if (detail) {
+            for (int j = 0; j < A.taps; ++j) {
+              const int r = i - (2 - A.taps + j);
+              if ((r & 1) == 0) acc += A.g[j] * src[a][(r & smask) >> 1];
+            }
+          } else {
+            for (int t = 0; t < A.taps; ++t) {
+              const int r = i - t;
+              if ((r & 1) == 0) acc += A.h[t] * src[a][(r & smask) >> 1];
+            }
+          }
+          dst[a][i] = acc;
+        }
+        __syncthreads();
+        double (*tmp)[256] = src; src = dst; dst = tmp;
+      }
+      f = src;
+    }
+    // 2. w = H* ψ_μ on its support only.  supp ψ_μ = S_0 × S_1 × S_2 (S_a = supp f_a) is a product set, so supp w ⊂
+    //    O_0 × O_1 × O_2 with O_a = S_a dilated by the box; everything else is an exact zero and is never touched.
+    double* row = A.out + ui * N;
+    {
+      const int mask = n - 1;
+      for (int64_t i = threadIdx.x; i < N; i += blockDim.x) row[i] = 0.0;
+      for (int idx = threadIdx.x; idx < 3 * n; idx += blockDim.x) S[idx / n][idx % n] = f[idx / n][idx % n] != 0.0;
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < 3 * n; idx += blockDim.x) {
+        const int a = idx / n, y = idx % n;
+        bool any = false;
+        for (int c = 0; c < A.cnt[a]; ++c) any |= S[a][(y + A.lo[a] + c) & mask] != 0;
+        M[a][y] = any;
+      }
+      __syncthreads();
+      build_lists(M, n, LM, cM);
+      const int c0 = cM[0], c1 = cM[1], c2 = cM[2];
+      for (int q = threadIdx.x; q < c0 * c1 * c2; q += blockDim.x) {
+        const int y2 = LM[2][q % c2], y1 = LM[1][(q / c2) % c1], y0 = LM[0][q / (c2 * c1)];
+        const int y = (y0 * n + y1) * n + y2;
         double acc = 0.0;
         for (int k = 0; k < A.m; ++k) {
           const double* uk = A.u + k * N;
           double s = 0.0;
           for (int a = 0; a < A.cnt[0]; ++a) {
-            const int c0 = (A.lo[0] + a) & mask, x0 = (y0 + c0) & mask;
+            const int c0i = (A.lo[0] + a) & mask, x0 = (y0 + c0i) & mask;
+            if (!S[0][x0]) continue;
             for (int b = 0; b < A.cnt[1]; ++b) {
-              const int c1 = (A.lo[1] + b) & mask, x1 = (y1 + c1) & mask;
-              const int line = x0 * n + x1;
-              if (!((linemask[line >> 5] >> (line & 31)) & 1u)) continue;
-              const double* ur = uk + (c0 * n + c1) * n;
-              const double* xr = X + (x0 * n + x1) * n;
+              const int c1i = (A.lo[1] + b) & mask, x1 = (y1 + c1i) & mask;
+              if (!S[1][x1]) continue;
+              const double* ur = uk + (c0i * n + c1i) * n;
+              double t = 0.0;
               for (int c = 0; c < A.cnt[2]; ++c) {
-                const int c2 = (A.lo[2] + c) & mask;
-                s += ur[c2] * xr[(y2 + c2) & mask];
+                const int c2i = (A.lo[2] + c) & mask;
+                t += ur[c2i] * f[2][(y2 + c2i) & mask];
               }
+              s += (f[0][x0] * f[1][x1]) * t;
             }
           }
           acc += A.v[k * N + y] * s;
@@ -179,39 +221,58 @@ __global__ void __launch_bounds__(512) rows3d_kernel(const Args A) {
       }
       __syncthreads();
     }
-    // 3. c = Ψ* w
+    // 3. c = Ψ* w, each pass on the product set its outputs can be nonzero on
     {
-      double* row = A.out + ui * N;
-      for (int lev = 1; lev <= J; ++lev) {
-        const int s = n >> (lev - 1), nl = s >> 1;
-        analysis_pass(A, Y, X, s, 0);
-        __syncthreads();
-        analysis_pass(A, X, Y, s, 1);
-        __syncthreads();
-        analysis_pass(A, Y, X, s, 2);
-        __syncthreads();
-        const int64_t base = subband_offset(n, J, lev, 1);
-        const int64_t cube = int64_t(nl) * nl * nl;
-        for (int idx = threadIdx.x; idx < s * s * s; idx += blockDim.x) {
-          const int i0 = idx / (s * s), i1 = (idx / s) % s, i2 = idx % s;
-          const int e = (i0 >= nl ? 4 : 0) | (i1 >= nl ? 2 : 0) | (i2 >= nl ? 1 : 0);
-          const int pos = ((i0 % nl) * nl + (i1 % nl)) * nl + (i2 % nl);
-          if (e == 0) Y[pos] = X[idx];
-          else row[base + (e - 1) * cube + pos] = X[idx];
+      for (int lv = 1; lv <= J; ++lv) {
+        const int s = n >> (lv - 1), nl = s >> 1, smask = s - 1;
+        for (int idx = threadIdx.x; idx < 3 * s; idx += blockDim.x) {
+          const int a = idx / s, i = idx % s;
+          bool any = false;
+          if (i < nl) {
+            for (int t = 0; t < A.taps; ++t) any |= M[a][(2 * i + t) & smask] != 0;
+          } else {
+            for (int j = 0; j < A.taps; ++j) any |= M[a][(2 * (i - nl) + 2 - A.taps + j) & smask] != 0;
+          }
+          P[a][i] = any;
         }
         __syncthreads();
+        build_lists(P, s, LP, cP);
+        analysis_pass(A, Y, X, s, 0, LP[0], cP[0], LM[1], cM[1], LM[2], cM[2], M[0]);
+        __syncthreads();
+        analysis_pass(A, X, Y, s, 1, LP[0], cP[0], LP[1], cP[1], LM[2], cM[2], M[1]);
+        __syncthreads();
+        analysis_pass(A, Y, X, s, 2, LP[0], cP[0], LP[1], cP[1], LP[2], cP[2], M[2]);
+        __syncthreads();
+        const int64_t base = subband_offset(n, J, lv, 1);
+        const int64_t cube = int64_t(nl) * nl * nl;
+        const int c0 = cP[0], c1 = cP[1], c2 = cP[2];
+        for (int q = threadIdx.x; q < c0 * c1 * c2; q += blockDim.x) {
+          const int i2 = LP[2][q % c2], i1 = LP[1][(q / c2) % c1], i0 = LP[0][q / (c2 * c1)];
+          const int e = (i0 >= nl ? 4 : 0) | (i1 >= nl ? 2 : 0) | (i2 >= nl ? 1 : 0);
+          const int pos = ((i0 % nl) * nl + (i1 % nl)) * nl + (i2 % nl);
+          const double val = X[(i0 * s + i1) * s + i2];
+          if (e == 0) Y[pos] = val;
+          else row[base + (e - 1) * cube + pos] = val;
+        }
+        for (int idx = threadIdx.x; idx < 3 * nl; idx += blockDim.x) M[idx / nl][idx % nl] = P[idx / nl][idx % nl];
+        __syncthreads();
+        build_lists(M, nl, LM, cM);
       }
       const int nJ = n >> J;
-      for (int i = threadIdx.x; i < nJ * nJ * nJ; i += blockDim.x) row[i] = Y[i];
+      const int c0 = cM[0], c1 = cM[1], c2 = cM[2];
+      for (int q = threadIdx.x; q < c0 * c1 * c2; q += blockDim.x) {
+        const int i = (LM[0][q / (c2 * c1)] * nJ + LM[1][(q / c2) % c1]) * nJ + LM[2][q % c2];
+        row[i] = Y[i];
+      }
       __syncthreads();
     }
   }
 }
 
-// units, u, v, out: DEVICE.  h: HOST.  Returns a cudaError_t as int (0 = success); synchronises `st` once (the
+// units, order, u, v, out: DEVICE.  h: HOST.  Returns a cudaError_t as int (0 = success); synchronises `st` once (the
 // support box comes back to the host before the launch).
 int rows3d(int n, int J, const double* h, int taps, int m, const double* u, const double* v, const int64_t* units,
-           int64_t count, double* out, cudaStream_t st) {
+           const int64_t* order, int64_t count, double* out, cudaStream_t st) {
   if (count == 0) return 0;
   Args A{};
   A.n = n; A.J = J; A.taps = taps; A.m = m;
@@ -220,20 +281,20 @@ int rows3d(int n, int J, const double* h, int taps, int m, const double* u, cons
     const int i = 2 - taps + j;                       // g[i] = (−1)^{1−i} h[1−i]
     A.g[j] = (((1 - i) & 1) ? -1.0 : 1.0) * h[1 - i];
   }
-  A.u = u; A.v = v; A.units = units; A.count = count; A.out = out;
+  A.u = u; A.v = v; A.units = units; A.order = order; A.count = count; A.out = out;
   const int64_t N = int64_t(n) * n * n;
   int* rad = nullptr;
-  cudaError_t e = cudaMalloc(&rad, 3 * sizeof(int));
+  cudaError_t e = cudaMalloc(&rad, 8 * sizeof(int));   // [0..2] support radii, [4..5] the unit counter
   if (e != cudaSuccess) return int(e);
   int rh[3] = {0, 0, 0};
-  e = cudaMemsetAsync(rad, 0, 3 * sizeof(int), st);
+  e = cudaMemsetAsync(rad, 0, 8 * sizeof(int), st);
   if (e == cudaSuccess) {
     support_kernel<<<296, 256, 0, st>>>(u, m * N, n, rad);
     e = cudaMemcpyAsync(rh, rad, 3 * sizeof(int), cudaMemcpyDeviceToHost, st);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  cudaFree(rad);
-  if (e != cudaSuccess) return int(e);
+  if (e != cudaSuccess) { cudaFree(rad); return int(e); }
+  A.next = reinterpret_cast<unsigned long long*>(rad + 4);
   for (int a = 0; a < 3; ++a) {
     const bool whole = 2 * rh[a] + 1 >= n;
     A.lo[a] = whole ? 0 : -rh[a];
@@ -244,12 +305,13 @@ int rows3d(int n, int J, const double* h, int taps, int m, const double* u, cons
   ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t(2) << 30) / per_cta));
   double* scratch = nullptr;
   e = cudaMalloc(&scratch, size_t(ctas * per_cta));
-  if (e != cudaSuccess) return int(e);
+  if (e != cudaSuccess) { cudaFree(rad); return int(e); }
   A.scratch = scratch;
   rows3d_kernel<<<unsigned(ctas), 512, 0, st>>>(A);
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFree(scratch);
+  cudaFree(rad);
   return int(e);
 }
 

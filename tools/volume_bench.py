@@ -13,7 +13,7 @@ from paper_2005_09870_b200 import pcwd  # noqa: E402
 from synth.filters import daubechies  # noqa: E402
 from synth.volume import volume_problem  # noqa: E402
 
-for n, J, M, m, R, count in ((32, 3, 4, 4, 2, 1184), (64, 4, 4, 4, 2, 592)):
+for n, J, M, m, R, count in ((32, 3, 4, 4, 2, 1184), (32, 3, 4, 4, 2, 18944), (64, 4, 4, 4, 2, 592), (64, 4, 4, 4, 2, 4736)):
     h = daubechies(M)
     u, v = volume_problem(n, m, R, 7)
     ud, vd = torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda()
