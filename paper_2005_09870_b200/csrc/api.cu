@@ -1792,12 +1792,14 @@ int pcwd_rows3d(int32_t n, int32_t levels, const double* h, int32_t taps, int32_
   std::vector<int64_t> order(count);
   for (int64_t i = 0; i < count; ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return uh[a] < uh[b]; });
+  std::vector<int64_t> sorted_mu(count);
+  for (int64_t i = 0; i < count; ++i) sorted_mu[i] = uh[order[i]];
   uh.insert(uh.end(), order.begin(), order.end());
   int64_t* ud = nullptr;
   CK(cudaMalloc(&ud, 2 * count * sizeof(int64_t)));
   cudaError_t e = cudaMemcpy(ud, uh.data(), 2 * count * sizeof(int64_t), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
-    e = cudaError_t(pcwd_vol::rows3d(n, levels, h, taps, m, u, v, ud, ud + count, count, out,
+    e = cudaError_t(pcwd_vol::rows3d(n, levels, h, taps, m, u, v, ud, ud + count, sorted_mu.data(), count, out,
                                      static_cast<cudaStream_t>(stream)));
   cudaFree(ud);
   if (e != cudaSuccess)

@@ -293,5 +293,5 @@ int finish(const double* U, const double* c, int d, int n, int R, int g, int m, 
 // volume.cu: the d = 3 variant — rows of Θ on the n³ torus (see the file header).  Returns a cudaError_t as int.
 namespace pcwd_vol {
 int rows3d(int n, int J, const double* h, int taps, int m, const double* u, const double* v, const int64_t* units,
-           const int64_t* order, int64_t count, double* out, cudaStream_t st);
+           const int64_t* order, const int64_t* sorted_mu, int64_t count, double* out, cudaStream_t st);
 }  // namespace pcwd_vol

@@ -66,7 +66,7 @@ __device__ void build_lists(const unsigned char (*mask)[256], int len, short (*l
 // One analysis step along axis `ax` of a cube of side s (power of two), out = a | d concatenated on that axis,
 // restricted to a product set: outputs (i0, i1, i2) ∈ L0 × L1 × L2 only, inputs read where `min` (the input's mask
 // along `ax`) is set — everything off the product set is an exact zero that is neither stored nor loaded.
-__device__ void analysis_pass(const Args& A, const double* __restrict__ x, double* __restrict__ y, int s, int ax,
+__device__ void analysis_pass(const Args& A, const double* x, double* y, int s, int ax,
                               const short* L0, int c0, const short* L1, int c1, const short* L2, int c2,
                               const unsigned char* min) {
   const int half = s >> 1, mask = s - 1;
@@ -105,7 +105,8 @@ __device__ __forceinline__ int64_t subband_offset(int n, int J, int lev, int e) 
   return off + (e - 1) * nl * nl * nl;
 }
 
-__global__ void __launch_bounds__(512) rows3d_kernel(const Args A) {
+template <int NT>
+__global__ void __launch_bounds__(NT) rows3d_kernel(const Args A) {
   const int n = A.n, J = A.J;
   const int64_t N = int64_t(n) * n * n;
   __shared__ unsigned char S[3][256];    // supp f_a
@@ -181,7 +182,6 @@ __global__ void __launch_bounds__(512) rows3d_kernel(const Args A) {
     double* row = A.out + ui * N;
     {
       const int mask = n - 1;
-      for (int64_t i = threadIdx.x; i < N; i += blockDim.x) row[i] = 0.0;
       for (int idx = threadIdx.x; idx < 3 * n; idx += blockDim.x) S[idx / n][idx % n] = f[idx / n][idx % n] != 0.0;
       __syncthreads();
       for (int idx = threadIdx.x; idx < 3 * n; idx += blockDim.x) {
@@ -269,10 +269,13 @@ __global__ void __launch_bounds__(512) rows3d_kernel(const Args A) {
   }
 }
 
-// units, order, u, v, out: DEVICE.  h: HOST.  Returns a cudaError_t as int (0 = success); synchronises `st` once (the
-// support box comes back to the host before the launch).
+// units, order, u, v, out: DEVICE.  h, sorted_mu (the Λ indices in `order`'s order, ascending): HOST.  Returns a
+// cudaError_t as int (0 = success); synchronises `st` (the support box comes back to the host before the launches).
+// Two launches side by side: the units whose 1-D supports cover at least half an axis (levels ≥ ℓ_c, the leading
+// entries of `order`) on 1024-thread CTAs, the fine ones — a few thousand outputs each, latency-bound — on many
+// 128-thread CTAs.
 int rows3d(int n, int J, const double* h, int taps, int m, const double* u, const double* v, const int64_t* units,
-           const int64_t* order, int64_t count, double* out, cudaStream_t st) {
+           const int64_t* order, const int64_t* sorted_mu, int64_t count, double* out, cudaStream_t st) {
   if (count == 0) return 0;
   Args A{};
   A.n = n; A.J = J; A.taps = taps; A.m = m;
@@ -281,10 +284,10 @@ int rows3d(int n, int J, const double* h, int taps, int m, const double* u, cons
     const int i = 2 - taps + j;                       // g[i] = (−1)^{1−i} h[1−i]
     A.g[j] = (((1 - i) & 1) ? -1.0 : 1.0) * h[1 - i];
   }
-  A.u = u; A.v = v; A.units = units; A.order = order; A.count = count; A.out = out;
+  A.u = u; A.v = v; A.units = units; A.out = out;
   const int64_t N = int64_t(n) * n * n;
   int* rad = nullptr;
-  cudaError_t e = cudaMalloc(&rad, 8 * sizeof(int));   // [0..2] support radii, [4..5] the unit counter
+  cudaError_t e = cudaMalloc(&rad, 8 * sizeof(int));   // [0..2] support radii, [4..5], [6..7] the two unit counters
   if (e != cudaSuccess) return int(e);
   int rh[3] = {0, 0, 0};
   e = cudaMemsetAsync(rad, 0, 8 * sizeof(int), st);
@@ -294,22 +297,57 @@ int rows3d(int n, int J, const double* h, int taps, int m, const double* u, cons
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) { cudaFree(rad); return int(e); }
-  A.next = reinterpret_cast<unsigned long long*>(rad + 4);
   for (int a = 0; a < 3; ++a) {
     const bool whole = 2 * rh[a] + 1 >= n;
     A.lo[a] = whole ? 0 : -rh[a];
     A.cnt[a] = whole ? n : 2 * rh[a] + 1;
   }
+  // ℓ_c: the first level whose dilated 1-D support (2^ℓ − 1)(taps − 1) + 1 + 2R reaches n/2; units of levels ≥ ℓ_c
+  // are exactly those with Λ index < (n >> (ℓ_c − 1))³ (the layout is coarse first).
+  const int R = std::max(rh[0], std::max(rh[1], rh[2]));
+  int lc = 1;
+  while (lc <= J && ((int64_t(1) << lc) - 1) * (taps - 1) + 1 + 2 * R < n / 2) ++lc;
+  const int64_t side = n >> (lc - 1), bound = lc > J ? 0 : side * side * side;
+  int64_t n_coarse = 0;
+  while (n_coarse < count && sorted_mu[n_coarse] < bound) ++n_coarse;
+  const int64_t n_fine = count - n_coarse;
   const int64_t per_cta = 2 * N * int64_t(sizeof(double));
-  int64_t ctas = std::min<int64_t>(count, 148 * 4);
-  ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t(2) << 30) / per_cta));
+  const int64_t cap = std::max<int64_t>(1, (int64_t(4) << 30) / per_cta);
+  const int64_t ctas_c = std::min<int64_t>(std::min<int64_t>(n_coarse, 148 * 2), cap);
+  const int64_t ctas_f = std::min<int64_t>(std::min<int64_t>(n_fine, 148 * 8), cap);
   double* scratch = nullptr;
-  e = cudaMalloc(&scratch, size_t(ctas * per_cta));
+  e = cudaMalloc(&scratch, size_t((ctas_c + ctas_f) * per_cta));
   if (e != cudaSuccess) { cudaFree(rad); return int(e); }
-  A.scratch = scratch;
-  rows3d_kernel<<<unsigned(ctas), 512, 0, st>>>(A);
-  e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev = nullptr;
+  e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMemsetAsync(out, 0, size_t(count) * N * sizeof(double), st);   // the rows' exact zeros
+  if (e == cudaSuccess) e = cudaEventRecord(ev, st);
+  if (e == cudaSuccess && n_coarse > 0) {
+    e = cudaStreamWaitEvent(s2, ev, 0);
+    Args C = A;
+    C.order = order; C.count = n_coarse; C.scratch = scratch;
+    C.next = reinterpret_cast<unsigned long long*>(rad + 4);
+    // few coarse units: ask for more than half an SM's shared memory so that every CTA gets an SM of its own
+    const size_t pad = n_coarse <= 148 ? size_t(120) << 10 : 0;
+    if (e == cudaSuccess && pad)
+      e = cudaFuncSetAttribute(rows3d_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pad));
+    if (e == cudaSuccess) rows3d_kernel<1024><<<unsigned(ctas_c), 1024, pad, s2>>>(C);
+    if (e == cudaSuccess) e = cudaGetLastError();
+  }
+  if (e == cudaSuccess && n_fine > 0) {
+    Args F = A;
+    F.order = order + n_coarse; F.count = n_fine; F.scratch = scratch + ctas_c * 2 * N;
+    F.next = reinterpret_cast<unsigned long long*>(rad + 6);
+    rows3d_kernel<128><<<unsigned(ctas_f), 128, 0, st>>>(F);
+    e = cudaGetLastError();
+  }
+  cudaError_t e2 = s2 ? cudaStreamSynchronize(s2) : cudaSuccess;
+  cudaError_t e1 = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = e1 != cudaSuccess ? e1 : e2;
+  if (ev) cudaEventDestroy(ev);
+  if (s2) cudaStreamDestroy(s2);
   cudaFree(scratch);
   cudaFree(rad);
   return int(e);
