@@ -244,8 +244,9 @@ int pcwd_columns(void* handle, const int64_t* lambdas, int64_t count, double* ou
  * levels J..1, orientations e = 4 e0 + 2 e1 + e2 = 1..7, positions row-major.  A handle-free call: n a power of two
  * ≤ 256; h: HOST, `taps` values of an orthogonal low-pass filter (else PCWD_E_CONFIG); u, v: DEVICE, m × n³ fp64,
  * u_k(z) at index z mod n, row-major (z0, z1, z2); units: HOST or DEVICE, `count` Λ indices in [0, n³) (else
- * PCWD_E_PARAM); out: DEVICE, count × n³ fp64 allocated by the caller (row i = row units[i] of Θ).  Computes in fp64
- * with whole-torus passes (no windowing); allocates and frees its scratch; synchronous. */
+ * PCWD_E_PARAM); out: DEVICE, count × n³ fp64 allocated by the caller (row i = row units[i] of Θ).  Computes in fp64,
+ * each pass only on the product set of per-axis supports its result can be nonzero on (exact zeros elsewhere);
+ * allocates and frees its scratch (≤ 4 GiB, else PCWD_E_OOM); synchronous. */
 int pcwd_rows3d(int32_t n, int32_t levels, const double* h, int32_t taps, int32_t m, const double* u, const double* v,
                 const int64_t* units, int64_t count, double* out, void* stream);
 

@@ -1,14 +1,16 @@
 // d = 3 variant: rows of Θ = Ψ* H Ψ on the periodic n × n × n grid.
 //
-// Row μ is Ψ*(H* ψ_μ) (R1; H* g = Σ_k v_k ⊙ (ũ_k ⋆ g), R9).  One CTA per unit, the unit's two n³ work arrays (the
-// analysis cascade's ping-pong) in a global scratch slice:
+// Row μ is Ψ*(H* ψ_μ) (R1; H* g = Σ_k v_k ⊙ (ũ_k ⋆ g), R9).  One CTA per unit, taken from a launch-wide counter, coarse
+// units first; the unit's two n³ work arrays (the analysis cascade's ping-pong) in a global scratch slice:
 //   1. ψ_μ = Ψ e_μ = f_0 ⊗ f_1 ⊗ f_2 (tensor-product basis): three 1-D synthesis cascades (P:94-96
 //      transposed) in shared memory;
-//   2. w(y) = Σ_k v_k(y) Σ_c u_k(c) ψ_μ((y + c) mod n) over the cyclic support box of the u_k, skipping the
-//      (x0, x1) lines on which ψ_μ is identically zero;
-//   3. c = Ψ* w by the analysis cascade, axis 0 first (R6 carried to three axes), written in the Λ layout
-//      (coarse block, levels J..1, orientations 4 e0 + 2 e1 + e2 = 1..7, positions row-major).
-// Whole-torus passes in fp64, no windowing: a plain variant path for small volumes, not the tuned d ≤ 2 pipeline.
+//   2. w(y) = Σ_k v_k(y) Σ_c u_k(c) ψ_μ((y + c) mod n) over the cyclic support box of the u_k, on O_0 × O_1 × O_2 only
+//      (O_a = supp f_a dilated by the box: supp w is inside this product set);
+//   3. c = Ψ* w by the analysis cascade, axis 0 first (R6 carried to three axes), every pass on the product set its
+//      outputs can be nonzero on (1-D masks pushed through the steps), written in the Λ layout (coarse block, levels
+//      J..1, orientations 4 e0 + 2 e1 + e2 = 1..7, positions row-major).
+// fp64.  Supports are tracked as data (no class geometry, templates, TMA staging or retention rule as in the d ≤ 2
+// pipeline): a variant path, see DESIGN.md §6b for what bounds it.
 #include <cuda_runtime.h>
 
 #include <algorithm>

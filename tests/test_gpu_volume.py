@@ -52,7 +52,8 @@ def test_every_unit(case):
     _compare("vol3_" + name, n, J, h, u, v, np.arange(n ** 3))
 
 
-SAMPLED = [("db3_n16_J3", 16, 3, 3, 3, 2, 21, 3), ("db4_n32_J2", 32, 2, 4, 2, 2, 22, 1), ("db2_n32_J5", 32, 5, 2, 3, 3, 23, 1)]
+SAMPLED = [("db3_n16_J3", 16, 3, 3, 3, 2, 21, 3), ("db4_n32_J2", 32, 2, 4, 2, 2, 22, 1), ("db2_n32_J5", 32, 5, 2, 3, 3, 23, 1),
+           ("db2_n32_J1_finelaunchonly", 32, 1, 2, 2, 1, 24, 2)]   # no unit reaches the coarse launch
 
 
 @pytest.mark.parametrize("case", SAMPLED, ids=[c[0] for c in SAMPLED])
