@@ -152,3 +152,20 @@ def test_corrupted_filter_rejected():
     h[3] += 1e-6
     assert P.validate(_spec(h=h)) == 2
     assert "h:" in P.lib().pcwd_last_error().decode()
+
+
+@pytest.mark.parametrize("kw,code", [(dict(n=6), 1), (dict(n=512), 1), (dict(levels=0), 2), (dict(levels=4), 2),
+                                     (dict(taps=3), 2), (dict(scale=1.01), 2), (dict(m=0), 3)])
+def test_rows3d_rejects_before_touching_cuda(kw, code):
+    """pcwd_rows3d (d = 3) validates the grid, the depth and the filter on the host (E_SHAPE / E_CONFIG / E_PARAM)
+    before any CUDA call."""
+    from synth.filters import daubechies
+    a = dict(n=8, levels=2, taps=4, scale=1.0, m=1)
+    a.update(kw)
+    h = np.ascontiguousarray(daubechies(2) * a["scale"])
+    dummy = np.zeros(8)
+    units = np.zeros(1, dtype=np.int64)
+    rc = P.lib().pcwd_rows3d(a["n"], a["levels"], ctypes.c_void_p(h.ctypes.data), a["taps"], a["m"],
+                             ctypes.c_void_p(dummy.ctypes.data), ctypes.c_void_p(dummy.ctypes.data),
+                             ctypes.c_void_p(units.ctypes.data), 1, ctypes.c_void_p(dummy.ctypes.data), ctypes.c_void_p(0))
+    assert rc == code, P.lib().pcwd_last_error().decode()
