@@ -48,6 +48,14 @@ __global__ void support_kernel(const double* u, int64_t total, int n, int* rad) 
   }
 }
 
+// q / d for q < 2^24, 1 ≤ d ≤ 256 by one multiply: M = ⌈2^32 / d⌉ overshoots q/d by < q / 2^32 < 1/256 ≤ 1/d, so the
+// floor is exact; d = 1 (M would be 2^32) is passed through.
+struct FastDiv {
+  unsigned M, d;
+  __device__ explicit FastDiv(int dd) : M(dd > 1 ? 0xFFFFFFFFu / unsigned(dd) + 1u : 0u), d(unsigned(dd)) {}
+  __device__ __forceinline__ unsigned div(unsigned q) const { return d > 1 ? __umulhi(q, M) : q; }
+};
+
 // Index lists of three 1-D masks (one warp per axis, ballot compaction); all threads of the CTA call it.
 __device__ void build_lists(const unsigned char (*mask)[256], int len, short (*list)[256], int* cnt) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -74,8 +82,10 @@ __device__ void analysis_pass(const Args& A, const double* x, double* y, int s, 
   const int half = s >> 1, mask = s - 1;
   const int stride = ax == 0 ? s * s : (ax == 1 ? s : 1);
   const int total = c0 * c1 * c2;
+  const FastDiv d2(c2), d1(c1);
   for (int q = threadIdx.x; q < total; q += blockDim.x) {
-    const int i2 = L2[q % c2], i1 = L1[(q / c2) % c1], i0 = L0[q / (c2 * c1)];
+    const unsigned t = d2.div(q), j0 = d1.div(t);
+    const int i2 = L2[q - t * c2], i1 = L1[t - j0 * c1], i0 = L0[j0];
     const int idx = (i0 * s + i1) * s + i2;
     const int i = ax == 0 ? i0 : (ax == 1 ? i1 : i2);
     const double* line = x + (idx - i * stride);
@@ -195,8 +205,10 @@ __global__ void __launch_bounds__(NT) rows3d_kernel(const Args A) {
       __syncthreads();
       build_lists(M, n, LM, cM);
       const int c0 = cM[0], c1 = cM[1], c2 = cM[2];
+      const FastDiv d2(c2), d1(c1);
       for (int q = threadIdx.x; q < c0 * c1 * c2; q += blockDim.x) {
-        const int y2 = LM[2][q % c2], y1 = LM[1][(q / c2) % c1], y0 = LM[0][q / (c2 * c1)];
+        const unsigned t = d2.div(q), j0 = d1.div(t);
+        const int y2 = LM[2][q - t * c2], y1 = LM[1][t - j0 * c1], y0 = LM[0][j0];
         const int y = (y0 * n + y1) * n + y2;
         double acc = 0.0;
         for (int k = 0; k < A.m; ++k) {
@@ -248,8 +260,10 @@ __global__ void __launch_bounds__(NT) rows3d_kernel(const Args A) {
         const int64_t base = subband_offset(n, J, lv, 1);
         const int64_t cube = int64_t(nl) * nl * nl;
         const int c0 = cP[0], c1 = cP[1], c2 = cP[2];
+        const FastDiv d2(c2), d1(c1);
         for (int q = threadIdx.x; q < c0 * c1 * c2; q += blockDim.x) {
-          const int i2 = LP[2][q % c2], i1 = LP[1][(q / c2) % c1], i0 = LP[0][q / (c2 * c1)];
+          const unsigned t = d2.div(q), j0 = d1.div(t);
+          const int i2 = LP[2][q - t * c2], i1 = LP[1][t - j0 * c1], i0 = LP[0][j0];
           const int e = (i0 >= nl ? 4 : 0) | (i1 >= nl ? 2 : 0) | (i2 >= nl ? 1 : 0);
           const int pos = ((i0 % nl) * nl + (i1 % nl)) * nl + (i2 % nl);
           const double val = X[(i0 * s + i1) * s + i2];
